@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the LiDAR first-return cast hot path (FGGS-LiDAR, arXiv 2509.17390 §IV-C) on B200.
+
+One step = one pass of the whole hot path of SURVEY.md §8(a) over one batch of synthetic input:
+  A1 mesh upload + validation (device-resident mesh -> scene copy), A2-A7 LBVH build (centroids,
+  Morton codes, radix sort, Karras tree, refit, leaf-order records, nodes), A8-A11 cast of every
+  beam of every pose in the batch (raygen, traversal, watertight test, range/tri_id write) and,
+  for N > 1, A12 the NCCL all-gather of the results.
+Default workload (BASELINE.json configs[1], SURVEY C2 throughput mode): procedural indoor rooms
+(~1.0 M triangles), HDL64-style 64 x 2048 spinning pattern, 64 yaw-offset poses per GPU per step.
+
+Prints ONE JSON line (rank 0). `--impl reference` times the CPU oracle (the reference arm for
+this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["fgl", "reference"], default="fgl")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--poses", type=int, default=None, help="poses per GPU per step")
+    ap.add_argument("--mode", choices=["full", "cast"], default="full",
+                    help="full = upload+build+cast per step (default); cast = cast only on a prebuilt scene")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle baseline")
+    return ap.parse_args()
+
+
+METRIC = "rays/sec (LiDAR first-return cast, full hot path per step)"
+DEFAULT_POSES = {"C1": 1, "C2": 64, "C3": 1, "C4": 1000, "C5": 512}
+
+
+def _workload(name: str, poses_per_rank: int, world: int, rank: int):
+    import synth
+    if name in ("C2",):
+        cfg = synth.config("C2", poses=poses_per_rank * world)
+    elif name == "C4":
+        cfg = synth.config("C4", poses=poses_per_rank * world)
+    elif name == "C5":
+        cfg = synth.config("C5", poses=poses_per_rank * world)
+    else:
+        cfg = synth.config(name)
+        cfg["poses"] = np.concatenate([cfg["poses"]] * (poses_per_rank * world))
+    P = poses_per_rank
+    cfg["poses_rank"] = cfg["poses"][rank * P:(rank + 1) * P]
+    return cfg
+
+
+def _describe(cfg, P, world):
+    pat = cfg["pattern"]
+    if hasattr(pat, "elev_deg"):
+        pdesc = f"{pat.name} {pat.channels}x{pat.columns} spinning"
+    else:
+        pdesc = f"rosette {pat.points_per_frame} pts/frame"
+    return f"{cfg['name']}: {cfg['mesh'].meta.get('kind')} {cfg['mesh'].T} tris, {pdesc}, {P} poses/GPU/step"
+
+
+# ----------------------------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampler running during the timed region (clocks + throttle reasons)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for k, n in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(rows), "reasons": sorted(reasons)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic(config: str):
+    """dram read+write bytes per launch of the cast kernel from the committed ncu summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            s = json.load(f)
+        return s[config]["k_cast"]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------------------------
+def _cpu_baseline(cfg, seconds: float):
+    """The oracle (CPU double brute force, Eq. 20 by the naive scan P:291-294), as it stands, on a
+    bounded seeded sample of the workload's rays, on this host's cores."""
+    import oracle
+    m, pat = cfg["mesh"], cfg["pattern"]
+    o, d = oracle.pattern_rays(pat, cfg["poses_rank"][:1])
+    rng = np.random.default_rng(0)
+    probe = 64
+    idx = rng.choice(o.shape[0], probe, replace=False)
+    t0 = time.perf_counter()
+    oracle.cast(m.verts, m.tris, o[idx], d[idx], pat.t_min, pat.t_max)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    n = int(min(o.shape[0], max(probe, probe * seconds / dt)))
+    idx = rng.choice(o.shape[0], n, replace=False)
+    t0 = time.perf_counter()
+    oracle.cast(m.verts, m.tris, o[idx], d[idx], pat.t_min, pat.t_max)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
+            "sample": f"{n} seeded rays of pose 0 of {cfg['name']} vs all {m.T} triangles "
+                      f"({n * m.T:.3g} double MT tests, {dt:.1f} s)"}
+
+
+def run_reference(a):
+    """--impl reference: the oracle on the host cores, each step a bounded sample of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    P = a.poses or DEFAULT_POSES[a.config]
+    cfg = _workload(a.config, P, 1, 0)
+    m, pat = cfg["mesh"], cfg["pattern"]
+    o, d = oracle.pattern_rays(pat, cfg["poses_rank"][:1])
+    rng = np.random.default_rng(1)
+    # size each step to ~1.5 s of CPU work so W + K steps finish in a few minutes
+    t0 = time.perf_counter()
+    oracle.cast(m.verts, m.tris, o[:64], d[:64], pat.t_min, pat.t_max)
+    per_ray = (time.perf_counter() - t0) / 64
+    n = int(max(8, min(o.shape[0], 1.5 / max(per_ray, 1e-9))))
+    for _ in range(a.warmup):
+        idx = rng.choice(o.shape[0], n, replace=False)
+        oracle.cast(m.verts, m.tris, o[idx], d[idx], pat.t_min, pat.t_max)
+    times = []
+    for _ in range(a.steps):
+        idx = rng.choice(o.shape[0], n, replace=False)
+        t0 = time.perf_counter()
+        oracle.cast(m.verts, m.tris, o[idx], d[idx], pat.t_min, pat.t_max)
+        times.append(time.perf_counter() - t0)
+    ms = 1000 * statistics.mean(times)
+    v = n / (ms / 1000)
+    line = {"metric": METRIC, "value": v, "unit": "rays/s", "n_gpus": 0,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": _describe(cfg, P, 1), "sample_rays_per_step": n, "triangles": m.T},
+            "cpu_baseline": {"value": v, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
+                             "sample": f"{n} seeded rays per step of {a.config} pose 0 vs all {m.T} triangles"},
+            "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------------------------
+def main():
+    a = _args()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_17390_b200 as fgl
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.gpus != world and world > 1:
+        print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = a.poses or DEFAULT_POSES[a.config]
+    cfg = _workload(a.config, P, world, rank)
+    m, pat = cfg["mesh"], cfg["pattern"]
+    rays_per_pose = fgl.rays_per_pose(pat)
+    rays_rank = P * rays_per_pose
+    verts_d = torch.from_numpy(m.verts).to(dev)
+    tris_d = torch.from_numpy(m.tris).to(dev)
+    poses_d = torch.from_numpy(np.ascontiguousarray(cfg["poses_rank"])).to(dev)
+    stream = torch.cuda.current_stream()
+    scene = fgl.Scene(verts_d, tris_d, device=dev)
+    out = scene.cast(poses_d, pat)
+    shape = tuple(out["range"].shape)
+    gather = None
+    if world > 1:
+        g_rng = torch.empty((world,) + shape, dtype=torch.float32, device=dev)
+        g_tid = torch.empty((world,) + shape, dtype=torch.int32, device=dev)
+        gather = (g_rng, g_tid)
+    flush = None if a.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step(cast_ev=None):
+        if a.mode == "full":
+            scene.upload(verts_d, tris_d)        # A1 (D2D copy + validation)
+            scene.build()                        # A2-A7
+        if cast_ev:
+            cast_ev[0].record(stream)
+        scene.cast(poses_d, pat, out=out)        # A8-A11
+        if cast_ev:
+            cast_ev[1].record(stream)
+        if gather is not None:                   # A12
+            dist.all_gather_into_tensor(gather[0], out["range"])
+            dist.all_gather_into_tensor(gather[1], out["tri_id"])
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    K = a.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = fgl.kernel_launches()
+    with Clocks(local) as clk:
+        for i in range(K):
+            if flush is not None:
+                flush.zero_()                    # evict L2 between timed steps (not timed)
+            ev[i][0].record(stream)
+            step(cev[i])
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    launches = fgl.kernel_launches() - launches0
+    step_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    cast_ms = [e[0].elapsed_time(e[1]) for e in cev]
+    ms = statistics.mean(step_ms)
+    cms = statistics.mean(cast_ms)
+    if world > 1:
+        t = torch.tensor([ms, cms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, cms = t.tolist()
+    clocks = clk.summary()
+
+    # --- Eq. 21 counters on the same rays (COUNT variant, untimed) -> algorithmic bytes ------
+    cres = scene.cast(poses_d, pat, counts=True)
+    n_nodes = cres["node_counts"].double().mean().item()
+    n_tris = cres["tri_counts"].double().mean().item()
+    bytes_per_ray = 64.0 * n_nodes + 48.0 * n_tris + 8.0
+    peak, peak_kind = _peaks()
+    achieved = bytes_per_ray * rays_rank / (cms / 1000) / 1e9
+    traffic = _ncu_traffic(a.config)
+
+    # --- e2e through the public API with host buffers --------------------------------------
+    e2e = None
+    if not a.no_e2e:
+        vh = torch.from_numpy(m.verts).pin_memory()
+        th = torch.from_numpy(m.tris).pin_memory()
+        ph = torch.from_numpy(np.ascontiguousarray(cfg["poses_rank"])).pin_memory()
+        rh = torch.empty(shape, dtype=torch.float32).pin_memory()
+        ih = torch.empty(shape, dtype=torch.int32).pin_memory()
+        pd = torch.empty_like(poses_d)
+        sc2 = fgl.Scene(device=dev)
+
+        def e2e_step():
+            sc2.upload(vh, th)                               # H2D mesh (pinned) + validation
+            pd.copy_(ph, non_blocking=True)                  # H2D poses
+            sc2.build()
+            r = sc2.cast(pd, pat)
+            rh.copy_(r["range"], non_blocking=True)          # D2H results
+            ih.copy_(r["tri_id"], non_blocking=True)
+
+        for _ in range(max(2, a.warmup // 2)):
+            e2e_step()
+        torch.cuda.synchronize()
+        ke = max(3, K // 2)
+        eev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ke)]
+        for i in range(ke):
+            if flush is not None:
+                flush.zero_()
+            eev[i][0].record(stream)
+            e2e_step()
+            eev[i][1].record(stream)
+        torch.cuda.synchronize()
+        ems = statistics.mean(e[0].elapsed_time(e[1]) for e in eev)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": rays_rank * world / (ems / 1000), "unit": "rays/s",
+               "h2d_bytes_per_step": int(m.verts.nbytes + m.tris.nbytes + cfg["poses_rank"].nbytes),
+               "d2h_bytes_per_step": int(rh.numel() * 4 + ih.numel() * 4), "ms_per_step": ems}
+        del sc2
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = _cpu_baseline(cfg, a.cpu_seconds)
+
+    if rank == 0:
+        st = scene.stats()
+        total_rays = rays_rank * world
+        line = {
+            "metric": METRIC,
+            "value": total_rays / (ms / 1000), "unit": "rays/s", "n_gpus": world, "steps": K, "warmup": a.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": _describe(cfg, P, world), "step": "upload+build+cast" + ("+allgather" if world > 1 else "")
+                       if a.mode == "full" else "cast only (prebuilt scene)",
+                       "triangles": m.T, "rays_per_step": total_rays, "poses_per_step": P * world,
+                       "l2": "flushed between steps (256 MiB memset, untimed)" if flush is not None else "not flushed",
+                       "parallelism": f"dp{world} (poses sharded, mesh replicated)"},
+            "frames_per_s": P * world / (ms / 1000),
+            "cast_rays_per_s": total_rays / (cms / 1000), "cast_ms": cms, "build_ms": st["build_ms"],
+            "nodes_per_ray": n_nodes, "tris_per_ray": n_tris,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_cast",
+                         "note": f"algorithmic bytes/ray = 64*nodes + 48*tris + 8 = {bytes_per_ray:.0f} B; "
+                                 f"peak {peak_kind} (MEASURED_PEAKS.json hbm_gbs); cast time from CUDA events "
+                                 f"on the launch stream"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

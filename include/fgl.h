@@ -1,0 +1,176 @@
+/*
+ * fgl.h — C ABI of libfgl.so, the B200 (sm_100a) LiDAR first-return ray caster.
+ *
+ * The operation exposed is the nearest-hit LiDAR measurement of PAPER.md §IV-C
+ * (arXiv 2509.17390, "Ray-casting for LiDAR Simulation"):
+ *   beam j of a sensor with pose T_s = (R_s | t_s) in SE(3) is the ray r_j(t) = x_s + t d_j,
+ *   x_s := t_s, d_j a unit direction from the scanning pattern (Eq. 19);
+ *   its return is t_j* = min { tau(r_j, tri_k) : 1 <= k <= T, tau in [t_min, t_max] } over the
+ *   triangle mesh M = {tri_k} (Eq. 20), range rho_j = t_j* since ||d_j|| = 1.
+ * The acceleration structure is the LBVH of §IV-A: Morton codes (Eq. 5), radix sort,
+ * LCP-split radix tree (Eq. 6), bottom-up bound union (Eq. 7), applied to triangle centroids.
+ *
+ * Conventions shared by every call
+ *   - All pointers are plain host or device pointers; the library never frees or retains a
+ *     caller pointer after the call returns (output buffers belong to the caller).
+ *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream). Work is enqueued on it and
+ *     the call returns without synchronising, except where a call says it synchronises.
+ *   - Argument errors are detected synchronously and return FGL_E_USAGE / FGL_E_DATA before any
+ *     work is enqueued. The message of the last failing call on the calling thread is
+ *     available from fgl_last_error().
+ *   - A miss is range = +INF and tri_id = -1. tri_id is the triangle's index in the uploaded
+ *     mesh. Ties at equal t go to the smaller tri_id (reading R4).
+ *   - The interval [t_min, t_max] is closed (R3). Triangles are two-sided (R2). Degenerate
+ *     (zero-area) triangles are never hit (R16).
+ *   - A built scene is immutable: casts on different streams may run concurrently (up to 64 in
+ *     flight per scene). upload/build must not overlap casts on the same scene.
+ */
+#ifndef FGL_H
+#define FGL_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FGL_API __attribute__((visibility("default")))
+#else
+#define FGL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FGL_OK = 0,
+    FGL_E_USAGE = 1,    /* bad argument, NULL pointer, cast before build                     */
+    FGL_E_DATA = 2,     /* T = 0, index out of range, NaN/Inf vertex                          */
+    FGL_E_RESOURCE = 3, /* out of device memory                                              */
+    FGL_E_CUDA = 4      /* any CUDA runtime error; the message carries cudaGetErrorString    */
+} fgl_status;
+
+enum { FGL_HOST = 0, FGL_DEVICE = 1 };
+
+typedef struct fgl_scene fgl_scene; /* opaque: device copies of the mesh, the BVH and scratch */
+
+typedef struct {
+    int32_t morton_bits; /* b of Eq. 5, 1..21; 0 = default 21 (63-bit keys)      */
+    int32_t leaf_size;   /* max triangles per BVH leaf, 1..8; 0 = default (4)                 */
+    int32_t reserved[6]; /* must be zero                                                     */
+} fgl_build_opts;
+
+typedef struct {
+    int64_t triangles, vertices;
+    int64_t nodes;        /* internal nodes of the binary LBVH (T - 1, or 1 when T = 1)       */
+    int64_t device_bytes; /* device memory owned by the scene                                 */
+    float scene_lo[3], scene_hi[3]; /* Morton scene box [o, o + L] (centroid bounds)   */
+    float build_ms;       /* device time of the last build (synchronises on its end event)   */
+    int32_t morton_bits, leaf_size;
+} fgl_stats;
+
+/* Spinning multi-beam pattern (R11, R12). Channel c has elevation
+ * elev_deg[c] (host array, degrees, monotone); column a has azimuth 2*pi*a/columns + az0
+ * (counter-clockwise from sensor +x). Sensor frame: x forward, y left, z up. Ray (p, c, a) is
+ * stored at p*channels*columns + c*columns + a. 1 <= channels <= 512, columns >= 1. */
+typedef struct {
+    int32_t channels, columns;
+    const float *elev_deg;
+    float az0_deg, t_min, t_max;
+} fgl_spinning;
+
+/* Two-prism (Livox-style) non-repetitive pattern (R20; the paper is silent). Sample
+ * n = frame*points_per_frame + k has exact 32-bit phases phi1 = n*inc1 mod 2^32,
+ * phi2 = phase2_0 - n*inc2 mod 2^32 (turns * 2^32). Ray (p, k) is stored at p*N + k. */
+typedef struct {
+    int32_t points_per_frame;
+    uint32_t inc1, inc2, phase2_0;
+    float half_fov_deg, t_min, t_max;
+} fgl_rosette;
+
+/* ---- scene lifetime -------------------------------------------------------------------- */
+FGL_API fgl_status fgl_scene_create(int cuda_device, fgl_scene **out);
+FGL_API void fgl_scene_destroy(fgl_scene *scene);
+
+/* Copy the mesh M = {tri_k} into scene-owned device memory and validate it:
+ * verts: float32 [V][3]; tris: int32 [T][3], 0 <= index < V. ptr_kind says whether both pointers
+ * are FGL_HOST or FGL_DEVICE. Synchronises `cuda_stream` to report FGL_E_DATA (T = 0, an index out
+ * of range, a non-finite vertex). Invalidates any previous build. T must be < 2^28. */
+FGL_API fgl_status fgl_scene_upload_mesh(fgl_scene *scene, const float *verts, int64_t V, const int32_t *tris,
+                                 int64_t T, int ptr_kind, void *cuda_stream);
+
+/* LBVH build, §IV-A, on the device, enqueued on `cuda_stream`:
+ * centroids + scene box -> Morton codes (Eq. 5) -> stable LSD radix sort -> Karras radix tree
+ * (Eq. 6) -> bottom-up refit (Eq. 7) -> triangle records reordered into leaf order -> traversal
+ * nodes. opts may be NULL (defaults). Does no host synchronisation. */
+FGL_API fgl_status fgl_scene_build(fgl_scene *scene, const fgl_build_opts *opts, void *cuda_stream);
+
+/* Fills *out. Synchronises on the last build's end event (for build_ms and the scene box). */
+FGL_API fgl_status fgl_scene_stats(fgl_scene *scene, fgl_stats *out);
+
+/* ---- casts (Eqs. 19-20) ---------------------------------------------------------------- */
+/* poses: device float32 [P][3][4] row-major (R | t), sensor -> world (R13). Directions are
+ * normalised after rotation. range: device float32 [P][channels][columns]; tri_id: device int32,
+ * same shape; hit_xyz: NULL or device float32 [..][3] (x* = x_s + t* d).
+ * node_counts / tri_counts: NULL, or device int32 per ray: BVH nodes visited and triangles tested
+ * (the N_nodes(r_j) and K_j of Eq. 21). */
+FGL_API fgl_status fgl_cast_spinning(const fgl_scene *scene, const fgl_spinning *pattern, const float *poses, int64_t P,
+                             float *range, int32_t *tri_id, float *hit_xyz, int32_t *node_counts,
+                             int32_t *tri_counts, void *cuda_stream);
+
+/* Rosette: poses[p] is frame first_frame + p; outputs [P][points_per_frame]. */
+FGL_API fgl_status fgl_cast_rosette(const fgl_scene *scene, const fgl_rosette *pattern, const float *poses, int64_t P,
+                            int64_t first_frame, float *range, int32_t *tri_id, float *hit_xyz,
+                            int32_t *node_counts, int32_t *tri_counts, void *cuda_stream);
+
+/* Explicit rays (SPEC first_hit): orig, dir device float32 [R][3]; t is the ray parameter
+ * (equal to the range when ||dir|| = 1). 0 <= t_min < t_max. */
+FGL_API fgl_status fgl_cast_rays(const fgl_scene *scene, const float *orig, const float *dir, int64_t R, float t_min,
+                         float t_max, float *range, int32_t *tri_id, void *cuda_stream);
+
+/* The naive O(N_r T) cast of P:291-294 on the GPU (no BVH; needs only an uploaded mesh), with the
+ * same watertight test and tie-break as the BVH cast. A parity bridge and a baseline. */
+FGL_API fgl_status fgl_cast_rays_bruteforce(const fgl_scene *scene, const float *orig, const float *dir, int64_t R,
+                                    float t_min, float t_max, float *range, int32_t *tri_id, void *cuda_stream);
+
+/* Write the exact float32 rays (origin, unit direction) the cast kernels generate for a pattern,
+ * device float32 [R][3] each, in the cast's output order. */
+FGL_API fgl_status fgl_export_rays_spinning(const fgl_spinning *pattern, const float *poses, int64_t P, float *orig,
+                                    float *dir, void *cuda_stream);
+FGL_API fgl_status fgl_export_rays_rosette(const fgl_rosette *pattern, const float *poses, int64_t P, int64_t first_frame,
+                                   float *orig, float *dir, void *cuda_stream);
+
+/* ---- LBVH internals, for parity tests (host destination pointers; each may be NULL) ----- */
+typedef struct {
+    float *scene_box;      /* [6]  lo.xyz, hi.xyz                                              */
+    uint64_t *codes;       /* [T]  Morton codes in input order (Eq. 5)                          */
+    uint64_t *sorted_keys; /* [T]  codes after the stable sort                                  */
+    uint32_t *perm;        /* [T]  input triangle index at each sorted position                 */
+    int32_t *child;        /* [T-1][2] radix tree (Eq. 6): internal i, or leaf j encoded as ~j  */
+    int32_t *range;        /* [T-1][2] first, last sorted position covered by internal node i    */
+    float *leaf_box;       /* [T][6]   exact AABB of the triangle at sorted position j          */
+    float *node_box;       /* [T-1][6] Eq. 7 union                                              */
+    float *tri48;          /* [T][12]  leaf-order triangle records {v0, id}, {v1, 0}, {v2, 0}    */
+    float *nodes;          /* [max(T-1,1)][16] traversal nodes (DESIGN.md §5 "node64")          */
+} fgl_export;
+
+/* Synchronously copies the requested build arrays of a built scene to host memory. */
+FGL_API fgl_status fgl_scene_export(const fgl_scene *scene, const fgl_export *out, void *cuda_stream);
+
+/* Stand-alone build steps on caller device buffers (enqueued on cuda_stream):
+ * Eq. 5 Morton codes of n points (device float32 [n][3]) in the box [lo, hi] (host float[3]). */
+FGL_API fgl_status fgl_morton_codes(const float *points, int64_t n, const float *lo, const float *hi, int32_t bits,
+                            uint64_t *codes, void *cuda_stream);
+/* Stable LSD radix sort of (key, value) pairs in place, on the low key_bits bits of the keys
+ * (1..64). Allocates its scratch with cudaMallocAsync on the stream. */
+FGL_API fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key_bits, void *cuda_stream);
+
+/* ---- misc ----------------------------------------------------------------------------- */
+FGL_API const char *fgl_last_error(void); /* thread-local; valid until the next fgl call on the thread */
+FGL_API const char *fgl_version(void);
+FGL_API int32_t fgl_abi_version(void);   /* bumped on any incompatible change of this header */
+/* Number of kernels libfgl has launched in this process (all devices, all threads). */
+FGL_API int64_t fgl_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FGL_H */

@@ -1,0 +1,473 @@
+// C ABI of libfgl.so (include/fgl.h): argument validation, scene lifetime, error reporting, and
+// the orchestration of the build and cast kernels on the caller's stream.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/fgl.h"
+#include "fgl_internal.cuh"
+
+using fgl::Error;
+
+namespace fgl {
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace fgl
+
+struct fgl_scene {
+    int dev = 0;
+    int64_t V = 0, T = 0, cap_T = 0, cap_V = 0;
+    float *verts = nullptr;
+    int32_t *tris = nullptr;
+    unsigned int *vflag = nullptr;  // validation flag
+    unsigned int *hflag = nullptr;  // pinned host copy
+    fgl::BuildBuffers b;
+    fgl::CastCounter *counters = nullptr;
+    std::atomic<uint32_t> slot{0};
+    bool built = false;
+    int bits = 21, leaf_size = 4;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    size_t bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+fgl_status fail(int code, const std::string &msg) {
+    g_err = msg;
+    return (fgl_status)code;
+}
+
+#define FGL_API_BEGIN try {
+#define FGL_API_END                                                   \
+    }                                                                 \
+    catch (const fgl::Error &e) {                                     \
+        return fail(e.code, e.what());                                \
+    }                                                                 \
+    catch (const std::exception &e) {                                 \
+        return fail(FGL_E_RESOURCE, e.what());                        \
+    }                                                                 \
+    return FGL_OK;
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        FGL_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) FGL_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <class T>
+void dalloc(fgl_scene *s, T **p, size_t n) {
+    if (*p) {
+        cudaFree(*p);
+        *p = nullptr;
+    }
+    if (n == 0) n = 1;
+    FGL_CUDA(cudaMalloc((void **)p, n * sizeof(T)));
+    s->bytes += n * sizeof(T);
+}
+
+void free_build(fgl_scene *s) {
+    fgl::BuildBuffers &b = s->b;
+    void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.counts,
+                  b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes};
+    for (void *p : ps)
+        if (p) cudaFree(p);
+    b = fgl::BuildBuffers();
+}
+
+void alloc_build(fgl_scene *s, int64_t T) {
+    free_build(s);
+    s->bytes = 0;
+    fgl::BuildBuffers &b = s->b;
+    b.T = T;
+    const int64_t nin = std::max<int64_t>(T - 1, 1);
+    dalloc(s, &b.cent, T);
+    dalloc(s, &b.box, 8);
+    dalloc(s, &b.partial, fgl::kPrepBlocks * 6);
+    dalloc(s, &b.sync, 4);
+    FGL_CUDA(cudaMemset(b.sync, 0, 4 * sizeof(unsigned int)));
+    dalloc(s, &b.keys[0], T);
+    dalloc(s, &b.keys[1], T);
+    dalloc(s, &b.vals[0], T);
+    dalloc(s, &b.vals[1], T);
+    dalloc(s, &b.ghist, 8 * 256);
+    dalloc(s, &b.counts, (size_t)256 * fgl::sort_tile_blocks(T));
+    dalloc(s, &b.tri, 3 * T);
+    dalloc(s, &b.child, nin);
+    dalloc(s, &b.range, nin);
+    dalloc(s, &b.parent, 2 * T);
+    dalloc(s, &b.flags, nin);
+    dalloc(s, &b.leafbox, 2 * T);
+    dalloc(s, &b.nodebox, 2 * nin);
+    dalloc(s, &b.nodes, nin);
+}
+
+fgl::SceneView view(const fgl_scene *s) { return fgl::SceneView{s->b.tri, s->b.nodes}; }
+
+fgl::CastCounter *next_counter(const fgl_scene *s) {
+    auto *ms = const_cast<fgl_scene *>(s);
+    uint32_t k = ms->slot.fetch_add(1, std::memory_order_relaxed) % fgl::kCounterSlots;
+    return s->counters + k;
+}
+
+void check_interval(float t_min, float t_max) {
+    if (!(t_min >= 0.f) || !(t_max > t_min) || std::isnan(t_max))
+        throw Error(FGL_E_USAGE, "need 0 <= t_min < t_max");
+}
+
+void check_built(const fgl_scene *s) {
+    if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    if (!s->built) throw Error(FGL_E_USAGE, "scene is not built (call fgl_scene_build first)");
+}
+
+fgl::SpinParams spin_params(const fgl_spinning *p) {
+    if (!p) throw Error(FGL_E_USAGE, "pattern is NULL");
+    if (p->channels < 1 || p->channels > 512) throw Error(FGL_E_USAGE, "channels must be in [1, 512]");
+    if (p->columns < 1) throw Error(FGL_E_USAGE, "columns must be >= 1");
+    if (!p->elev_deg) throw Error(FGL_E_USAGE, "elev_deg is NULL");
+    check_interval(p->t_min, p->t_max);
+    bool inc = true, dec = true;
+    for (int c = 0; c < p->channels; ++c) {
+        if (!std::isfinite(p->elev_deg[c]) || std::fabs(p->elev_deg[c]) > 90.f)
+            throw Error(FGL_E_USAGE, "elevations must be finite degrees in [-90, 90]");
+        if (c) {
+            inc = inc && p->elev_deg[c] >= p->elev_deg[c - 1];
+            dec = dec && p->elev_deg[c] <= p->elev_deg[c - 1];
+        }
+    }
+    if (!inc && !dec) throw Error(FGL_E_USAGE, "elevations must be monotone (S:454)");
+    if (!std::isfinite(p->az0_deg)) throw Error(FGL_E_USAGE, "az0_deg must be finite");
+    fgl::SpinParams sp;
+    memset(&sp, 0, sizeof(sp));
+    sp.channels = p->channels, sp.columns = p->columns;
+    sp.az0_deg = p->az0_deg, sp.t_min = p->t_min, sp.t_max = p->t_max;
+    memcpy(sp.elev_deg, p->elev_deg, sizeof(float) * p->channels);
+    return sp;
+}
+
+fgl::RosetteParams rosette_params(const fgl_rosette *p, int64_t first_frame) {
+    if (!p) throw Error(FGL_E_USAGE, "pattern is NULL");
+    if (p->points_per_frame < 1) throw Error(FGL_E_USAGE, "points_per_frame must be >= 1");
+    if (!(p->half_fov_deg > 0.f && p->half_fov_deg <= 90.f)) throw Error(FGL_E_USAGE, "half_fov_deg must be in (0, 90]");
+    if (first_frame < 0) throw Error(FGL_E_USAGE, "first_frame must be >= 0");
+    check_interval(p->t_min, p->t_max);
+    fgl::RosetteParams r;
+    r.n = p->points_per_frame;
+    r.inc1 = p->inc1, r.inc2 = p->inc2, r.phase2_0 = p->phase2_0;
+    r.half_fov_deg = p->half_fov_deg, r.t_min = p->t_min, r.t_max = p->t_max;
+    r.first_frame = first_frame;
+    return r;
+}
+
+fgl::CastOut cast_out(float *range, int32_t *tri_id, float *hit, int32_t *nc, int32_t *tc) {
+    if (!range || !tri_id) throw Error(FGL_E_USAGE, "range / tri_id output is NULL");
+    return fgl::CastOut{range, tri_id, hit, nc, tc};
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *fgl_last_error(void) { return g_err.c_str(); }
+const char *fgl_version(void) { return "fgl 0.1.0 (sm_100a)"; }
+int32_t fgl_abi_version(void) { return 1; }
+int64_t fgl_kernel_launches(void) { return fgl::g_launches.load(std::memory_order_relaxed); }
+
+fgl_status fgl_scene_create(int cuda_device, fgl_scene **out) {
+    FGL_API_BEGIN
+    if (!out) throw Error(FGL_E_USAGE, "out is NULL");
+    *out = nullptr;
+    int n = 0;
+    FGL_CUDA(cudaGetDeviceCount(&n));
+    if (cuda_device < 0 || cuda_device >= n) throw Error(FGL_E_USAGE, "no such CUDA device");
+    DeviceGuard g(cuda_device);
+    fgl_scene *s = new fgl_scene();
+    s->dev = cuda_device;
+    try {
+        FGL_CUDA(cudaMalloc((void **)&s->counters, sizeof(fgl::CastCounter) * fgl::kCounterSlots));
+        FGL_CUDA(cudaMemset(s->counters, 0, sizeof(fgl::CastCounter) * fgl::kCounterSlots));
+        FGL_CUDA(cudaMalloc((void **)&s->vflag, sizeof(unsigned int)));
+        FGL_CUDA(cudaMallocHost((void **)&s->hflag, sizeof(unsigned int)));
+        FGL_CUDA(cudaEventCreate(&s->ev0));
+        FGL_CUDA(cudaEventCreate(&s->ev1));
+    } catch (...) {
+        fgl_scene_destroy(s);
+        throw;
+    }
+    *out = s;
+    FGL_API_END
+}
+
+void fgl_scene_destroy(fgl_scene *s) {
+    if (!s) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(s->dev);
+    free_build(s);
+    if (s->verts) cudaFree(s->verts);
+    if (s->tris) cudaFree(s->tris);
+    if (s->counters) cudaFree(s->counters);
+    if (s->vflag) cudaFree(s->vflag);
+    if (s->hflag) cudaFreeHost(s->hflag);
+    if (s->ev0) cudaEventDestroy(s->ev0);
+    if (s->ev1) cudaEventDestroy(s->ev1);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete s;
+}
+
+fgl_status fgl_scene_upload_mesh(fgl_scene *s, const float *verts, int64_t V, const int32_t *tris, int64_t T,
+                                 int ptr_kind, void *stream) {
+    FGL_API_BEGIN
+    if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    if (ptr_kind != FGL_HOST && ptr_kind != FGL_DEVICE) throw Error(FGL_E_USAGE, "ptr_kind must be FGL_HOST or FGL_DEVICE");
+    if (T <= 0) throw Error(FGL_E_DATA, "mesh has no triangles (T = 0)");
+    if (V <= 0) throw Error(FGL_E_DATA, "mesh has no vertices");
+    if (!verts || !tris) throw Error(FGL_E_USAGE, "verts / tris is NULL");
+    if (T > fgl::kMaxTris) throw Error(FGL_E_USAGE, "too many triangles (T must be < 2^28)");
+    if (V > INT32_MAX) throw Error(FGL_E_USAGE, "too many vertices (V must fit int32)");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    s->built = false;
+    if (V > s->cap_V) {
+        if (s->verts) cudaFree(s->verts), s->verts = nullptr;
+        FGL_CUDA(cudaMalloc((void **)&s->verts, sizeof(float) * 3 * V));
+        s->cap_V = V;
+    }
+    if (T > s->cap_T) {
+        if (s->tris) cudaFree(s->tris), s->tris = nullptr;
+        FGL_CUDA(cudaMalloc((void **)&s->tris, sizeof(int32_t) * 3 * T));
+        alloc_build(s, T);
+        s->cap_T = T;
+    }
+    s->b.T = T;
+    s->V = V, s->T = T;
+    cudaMemcpyKind kind = ptr_kind == FGL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    FGL_CUDA(cudaMemcpyAsync(s->verts, verts, sizeof(float) * 3 * V, kind, st));
+    FGL_CUDA(cudaMemcpyAsync(s->tris, tris, sizeof(int32_t) * 3 * T, kind, st));
+    fgl::launch_validate(s->verts, V, s->tris, T, s->vflag, st);
+    FGL_CUDA(cudaMemcpyAsync(s->hflag, s->vflag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    FGL_CUDA(cudaStreamSynchronize(st));
+    if (*s->hflag & 1u) throw Error(FGL_E_DATA, "triangle index out of range [0, V)");
+    if (*s->hflag & 2u) throw Error(FGL_E_DATA, "non-finite vertex coordinate");
+    FGL_API_END
+}
+
+fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *stream) {
+    FGL_API_BEGIN
+    if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
+    int bits = 21, leaf = 4;
+    if (opts) {
+        for (int i = 0; i < 6; ++i)
+            if (opts->reserved[i]) throw Error(FGL_E_USAGE, "fgl_build_opts.reserved must be zero");
+        if (opts->morton_bits) bits = opts->morton_bits;
+        if (opts->leaf_size) leaf = opts->leaf_size;
+    }
+    if (bits < 1 || bits > 21) throw Error(FGL_E_USAGE, "morton_bits must be in [1, 21]");
+    if (leaf < 1 || leaf > fgl::kMaxLeaf) throw Error(FGL_E_USAGE, "leaf_size must be in [1, 8]");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    s->bits = bits, s->leaf_size = leaf;
+    FGL_CUDA(cudaEventRecord(s->ev0, st));
+    fgl::launch_build(s->verts, s->tris, s->b, bits, leaf, st);
+    FGL_CUDA(cudaEventRecord(s->ev1, st));
+    s->built = true;
+    FGL_API_END
+}
+
+fgl_status fgl_scene_stats(fgl_scene *s, fgl_stats *out) {
+    FGL_API_BEGIN
+    if (!s || !out) throw Error(FGL_E_USAGE, "NULL argument");
+    DeviceGuard g(s->dev);
+    memset(out, 0, sizeof(*out));
+    out->triangles = s->T;
+    out->vertices = s->V;
+    out->nodes = std::max<int64_t>(s->T - 1, 1);
+    out->device_bytes = (int64_t)(s->bytes + sizeof(float) * 3 * s->cap_V + sizeof(int32_t) * 3 * s->cap_T);
+    out->morton_bits = s->bits;
+    out->leaf_size = s->leaf_size;
+    if (s->built) {
+        FGL_CUDA(cudaEventSynchronize(s->ev1));
+        FGL_CUDA(cudaEventElapsedTime(&out->build_ms, s->ev0, s->ev1));
+        float box[6];
+        FGL_CUDA(cudaMemcpy(box, s->b.box, sizeof(box), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 3; ++i) out->scene_lo[i] = box[i], out->scene_hi[i] = box[3 + i];
+    }
+    FGL_API_END
+}
+
+fgl_status fgl_cast_spinning(const fgl_scene *s, const fgl_spinning *pattern, const float *poses, int64_t P,
+                             float *range, int32_t *tri_id, float *hit_xyz, int32_t *node_counts, int32_t *tri_counts,
+                             void *stream) {
+    FGL_API_BEGIN
+    check_built(s);
+    fgl::SpinParams sp = spin_params(pattern);
+    if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
+    if (P == 0) return FGL_OK;
+    if (!poses) throw Error(FGL_E_USAGE, "poses is NULL");
+    fgl::CastOut o = cast_out(range, tri_id, hit_xyz, node_counts, tri_counts);
+    DeviceGuard g(s->dev);
+    fgl::launch_cast_spinning(view(s), sp, poses, P, o, next_counter(s), (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_cast_rosette(const fgl_scene *s, const fgl_rosette *pattern, const float *poses, int64_t P,
+                            int64_t first_frame, float *range, int32_t *tri_id, float *hit_xyz, int32_t *node_counts,
+                            int32_t *tri_counts, void *stream) {
+    FGL_API_BEGIN
+    check_built(s);
+    fgl::RosetteParams rp = rosette_params(pattern, first_frame);
+    if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
+    if (P == 0) return FGL_OK;
+    if (!poses) throw Error(FGL_E_USAGE, "poses is NULL");
+    fgl::CastOut o = cast_out(range, tri_id, hit_xyz, node_counts, tri_counts);
+    DeviceGuard g(s->dev);
+    fgl::launch_cast_rosette(view(s), rp, poses, P, o, next_counter(s), (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_cast_rays(const fgl_scene *s, const float *orig, const float *dir, int64_t R, float t_min, float t_max,
+                         float *range, int32_t *tri_id, void *stream) {
+    FGL_API_BEGIN
+    check_built(s);
+    check_interval(t_min, t_max);
+    if (R < 0) throw Error(FGL_E_USAGE, "R must be >= 0");
+    if (R == 0) return FGL_OK;
+    if (!orig || !dir) throw Error(FGL_E_USAGE, "orig / dir is NULL");
+    fgl::CastOut o = cast_out(range, tri_id, nullptr, nullptr, nullptr);
+    DeviceGuard g(s->dev);
+    fgl::launch_cast_rays(view(s), orig, dir, R, t_min, t_max, o, next_counter(s), (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_cast_rays_bruteforce(const fgl_scene *s, const float *orig, const float *dir, int64_t R, float t_min,
+                                    float t_max, float *range, int32_t *tri_id, void *stream) {
+    FGL_API_BEGIN
+    if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
+    check_interval(t_min, t_max);
+    if (R < 0) throw Error(FGL_E_USAGE, "R must be >= 0");
+    if (R == 0) return FGL_OK;
+    if (!orig || !dir || !range || !tri_id) throw Error(FGL_E_USAGE, "NULL pointer argument");
+    DeviceGuard g(s->dev);
+    fgl::launch_cast_bruteforce(s->verts, s->tris, s->T, orig, dir, R, t_min, t_max, range, tri_id,
+                                (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_export_rays_spinning(const fgl_spinning *pattern, const float *poses, int64_t P, float *orig, float *dir,
+                                    void *stream) {
+    FGL_API_BEGIN
+    fgl::SpinParams sp = spin_params(pattern);
+    if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
+    if (P == 0) return FGL_OK;
+    if (!poses || !orig || !dir) throw Error(FGL_E_USAGE, "NULL pointer argument");
+    fgl::launch_export_spinning(sp, poses, P, orig, dir, (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_export_rays_rosette(const fgl_rosette *pattern, const float *poses, int64_t P, int64_t first_frame,
+                                   float *orig, float *dir, void *stream) {
+    FGL_API_BEGIN
+    fgl::RosetteParams rp = rosette_params(pattern, first_frame);
+    if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
+    if (P == 0) return FGL_OK;
+    if (!poses || !orig || !dir) throw Error(FGL_E_USAGE, "NULL pointer argument");
+    fgl::launch_export_rosette(rp, poses, P, orig, dir, (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_scene_export(const fgl_scene *s, const fgl_export *out, void *stream) {
+    FGL_API_BEGIN
+    check_built(s);
+    if (!out) throw Error(FGL_E_USAGE, "out is NULL");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    FGL_CUDA(cudaStreamSynchronize(st));
+    const int64_t T = s->T, nin = std::max<int64_t>(T - 1, 0);
+    const fgl::BuildBuffers &b = s->b;
+    auto cp = [&](void *dst, const void *src, size_t bytes) {
+        if (dst && bytes) FGL_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    };
+    cp(out->scene_box, b.box, 6 * sizeof(float));
+    cp(out->sorted_keys, b.keys[b.sorted_slot], T * sizeof(uint64_t));
+    cp(out->perm, b.vals[b.sorted_slot], T * sizeof(uint32_t));
+    if (out->codes) {
+        // input-order codes: codes[perm[j]] = sorted_keys[j] (a permutation of the sorted array)
+        std::string tmpk(T * sizeof(uint64_t), '\0'), tmpp(T * sizeof(uint32_t), '\0');
+        cp(&tmpk[0], b.keys[b.sorted_slot], T * sizeof(uint64_t));
+        cp(&tmpp[0], b.vals[b.sorted_slot], T * sizeof(uint32_t));
+        const uint64_t *k = (const uint64_t *)tmpk.data();
+        const uint32_t *p = (const uint32_t *)tmpp.data();
+        for (int64_t j = 0; j < T; ++j) out->codes[p[j]] = k[j];
+    }
+    cp(out->child, b.child, nin * sizeof(int2));
+    cp(out->range, b.range, nin * sizeof(int2));
+    if (out->leaf_box || out->node_box) {
+        std::string tmp(std::max<int64_t>(2 * T, 2 * nin) * sizeof(float4), '\0');
+        float4 *f = (float4 *)&tmp[0];
+        if (out->leaf_box) {
+            cp(f, b.leafbox, 2 * T * sizeof(float4));
+            for (int64_t j = 0; j < T; ++j)
+                for (int i = 0; i < 3; ++i)
+                    out->leaf_box[6 * j + i] = (&f[2 * j].x)[i], out->leaf_box[6 * j + 3 + i] = (&f[2 * j + 1].x)[i];
+        }
+        if (out->node_box && nin) {
+            cp(f, b.nodebox, 2 * nin * sizeof(float4));
+            for (int64_t j = 0; j < nin; ++j)
+                for (int i = 0; i < 3; ++i)
+                    out->node_box[6 * j + i] = (&f[2 * j].x)[i], out->node_box[6 * j + 3 + i] = (&f[2 * j + 1].x)[i];
+        }
+    }
+    cp(out->tri48, b.tri, 3 * T * sizeof(float4));
+    cp(out->nodes, b.nodes, std::max<int64_t>(nin, 1) * sizeof(fgl::Node64));
+    FGL_API_END
+}
+
+fgl_status fgl_morton_codes(const float *points, int64_t n, const float *lo, const float *hi, int32_t bits,
+                            uint64_t *codes, void *stream) {
+    FGL_API_BEGIN
+    if (n < 0) throw Error(FGL_E_USAGE, "n must be >= 0");
+    if (bits < 1 || bits > 21) throw Error(FGL_E_USAGE, "bits must be in [1, 21]");
+    if (n == 0) return FGL_OK;
+    if (!points || !lo || !hi || !codes) throw Error(FGL_E_USAGE, "NULL pointer argument");
+    fgl::launch_morton_points(points, n, lo, hi, bits, codes, (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key_bits, void *stream) {
+    FGL_API_BEGIN
+    if (n < 0) throw Error(FGL_E_USAGE, "n must be >= 0");
+    if (key_bits < 1 || key_bits > 64) throw Error(FGL_E_USAGE, "key_bits must be in [1, 64]");
+    if (n > (int64_t)UINT32_MAX) throw Error(FGL_E_USAGE, "n too large");
+    if (n <= 1) return FGL_OK;
+    if (!keys || !vals) throw Error(FGL_E_USAGE, "NULL pointer argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    uint64_t *k1 = nullptr;
+    uint32_t *v1 = nullptr, *counts = nullptr, *ghist = nullptr;
+    FGL_CUDA(cudaMallocAsync((void **)&k1, n * sizeof(uint64_t), st));
+    FGL_CUDA(cudaMallocAsync((void **)&v1, n * sizeof(uint32_t), st));
+    FGL_CUDA(cudaMallocAsync((void **)&counts, (size_t)256 * fgl::sort_tile_blocks(n) * sizeof(uint32_t), st));
+    FGL_CUDA(cudaMallocAsync((void **)&ghist, 8 * 256 * sizeof(uint32_t), st));
+    int slot = 0;
+    fgl::radix_sort_pairs(keys, vals, k1, v1, n, key_bits, counts, ghist, false, &slot, st);
+    if (slot == 1) {
+        FGL_CUDA(cudaMemcpyAsync(keys, k1, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
+        FGL_CUDA(cudaMemcpyAsync(vals, v1, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+    }
+    cudaFreeAsync(k1, st);
+    cudaFreeAsync(v1, st);
+    cudaFreeAsync(counts, st);
+    cudaFreeAsync(ghist, st);
+    FGL_API_END
+}
+
+}  // extern "C"

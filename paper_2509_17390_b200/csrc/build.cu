@@ -1,0 +1,344 @@
+// LBVH construction over triangles on sm_100a — PAPER.md §IV-A "BVH Construction",
+// applied to the cast's triangle mesh (R8):
+//   prep     : triangle centroids (the Morton point) + exact scene box [o, o+L] (last-block reduce)
+//   morton   : Eq. 5 codes, b bits per axis, x lowest, + the all-pass digit histogram
+//   sort     : stable LSD radix sort (sort.cu), "radix sort run massively in parallel"
+//   reorder  : triangle records (tri48) gathered into sorted (leaf) order
+//   karras   : Eq. 6 LCP-split binary radix tree, one thread per internal node,
+//              "bitwise operations ... without recursion"
+//   refit    : Eq. 7 bottom-up union with atomic arrival counters
+//   nodes    : traversal nodes (both child boxes per node; subtrees of <= leaf_size triangles
+//              become leaves), laid out in Karras (Morton) order ("Morton order").
+#include "fgl_internal.cuh"
+
+namespace fgl {
+
+namespace {
+
+__global__ void k_validate(const float *__restrict__ verts, int64_t V, const int32_t *__restrict__ tris, int64_t T,
+                           unsigned int *flag) {
+    unsigned int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * T; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t x = tris[i];
+        if (x < 0 || x >= V) bad |= 1u;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * V; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(verts[i])) bad |= 2u;
+    if (bad) atomicOr(flag, bad);
+}
+
+__device__ __forceinline__ float3 ldv(const float *__restrict__ verts, int32_t i) {
+    return make_float3(__ldg(verts + 3 * (int64_t)i), __ldg(verts + 3 * (int64_t)i + 1), __ldg(verts + 3 * (int64_t)i + 2));
+}
+
+// centroid c = ((v0 + v1) + v2) / 3, float32 round-to-nearest, no contraction (R8)
+__device__ __forceinline__ float centroid1(float a, float b, float c) {
+    return __fdiv_rn(__fadd_rn(__fadd_rn(a, b), c), 3.0f);
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+    for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_prep(const float *__restrict__ verts, const int32_t *__restrict__ tris,
+                                              int64_t T, float4 *__restrict__ cent, float *__restrict__ partial,
+                                              unsigned int *sync, float *__restrict__ box) {
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < T; k += (int64_t)gridDim.x * blockDim.x) {
+        int32_t i0 = __ldg(tris + 3 * k), i1 = __ldg(tris + 3 * k + 1), i2 = __ldg(tris + 3 * k + 2);
+        float3 a = ldv(verts, i0), b = ldv(verts, i1), c = ldv(verts, i2);
+        float4 m = make_float4(centroid1(a.x, b.x, c.x), centroid1(a.y, b.y, c.y), centroid1(a.z, b.z, c.z), 0.f);
+        cent[k] = m;
+        lo[0] = fminf(lo[0], m.x), lo[1] = fminf(lo[1], m.y), lo[2] = fminf(lo[2], m.z);
+        hi[0] = fmaxf(hi[0], m.x), hi[1] = fmaxf(hi[1], m.y), hi[2] = fmaxf(hi[2], m.z);
+    }
+    __shared__ float s[8][6];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i = 0; i < 3; ++i) {
+        lo[i] = warp_min(lo[i]);
+        hi[i] = warp_max(hi[i]);
+    }
+    if (lane == 0)
+        for (int i = 0; i < 3; ++i) s[w][i] = lo[i], s[w][3 + i] = hi[i];
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x < 6) {
+        float v = s[0][threadIdx.x];
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+            v = threadIdx.x < 3 ? fminf(v, s[ww][threadIdx.x]) : fmaxf(v, s[ww][threadIdx.x]);
+        partial[blockIdx.x * 6 + threadIdx.x] = v;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(sync, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    // last block: reduce all partials (L2 reads), publish the box, reset the counter
+    if (threadIdx.x < 32) {
+        for (int i = 0; i < 6; ++i) {
+            float v = i < 3 ? INFINITY : -INFINITY;
+            for (int b = lane; b < (int)gridDim.x; b += 32) {
+                float x = __ldcg(partial + b * 6 + i);
+                v = i < 3 ? fminf(v, x) : fmaxf(v, x);
+            }
+            v = i < 3 ? warp_min(v) : warp_max(v);
+            if (lane == 0) box[i] = v;
+        }
+        if (lane == 0) *sync = 0u;
+    }
+}
+
+// spread the low 21 bits of x to every third bit (bit i -> bit 3i)
+__device__ __forceinline__ uint64_t spread3(uint32_t x) {
+    uint64_t v = x & 0x1fffffu;
+    v = (v | (v << 32)) & 0x1f00000000ffffull;
+    v = (v | (v << 16)) & 0x1f0000ff0000ffull;
+    v = (v | (v << 8)) & 0x100f00f00f00f00full;
+    v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+// Eq. 5 quantisation in float32 (the decision is a float one; R7):
+// L = hi - lo; s = L > 0 ? 2^b / L : 0; q = min(floor((c - lo) * s), 2^b - 1)
+struct MortonBox {
+    float lo[3], s[3];
+    uint32_t qmax;
+};
+
+__device__ __forceinline__ MortonBox morton_box(const float *lo, const float *hi, int bits) {
+    MortonBox m;
+    const float two_b = (float)(1u << bits);
+    m.qmax = (1u << bits) - 1u;
+    for (int i = 0; i < 3; ++i) {
+        m.lo[i] = lo[i];
+        float L = __fsub_rn(hi[i], lo[i]);
+        m.s[i] = L > 0.f ? __fdiv_rn(two_b, L) : 0.f;
+    }
+    return m;
+}
+
+__device__ __forceinline__ uint64_t morton_code(const MortonBox &m, float x, float y, float z) {
+    float c[3] = {x, y, z};
+    uint32_t q[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        float f = floorf(__fmul_rn(__fsub_rn(c[i], m.lo[i]), m.s[i]));
+        q[i] = f >= (float)m.qmax ? m.qmax : (uint32_t)f;
+    }
+    return spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+}
+
+__global__ void __launch_bounds__(256) k_morton(const float4 *__restrict__ cent, int64_t T,
+                                                const float *__restrict__ box, int bits, uint64_t *__restrict__ keys,
+                                                uint32_t *__restrict__ vals, uint32_t *__restrict__ ghist) {
+    __shared__ uint32_t h[8][256];
+    __shared__ MortonBox mb;
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+    if (threadIdx.x == 0) mb = morton_box(box, box + 3, bits);
+    __syncthreads();
+    const int npass = (3 * bits + 7) / 8;
+    const MortonBox m = mb;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < T; k += (int64_t)gridDim.x * blockDim.x) {
+        float4 c = cent[k];
+        uint64_t code = morton_code(m, c.x, c.y, c.z);
+        keys[k] = code;
+        vals[k] = (uint32_t)k;
+        for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(code >> (8 * p)) & 0xFF], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < npass * 256; i += blockDim.x) {
+        uint32_t v = (&h[0][0])[i];
+        if (v) atomicAdd(&ghist[i], v);
+    }
+}
+
+struct BoxArg {
+    float lo[3], hi[3];
+};
+
+__global__ void k_morton_points(const float *__restrict__ pts, int64_t n, BoxArg bx, int bits,
+                                uint64_t *__restrict__ codes) {
+    const MortonBox m = morton_box(bx.lo, bx.hi, bits);
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        codes[k] = morton_code(m, pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]);
+}
+
+// tri48 record j = triangle perm[j]: {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}; leaf box j
+__global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, const int32_t *__restrict__ tris,
+                                                 const uint32_t *__restrict__ perm, int64_t T,
+                                                 float4 *__restrict__ tri, float4 *__restrict__ leafbox) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < T; j += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t k = perm[j];
+        float3 a = ldv(verts, __ldg(tris + 3 * (int64_t)k)), b = ldv(verts, __ldg(tris + 3 * (int64_t)k + 1)),
+               c = ldv(verts, __ldg(tris + 3 * (int64_t)k + 2));
+        tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
+        tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
+        tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
+        leafbox[2 * j] = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
+        leafbox[2 * j + 1] = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
+    }
+}
+
+// LCP of augmented keys code_i || i (sorted position fallback for equal codes; R7); -1 outside
+__device__ __forceinline__ int delta(const uint64_t *__restrict__ k, int64_t n, int64_t i, int64_t j) {
+    if (j < 0 || j >= n) return -1;
+    uint64_t a = __ldg(k + i), b = __ldg(k + j);
+    if (a != b) return __clzll((long long)(a ^ b));
+    return 64 + __clz((int)((uint32_t)i ^ (uint32_t)j));
+}
+
+// Karras 2012 (Eq. 6 read as the non-recursive LCP split, R7): one thread per internal node i
+__global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, int64_t n, int2 *__restrict__ child,
+                                                int2 *__restrict__ range, int32_t *__restrict__ parent) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
+        const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
+        const int dmin = delta(k, n, i, i - d);
+        int64_t lmax = 2;
+        while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+        int64_t l = 0;
+        for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
+            if (delta(k, n, i, i + (l + t) * d) > dmin) l += t;
+        const int64_t j = i + l * d;
+        const int dnode = delta(k, n, i, j);
+        int64_t s = 0, t = l;
+        do {
+            t = (t + 1) >> 1;
+            if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
+        } while (t > 1);
+        const int64_t g = i + s * d + (d < 0 ? -1 : 0);
+        const int64_t f = i < j ? i : j, last = i < j ? j : i;
+        int32_t left = f == g ? ~(int32_t)g : (int32_t)g;
+        int32_t right = last == g + 1 ? ~(int32_t)(g + 1) : (int32_t)(g + 1);
+        child[i] = make_int2(left, right);
+        range[i] = make_int2((int32_t)f, (int32_t)last);
+        parent[left >= 0 ? left : (n - 1) + ~left] = (int32_t)i;
+        parent[right >= 0 ? right : (n - 1) + ~right] = (int32_t)i;
+        if (i == 0) parent[0] = -1;
+    }
+}
+
+__device__ __forceinline__ void ldbox(const float4 *p, float4 &lo, float4 &hi) {
+    lo = __ldcg(p);
+    hi = __ldcg(p + 1);
+}
+
+// Eq. 7 bottom-up: each leaf climbs; the second thread to reach a node writes the union
+__global__ void __launch_bounds__(256) k_refit(int64_t n, const int2 *__restrict__ child,
+                                               const int32_t *__restrict__ parent, int32_t *__restrict__ flags,
+                                               const float4 *__restrict__ leafbox, float4 *__restrict__ nodebox) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        int32_t p = parent[(n - 1) + j];
+        while (p >= 0) {
+            __threadfence();
+            if (atomicAdd(&flags[p], 1) == 0) break;
+            int2 c = __ldcg(&child[p]);
+            float4 l0, h0, l1, h1;
+            ldbox(c.x >= 0 ? nodebox + 2 * (int64_t)c.x : leafbox + 2 * (int64_t)(~c.x), l0, h0);
+            ldbox(c.y >= 0 ? nodebox + 2 * (int64_t)c.y : leafbox + 2 * (int64_t)(~c.y), l1, h1);
+            __stcg(nodebox + 2 * (int64_t)p, make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.f));
+            __stcg(nodebox + 2 * (int64_t)p + 1, make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.f));
+            p = parent[p];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const int2 *__restrict__ child,
+                                               const int2 *__restrict__ range, const float4 *__restrict__ leafbox,
+                                               const float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
+        int2 c = child[i];
+        int32_t ref[2];
+        float4 lo[2], hi[2];
+        int32_t cc[2] = {c.x, c.y};
+        for (int s = 0; s < 2; ++s) {
+            if (cc[s] < 0) {
+                int32_t j = ~cc[s];
+                ref[s] = make_leaf(j, 1);
+                lo[s] = leafbox[2 * (int64_t)j];
+                hi[s] = leafbox[2 * (int64_t)j + 1];
+            } else {
+                int2 r = range[cc[s]];
+                int32_t cnt = r.y - r.x + 1;
+                ref[s] = cnt <= leaf_size ? make_leaf(r.x, cnt) : cc[s];
+                lo[s] = nodebox[2 * (int64_t)cc[s]];
+                hi[s] = nodebox[2 * (int64_t)cc[s] + 1];
+            }
+        }
+        Node64 nd;
+        nd.a = make_float4(lo[0].x, hi[0].x, lo[0].y, hi[0].y);
+        nd.b = make_float4(lo[1].x, hi[1].x, lo[1].y, hi[1].y);
+        nd.c = make_float4(lo[0].z, hi[0].z, lo[1].z, hi[1].z);
+        nd.d = make_int4(ref[0], ref[1], 0, 0);
+        nodes[i] = nd;
+    }
+}
+
+// T == 1: a root whose first child is the single leaf and whose second child is empty
+__global__ void k_single(const float4 *__restrict__ leafbox, Node64 *__restrict__ nodes) {
+    float4 lo = leafbox[0], hi = leafbox[1];
+    Node64 nd;
+    nd.a = make_float4(lo.x, hi.x, lo.y, hi.y);
+    nd.b = make_float4(0.f, 0.f, 0.f, 0.f);
+    nd.c = make_float4(lo.z, hi.z, 0.f, 0.f);
+    nd.d = make_int4(make_leaf(0, 1), kEmptyRef, 0, 0);
+    nodes[0] = nd;
+}
+
+inline int grid_for(int64_t n, int threads = 256, int max_blocks = 148 * 16) {
+    int64_t b = (n + threads - 1) / threads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, max_blocks));
+}
+
+}  // namespace
+
+void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
+                     cudaStream_t s) {
+    FGL_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), s));
+    k_validate<<<grid_for(3 * std::max(T, V)), 256, 0, s>>>(verts, V, tris, T, flag);
+    FGL_LAUNCHED("k_validate");
+}
+
+void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits, uint64_t *codes,
+                          cudaStream_t s) {
+    if (n <= 0) return;
+    BoxArg bx;
+    for (int i = 0; i < 3; ++i) bx.lo[i] = lo[i], bx.hi[i] = hi[i];
+    k_morton_points<<<grid_for(n), 256, 0, s>>>(pts, n, bx, bits, codes);
+    FGL_LAUNCHED("k_morton_points");
+}
+
+void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
+                  cudaStream_t s) {
+    const int64_t T = b.T;
+    const int key_bits = 3 * bits;
+    k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, tris, T, b.cent, b.partial, b.sync, b.box);
+    FGL_LAUNCHED("k_prep");
+    FGL_CUDA(cudaMemsetAsync(b.ghist, 0, sizeof(uint32_t) * 8 * 256, s));
+    k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, b.keys[0], b.vals[0], b.ghist);
+    FGL_LAUNCHED("k_morton");
+    int slot = 0;
+    radix_sort_pairs(b.keys[0], b.vals[0], b.keys[1], b.vals[1], T, key_bits, b.counts, b.ghist, true, &slot, s);
+    b.sorted_slot = slot;
+    k_reorder<<<grid_for(T), 256, 0, s>>>(verts, tris, b.vals[slot], T, b.tri, b.leafbox);
+    FGL_LAUNCHED("k_reorder");
+    if (T == 1) {
+        k_single<<<1, 1, 0, s>>>(b.leafbox, b.nodes);
+        FGL_LAUNCHED("k_single");
+        return;
+    }
+    k_karras<<<grid_for(T - 1), 256, 0, s>>>(b.keys[slot], T, b.child, b.range, b.parent);
+    FGL_LAUNCHED("k_karras");
+    FGL_CUDA(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * (T - 1), s));
+    k_refit<<<grid_for(T), 256, 0, s>>>(T, b.child, b.parent, b.flags, b.leafbox, b.nodebox);
+    FGL_LAUNCHED("k_refit");
+    k_nodes<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.leafbox, b.nodebox, b.nodes);
+    FGL_LAUNCHED("k_nodes");
+}
+
+}  // namespace fgl

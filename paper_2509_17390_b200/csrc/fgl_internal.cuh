@@ -1,0 +1,135 @@
+// Internal declarations shared by the libfgl translation units (never by the oracle).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace fgl {
+
+// ---- errors -----------------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define FGL_CUDA(call)                                                                                  \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess) {                                                                        \
+            int code_ = (e_ == cudaErrorMemoryAllocation) ? 3 : 4;                                      \
+            throw ::fgl::Error(code_, std::string(#call) + ": " + cudaGetErrorString(e_));             \
+        }                                                                                               \
+    } while (0)
+
+void note_launch();  // process-wide count of libfgl kernel launches (fgl_kernel_launches)
+
+#define FGL_LAUNCHED(what)                                                                              \
+    do {                                                                                                \
+        ::fgl::note_launch();                                                                           \
+        cudaError_t e_ = cudaGetLastError();                                                            \
+        if (e_ != cudaSuccess) throw ::fgl::Error(4, std::string(what) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---- traversal node: binary LBVH node holding both children's boxes ("node64", 4 x 16 B) -------
+// a = (c0.lo.x, c0.hi.x, c0.lo.y, c0.hi.y)   b = (c1.lo.x, c1.hi.x, c1.lo.y, c1.hi.y)
+// c = (c0.lo.z, c0.hi.z, c1.lo.z, c1.hi.z)   d = (ref0, ref1, 0, 0)
+// ref >= 0: internal node index; ref < 0 and != kEmptyRef: leaf, ~ref = first << 3 | (count - 1)
+struct __align__(16) Node64 {
+    float4 a, b, c;
+    int4 d;
+};
+constexpr int32_t kEmptyRef = INT32_MIN;
+constexpr int kLeafShift = 3;
+constexpr int kMaxLeaf = 8;
+constexpr int64_t kMaxTris = (int64_t(1) << 28) - 1;
+
+__host__ __device__ inline int32_t make_leaf(int32_t first, int32_t count) {
+    return ~((first << kLeafShift) | (count - 1));
+}
+
+// ---- per-call work counters for persistent casts (self-resetting, 64 slots per scene) ----------
+struct CastCounter {
+    unsigned long long next;
+    unsigned int done;
+    unsigned int pad;
+};
+constexpr int kCounterSlots = 64;
+
+// ---- scene build buffers (device) ---------------------------------------------------------------
+struct BuildBuffers {
+    int64_t T = 0;
+    float4 *cent = nullptr;        // [T] centroid (x, y, z, 0)
+    float *box = nullptr;          // [6] scene box lo, hi
+    float *partial = nullptr;      // [kPrepBlocks][6]
+    unsigned int *sync = nullptr;  // [4] last-block counters
+    uint64_t *keys[2] = {nullptr, nullptr};
+    uint32_t *vals[2] = {nullptr, nullptr};
+    uint32_t *ghist = nullptr;     // [8][256] digit histograms
+    uint32_t *counts = nullptr;    // [256][nblk] per-block digit counts / offsets
+    float4 *tri = nullptr;         // [3T] tri48 in leaf order
+    int2 *child = nullptr;         // [T-1]
+    int2 *range = nullptr;         // [T-1]
+    int32_t *parent = nullptr;     // [2T-1]
+    int32_t *flags = nullptr;      // [T-1]
+    float4 *leafbox = nullptr;     // [2T]
+    float4 *nodebox = nullptr;     // [2(T-1)]
+    Node64 *nodes = nullptr;       // [max(T-1,1)]
+    int sorted_slot = 0;           // which keys/vals buffer holds the sorted result
+};
+
+constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
+
+// ---- launchers ------------------------------------------------------------------------------------
+// sort.cu
+int sort_tile_blocks(int64_t n);
+void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
+                      uint32_t *counts, uint32_t *ghist, bool ghist_ready, int *result_slot, cudaStream_t s);
+void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s);
+
+// build.cu
+void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
+                  cudaStream_t s);
+void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
+                     cudaStream_t s);
+void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
+                          uint64_t *codes, cudaStream_t s);
+
+// cast.cu
+struct SpinParams {
+    int32_t channels, columns;
+    float az0_deg, t_min, t_max;
+    float elev_deg[512];
+};
+struct RosetteParams {
+    int32_t n;
+    uint32_t inc1, inc2, phase2_0;
+    float half_fov_deg, t_min, t_max;
+    int64_t first_frame;
+};
+struct CastOut {
+    float *range;
+    int32_t *tri_id;
+    float *hit_xyz;
+    int32_t *node_counts, *tri_counts;
+};
+struct SceneView {
+    const float4 *tri;
+    const Node64 *nodes;
+};
+void launch_cast_spinning(const SceneView &sv, const SpinParams &p, const float *poses, int64_t P, const CastOut &o,
+                          CastCounter *ctr, cudaStream_t s);
+void launch_cast_rosette(const SceneView &sv, const RosetteParams &p, const float *poses, int64_t P,
+                         const CastOut &o, CastCounter *ctr, cudaStream_t s);
+void launch_cast_rays(const SceneView &sv, const float *orig, const float *dir, int64_t R, float t_min, float t_max,
+                      const CastOut &o, CastCounter *ctr, cudaStream_t s);
+void launch_cast_bruteforce(const float *verts, const int32_t *tris, int64_t T, const float *orig, const float *dir,
+                            int64_t R, float t_min, float t_max, float *range, int32_t *tri_id, cudaStream_t s);
+void launch_export_spinning(const SpinParams &p, const float *poses, int64_t P, float *orig, float *dir,
+                            cudaStream_t s);
+void launch_export_rosette(const RosetteParams &p, const float *poses, int64_t P, float *orig, float *dir,
+                           cudaStream_t s);
+
+}  // namespace fgl

@@ -1,0 +1,316 @@
+"""Thin ctypes binding of libfgl.so (include/fgl.h) — argument marshalling only.
+
+Every step of the cast path runs in the library's sm_100a kernels; this module only passes
+torch device pointers, sizes and the current CUDA stream through the C ABI. There is no CPU
+fallback: if libfgl.so is missing or no CUDA device is present the calls raise.
+
+PAPER.md anchors: mesh M, pose T_s, pattern d_j (Eq. 19),
+nearest hit t_j* / rho_j (Eq. 20), LBVH build (§IV-A).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, Structure, c_char_p, c_float, c_int, c_int32, c_int64, c_uint32, c_uint64, c_void_p
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfgl.so")
+
+OK, E_USAGE, E_DATA, E_RESOURCE, E_CUDA = range(5)
+HOST, DEVICE = 0, 1
+
+
+class FglError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"fgl status {status}: {msg}")
+        self.status = status
+
+
+class BuildOpts(Structure):
+    _fields_ = [("morton_bits", c_int32), ("leaf_size", c_int32), ("reserved", c_int32 * 6)]
+
+
+class Stats(Structure):
+    _fields_ = [("triangles", c_int64), ("vertices", c_int64), ("nodes", c_int64), ("device_bytes", c_int64),
+                ("scene_lo", c_float * 3), ("scene_hi", c_float * 3), ("build_ms", c_float),
+                ("morton_bits", c_int32), ("leaf_size", c_int32)]
+
+
+class SpinningC(Structure):
+    _fields_ = [("channels", c_int32), ("columns", c_int32), ("elev_deg", c_void_p), ("az0_deg", c_float),
+                ("t_min", c_float), ("t_max", c_float)]
+
+
+class RosetteC(Structure):
+    _fields_ = [("points_per_frame", c_int32), ("inc1", c_uint32), ("inc2", c_uint32), ("phase2_0", c_uint32),
+                ("half_fov_deg", c_float), ("t_min", c_float), ("t_max", c_float)]
+
+
+class ExportC(Structure):
+    _fields_ = [(n, c_void_p) for n in ("scene_box", "codes", "sorted_keys", "perm", "child", "range", "leaf_box",
+                                        "node_box", "tri48", "nodes")]
+
+
+# name: (restype, argtypes)
+_SIGS = {
+    "fgl_scene_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "fgl_scene_destroy": (None, [c_void_p]),
+    "fgl_scene_upload_mesh": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int, c_void_p]),
+    "fgl_scene_build": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "fgl_scene_stats": (c_int, [c_void_p, POINTER(Stats)]),
+    "fgl_cast_spinning": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p]),
+    "fgl_cast_rosette": (c_int, [c_void_p, POINTER(RosetteC), c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p, c_void_p]),
+    "fgl_cast_rays": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_float, c_float, c_void_p, c_void_p, c_void_p]),
+    "fgl_cast_rays_bruteforce": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_float, c_float, c_void_p, c_void_p,
+                                         c_void_p]),
+    "fgl_export_rays_spinning": (c_int, [POINTER(SpinningC), c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "fgl_export_rays_rosette": (c_int, [POINTER(RosetteC), c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+    "fgl_scene_export": (c_int, [c_void_p, POINTER(ExportC), c_void_p]),
+    "fgl_morton_codes": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
+    "fgl_sort_pairs": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
+    "fgl_last_error": (c_char_p, []),
+    "fgl_version": (c_char_p, []),
+    "fgl_abi_version": (c_int32, []),
+    "fgl_kernel_launches": (c_int64, []),
+}
+SYMBOLS = tuple(_SIGS)
+
+_lib = None
+
+
+def lib():
+    """Load libfgl.so (in-tree). Raises loudly if it is missing: there is no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libfgl.so not found at {LIB_PATH}; run __graft_entry__.build() "
+                              "(python paper_2509_17390_b200/_build.py)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        raise FglError(status, lib().fgl_last_error().decode(errors="replace"))
+
+
+def _stream(stream=None) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else int(t.data_ptr())
+
+
+def _dev(t: torch.Tensor, dtype, device, shape=None) -> torch.Tensor:
+    t = torch.as_tensor(t).to(device=device, dtype=dtype).contiguous()
+    if shape is not None:
+        t = t.reshape(shape)
+    return t
+
+
+def spinning_struct(pattern):
+    """fgl_spinning from any object with elev_deg, columns, az0_deg, t_min, t_max."""
+    e = np.ascontiguousarray(np.asarray(pattern.elev_deg, dtype=np.float32))
+    s = SpinningC(int(e.shape[0]), int(pattern.columns), e.ctypes.data, float(getattr(pattern, "az0_deg", 0.0)),
+                  float(pattern.t_min), float(pattern.t_max))
+    s._keep = e
+    return s
+
+
+def rosette_struct(pattern):
+    return RosetteC(int(pattern.points_per_frame), int(pattern.inc1) & 0xFFFFFFFF, int(pattern.inc2) & 0xFFFFFFFF,
+                    int(pattern.phase2_0) & 0xFFFFFFFF, float(pattern.half_fov_deg), float(pattern.t_min),
+                    float(pattern.t_max))
+
+
+def is_spinning(pattern) -> bool:
+    return hasattr(pattern, "elev_deg")
+
+
+def rays_per_pose(pattern) -> int:
+    if is_spinning(pattern):
+        return int(len(pattern.elev_deg)) * int(pattern.columns)
+    return int(pattern.points_per_frame)
+
+
+class Scene:
+    """A triangle mesh on one GPU with its LBVH. `Scene(verts, tris)` uploads (validating) and
+    builds; `cast(poses, pattern)` returns (range, tri_id) device tensors."""
+
+    def __init__(self, verts=None, tris=None, device=None, build: bool = True, morton_bits: int = 21,
+                 leaf_size: int = 4, stream=None):
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+        h = c_void_p()
+        _check(lib().fgl_scene_create(self.device.index or 0, ctypes.byref(h)))
+        self._h = h
+        self.morton_bits, self.leaf_size = morton_bits, leaf_size
+        self.T = 0
+        if verts is not None:
+            self.upload(verts, tris, stream)
+            if build:
+                self.build(stream=stream)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.fgl_scene_destroy(h)
+            except Exception:
+                pass
+        self._h = None
+
+    __del__ = close
+
+    # ---- upload / build -------------------------------------------------------------------
+    def upload(self, verts, tris, stream=None):
+        on_dev = isinstance(verts, torch.Tensor) and verts.is_cuda
+        if on_dev:
+            v = verts.to(torch.float32).contiguous()
+            t = tris.to(torch.int32).contiguous()
+            kind, pv, pt = DEVICE, v.data_ptr(), t.data_ptr()
+        else:
+            v = np.ascontiguousarray(np.asarray(verts if not isinstance(verts, torch.Tensor) else verts.numpy(),
+                                                dtype=np.float32))
+            t = np.ascontiguousarray(np.asarray(tris if not isinstance(tris, torch.Tensor) else tris.numpy(),
+                                                dtype=np.int32))
+            kind, pv, pt = HOST, v.ctypes.data, t.ctypes.data
+        V = int(v.shape[0]) if v.ndim > 1 else int(v.size) // 3
+        T = int(t.shape[0]) if t.ndim > 1 else int(t.size) // 3
+        _check(lib().fgl_scene_upload_mesh(self._h, pv, V, pt, T, kind, _stream(stream)))
+        self.T, self.V = T, V
+        return self
+
+    def build(self, morton_bits: int | None = None, leaf_size: int | None = None, stream=None):
+        o = BuildOpts(morton_bits or self.morton_bits, leaf_size or self.leaf_size, (c_int32 * 6)())
+        _check(lib().fgl_scene_build(self._h, ctypes.byref(o), _stream(stream)))
+        return self
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().fgl_scene_stats(self._h, ctypes.byref(s)))
+        return dict(triangles=s.triangles, vertices=s.vertices, nodes=s.nodes, device_bytes=s.device_bytes,
+                    scene_lo=list(s.scene_lo), scene_hi=list(s.scene_hi), build_ms=s.build_ms,
+                    morton_bits=s.morton_bits, leaf_size=s.leaf_size)
+
+    # ---- casts -----------------------------------------------------------------------------
+    def cast(self, poses, pattern, first_frame: int = 0, out=None, hit_xyz: bool = False, counts: bool = False,
+             stream=None):
+        """Cast every beam of `pattern` from every pose. Returns dict(range, tri_id[, hit_xyz,
+        node_counts, tri_counts]) of device tensors shaped [P][C][A] (spinning) or [P][N]."""
+        dev = self.device
+        poses = _dev(poses, torch.float32, dev).reshape(-1, 3, 4)
+        P = int(poses.shape[0])
+        if is_spinning(pattern):
+            shape = (P, len(pattern.elev_deg), int(pattern.columns))
+        else:
+            shape = (P, int(pattern.points_per_frame))
+        if out is None:
+            out = {}
+        rng = out.get("range")
+        if rng is None:
+            rng = torch.empty(shape, dtype=torch.float32, device=dev)
+        tid = out.get("tri_id")
+        if tid is None:
+            tid = torch.empty(shape, dtype=torch.int32, device=dev)
+        hx = torch.empty(shape + (3,), dtype=torch.float32, device=dev) if hit_xyz else None
+        nc = torch.empty(shape, dtype=torch.int32, device=dev) if counts else None
+        tc = torch.empty(shape, dtype=torch.int32, device=dev) if counts else None
+        st = _stream(stream)
+        if is_spinning(pattern):
+            s = spinning_struct(pattern)
+            _check(lib().fgl_cast_spinning(self._h, ctypes.byref(s), poses.data_ptr(), P, rng.data_ptr(),
+                                           tid.data_ptr(), _ptr(hx), _ptr(nc), _ptr(tc), st))
+        else:
+            s = rosette_struct(pattern)
+            _check(lib().fgl_cast_rosette(self._h, ctypes.byref(s), poses.data_ptr(), P, int(first_frame),
+                                          rng.data_ptr(), tid.data_ptr(), _ptr(hx), _ptr(nc), _ptr(tc), st))
+        res = dict(range=rng, tri_id=tid)
+        if hit_xyz:
+            res["hit_xyz"] = hx
+        if counts:
+            res["node_counts"], res["tri_counts"] = nc, tc
+        return res
+
+    def cast_rays(self, orig, dir, t_min: float, t_max: float, bruteforce: bool = False, stream=None):
+        o = _dev(orig, torch.float32, self.device, (-1, 3))
+        d = _dev(dir, torch.float32, self.device, (-1, 3))
+        R = int(o.shape[0])
+        rng = torch.empty(R, dtype=torch.float32, device=self.device)
+        tid = torch.empty(R, dtype=torch.int32, device=self.device)
+        f = lib().fgl_cast_rays_bruteforce if bruteforce else lib().fgl_cast_rays
+        _check(f(self._h, o.data_ptr(), d.data_ptr(), R, float(t_min), float(t_max), rng.data_ptr(), tid.data_ptr(),
+                 _stream(stream)))
+        return rng, tid
+
+    # ---- internals for parity tests ------------------------------------------------------------
+    def export(self, stream=None) -> dict:
+        T = self.T
+        nin = max(T - 1, 0)
+        a = dict(scene_box=np.zeros(6, np.float32), codes=np.zeros(T, np.uint64), sorted_keys=np.zeros(T, np.uint64),
+                 perm=np.zeros(T, np.uint32), child=np.zeros((nin, 2), np.int32), range=np.zeros((nin, 2), np.int32),
+                 leaf_box=np.zeros((T, 6), np.float32), node_box=np.zeros((nin, 6), np.float32),
+                 tri48=np.zeros((T, 12), np.float32), nodes=np.zeros((max(nin, 1), 16), np.float32))
+        e = ExportC(*[a[n].ctypes.data for n, _ in ExportC._fields_])
+        _check(lib().fgl_scene_export(self._h, ctypes.byref(e), _stream(stream)))
+        return a
+
+
+def export_rays(pattern, poses, first_frame: int = 0, device=None, stream=None):
+    """The exact float32 (origin, direction) the cast kernels generate, in output order."""
+    device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    poses = _dev(poses, torch.float32, device).reshape(-1, 3, 4)
+    P = int(poses.shape[0])
+    n = P * rays_per_pose(pattern)
+    o = torch.empty((n, 3), dtype=torch.float32, device=device)
+    d = torch.empty((n, 3), dtype=torch.float32, device=device)
+    if is_spinning(pattern):
+        s = spinning_struct(pattern)
+        _check(lib().fgl_export_rays_spinning(ctypes.byref(s), poses.data_ptr(), P, o.data_ptr(), d.data_ptr(),
+                                              _stream(stream)))
+    else:
+        s = rosette_struct(pattern)
+        _check(lib().fgl_export_rays_rosette(ctypes.byref(s), poses.data_ptr(), P, int(first_frame), o.data_ptr(),
+                                             d.data_ptr(), _stream(stream)))
+    return o, d
+
+
+def morton_codes(points: torch.Tensor, lo, hi, bits: int = 21, stream=None) -> torch.Tensor:
+    p = points.to(torch.float32).contiguous().reshape(-1, 3)
+    out = torch.empty(p.shape[0], dtype=torch.int64, device=p.device)
+    lo = np.ascontiguousarray(lo, np.float32)
+    hi = np.ascontiguousarray(hi, np.float32)
+    _check(lib().fgl_morton_codes(p.data_ptr(), int(p.shape[0]), lo.ctypes.data, hi.ctypes.data, int(bits),
+                                  out.data_ptr(), _stream(stream)))
+    return out  # uint64 bit patterns in an int64 tensor
+
+
+def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, key_bits: int = 64, stream=None):
+    """Stable radix sort in place of (uint64 key bit patterns in int64, int32/uint32 values)."""
+    assert keys.dtype == torch.int64 and vals.dtype in (torch.int32, torch.uint32)
+    assert keys.is_contiguous() and vals.is_contiguous() and keys.numel() == vals.numel()
+    _check(lib().fgl_sort_pairs(keys.data_ptr(), vals.data_ptr(), int(keys.numel()), int(key_bits), _stream(stream)))
+    return keys, vals
+
+
+def kernel_launches() -> int:
+    """Kernels libfgl.so has launched in this process (the bench's gpu_launches evidence)."""
+    return int(lib().fgl_kernel_launches())
+
+
+def version() -> str:
+    return lib().fgl_version().decode()

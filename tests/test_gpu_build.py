@@ -1,0 +1,143 @@
+"""GPU parity of the LBVH build rows (§IV-A, Eqs. 5-7) against the oracle,
+through the C ABI: Morton codes, the stable radix sort, the Karras radix tree and the Eq. 7
+refit must be bit-exact; the leaf-order triangle records and the traversal nodes are checked
+element by element against the oracle's tree."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fgl():
+    import paper_2509_17390_b200 as f
+    f.lib()
+    return f
+
+
+def _meshes():
+    return {
+        "tiny1": synth.Mesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 2]], np.float32), np.array([[0, 1, 2]], np.int32)),
+        "tiny2": synth.Mesh(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0]], np.float32),
+                            np.array([[0, 1, 2], [1, 3, 2]], np.int32)),
+        "dups": synth.Mesh(np.tile(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], np.float32), (50, 1)),
+                           np.arange(150, dtype=np.int32).reshape(50, 3)),
+        "c1": synth.scene_c1(),
+        "soup": synth.soup(20011, seed=7),
+    }
+
+
+def _decode_nodes(nodes, T, leaf_size):
+    """Walk the traversal nodes (DESIGN.md §5 node64 layout) from the root; return the list of
+    (box of child, ('leaf', first, count) | ('node', idx)) per visited slot, and leaf coverage."""
+    f = nodes.view(np.float32).reshape(-1, 16)
+    ii = nodes.view(np.int32).reshape(-1, 16)
+    cover = np.zeros(T, np.int32)
+    out = []
+    stack = [0]
+    while stack:
+        i = stack.pop()
+        a, b, c, d = f[i, 0:4], f[i, 4:8], f[i, 8:12], ii[i, 12:16]
+        boxes = [np.array([a[0], a[2], c[0], a[1], a[3], c[1]]), np.array([b[0], b[2], c[2], b[1], b[3], c[3]])]
+        for s in range(2):
+            ref = int(d[s])
+            if ref == -2 ** 31:
+                continue
+            if ref >= 0:
+                out.append((boxes[s], ("node", ref)))
+                stack.append(ref)
+            else:
+                v = ~ref
+                first, cnt = v >> 3, (v & 7) + 1
+                assert cnt <= leaf_size
+                cover[first:first + cnt] += 1
+                out.append((boxes[s], ("leaf", first, cnt)))
+    return out, cover
+
+
+@pytest.mark.parametrize("name", ["tiny1", "tiny2", "dups", "c1", "soup"])
+@pytest.mark.parametrize("leaf_size", [1, 4, 8])
+def test_build_matches_oracle(fgl, name, leaf_size):
+    m = _meshes()[name]
+    s = fgl.Scene(m.verts, m.tris, leaf_size=leaf_size)
+    g = s.export()
+    o = oracle.lbvh(m.verts, m.tris)
+    T = m.T
+    assert np.array_equal(g["scene_box"][:3], o["lo"]) and np.array_equal(g["scene_box"][3:], o["hi"])
+    assert np.array_equal(g["codes"], o["code"])                       # Eq. 5
+    assert np.array_equal(g["sorted_keys"], o["sorted_keys"])          # sort: keys
+    assert np.array_equal(g["perm"], o["perm"])                        # sort: stable order
+    assert np.array_equal(g["child"], o["child"])                      # Eq. 6 radix tree
+    assert np.array_equal(g["range"], o["range"])
+    assert np.array_equal(g["leaf_box"], o["leaf_box"])                # Eq. 7 leaves
+    assert np.array_equal(g["node_box"], o["node_box"])                # Eq. 7 unions
+    # leaf-order triangle records: exact input vertices + original id
+    tri = g["tri48"].reshape(T, 3, 4)
+    assert np.array_equal(tri[:, :, :3], m.verts[m.tris[o["perm"]]])
+    assert np.array_equal(tri[:, 0, 3].view(np.int32), o["perm"].astype(np.int32))
+    # traversal nodes: every reachable child box is the exact union of its triangles, leaves cover
+    # every sorted position exactly once
+    visited, cover = _decode_nodes(g["nodes"], T, leaf_size)
+    assert np.all(cover == 1)
+    V = m.verts[m.tris[o["perm"]]]
+    for box, ref in visited:
+        if ref[0] == "leaf":
+            f, c = ref[1], ref[2]
+        else:
+            f, l = o["range"][ref[1]]
+            c = l - f + 1
+            assert c > leaf_size
+        sub = V[f:f + c].reshape(-1, 3)
+        assert np.array_equal(box, np.concatenate([sub.min(0), sub.max(0)]))
+
+
+def test_build_is_deterministic(fgl):
+    m = synth.soup(5000, seed=1)
+    a = fgl.Scene(m.verts, m.tris).export()
+    b = fgl.Scene(m.verts, m.tris).export()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_build_rooms_full_size(fgl):
+    m = synth.scene_rooms(2)
+    s = fgl.Scene(m.verts, m.tris)
+    g = s.export()
+    o = oracle.lbvh(m.verts, m.tris)
+    for k_g, k_o in (("codes", "code"), ("sorted_keys", "sorted_keys"), ("perm", "perm"), ("child", "child"),
+                     ("range", "range"), ("leaf_box", "leaf_box"), ("node_box", "node_box")):
+        assert np.array_equal(g[k_g], o[k_o]), k_g
+    st = s.stats()
+    assert st["triangles"] == m.T and st["build_ms"] > 0
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4095, 4096, 4097, 100_003, 1_000_000])
+@pytest.mark.parametrize("bits", [8, 30, 63, 64])
+def test_sort_pairs_matches_oracle(fgl, n, bits):
+    rng = np.random.default_rng(n + bits)
+    hi = 2 ** bits if bits < 64 else 2 ** 64
+    keys = rng.integers(0, min(hi, 2 ** 63), size=n, dtype=np.uint64)
+    if bits == 64:
+        keys |= (rng.integers(0, 2, size=n).astype(np.uint64) << np.uint64(63))
+    if n > 10:
+        keys[: n // 3] = keys[n // 3: 2 * (n // 3)]  # plenty of duplicates
+    vals = np.arange(n, dtype=np.uint32)
+    k = torch.from_numpy(keys.view(np.int64).copy()).cuda()
+    v = torch.from_numpy(vals.view(np.int32).copy()).cuda()
+    fgl.sort_pairs(k, v, key_bits=bits)
+    sk, perm = oracle.stable_sort(keys)
+    assert np.array_equal(k.cpu().numpy().view(np.uint64), sk)
+    assert np.array_equal(v.cpu().numpy().view(np.uint32), perm)
+
+
+def test_morton_primitive_matches_oracle(fgl):
+    rng = np.random.default_rng(5)
+    pts = rng.normal(size=(50000, 3)).astype(np.float32)
+    lo, hi = oracle.scene_box(pts)
+    for bits in (1, 7, 10, 21):
+        g = fgl.morton_codes(torch.from_numpy(pts).cuda(), lo, hi, bits).cpu().numpy().view(np.uint64)
+        assert np.array_equal(g, oracle.morton(pts, lo, hi, bits))

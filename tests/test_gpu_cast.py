@@ -1,0 +1,262 @@
+"""GPU parity of the cast rows (raygen A8, traversal A9, watertight leaf test A10, output A11 of
+SURVEY §8(a); Eqs. 19-20) against the CPU oracle, through the C ABI.
+
+Gate (north star + DESIGN.md §4): on every ray the oracle classifies as unambiguous the GPU
+tri_id equals the oracle's exactly and |range - t*| <= 1e-4 t* + 1e-5 m; on ambiguous rays the
+GPU answer is one of the oracle's candidates (or a permitted miss); ambiguous rays <= 1%.
+Mode B feeds the oracle the exact float32 rays the kernel generated (fgl_export_rays_*);
+mode A lets the oracle generate its own rays in double (checks the ray generator too)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fgl():
+    import paper_2509_17390_b200 as f
+    f.lib()
+    return f
+
+
+_cache = {}
+
+
+def _cfg(name, **kw):
+    key = (name, tuple(sorted(kw.items())))
+    if key not in _cache:
+        _cache[key] = synth.config(name, **kw)
+    return _cache[key]
+
+
+def _scene(fgl, mesh, **kw):
+    key = ("scene", id(mesh), tuple(sorted(kw.items())))
+    if key not in _cache:
+        _cache[key] = fgl.Scene(mesh.verts, mesh.tris, **kw)
+    return _cache[key]
+
+
+def _assert_parity(verdict, rng, tid, max_amb=0.01, label=""):
+    j = oracle.judge(verdict, rng, tid)
+    amb = j["ambiguous"] / max(j["n"], 1)
+    msg = f"{label}: n={j['n']} ambiguous={j['ambiguous']} unamb_mismatch={len(j['unamb_mismatch'])} " \
+          f"amb_outside={len(j['amb_outside'])}"
+    if len(j["unamb_mismatch"]):
+        r = j["unamb_mismatch"][:5]
+        msg += f" first: gpu={list(zip(rng[r], tid[r]))} oracle={list(zip(verdict.t1[r], verdict.k1[r]))}"
+    assert len(j["unamb_mismatch"]) == 0, msg
+    assert len(j["amb_outside"]) == 0, msg
+    assert amb <= max_amb, msg
+    return j
+
+
+def _sample(n_total, n, seed):
+    if n >= n_total:
+        return np.arange(n_total)
+    return np.sort(np.random.default_rng(seed).choice(n_total, n, replace=False))
+
+
+def _run(fgl, cfg, n_sample=None, seed=0, first_frame=0, mode="B", **scene_kw):
+    m, pat, poses = cfg["mesh"], cfg["pattern"], cfg["poses"]
+    s = _scene(fgl, m, **scene_kw)
+    res = s.cast(poses, pat, first_frame=first_frame)
+    rng = res["range"].reshape(-1).cpu().numpy()
+    tid = res["tri_id"].reshape(-1).cpu().numpy()
+    idx = _sample(rng.shape[0], n_sample or rng.shape[0], seed)
+    if mode == "B":
+        o, d = fgl.export_rays(pat, poses, first_frame=first_frame)
+        o = o.cpu().numpy().astype(np.float64)[idx]
+        d = d.cpu().numpy().astype(np.float64)[idx]
+        eps = oracle.EPS_MODE_B
+    else:
+        o, d = oracle.pattern_rays(pat, poses, first_frame)
+        o, d = o[idx], d[idx]
+        eps = oracle.EPS_MODE_A
+    v = oracle.cast_and_classify(m.verts, m.tris, o, d, pat.t_min, pat.t_max, eps_rel=eps)
+    return v, rng[idx], tid[idx], res
+
+
+# ---------------------------------------------------------------------------------------------
+def test_raygen_spinning_matches_oracle(fgl):
+    for name, cols in (("VLP16", 360), ("HDL64", 2048), ("OS128", 2048)):
+        pat = synth.spinning_preset(name, cols, az0_deg=1.25)
+        poses = synth.random_poses(3, 2, (-100, -100, -5), (100, 100, 5))
+        o, d = fgl.export_rays(pat, poses)
+        oo, dd = oracle.pattern_rays(pat, poses)
+        assert np.array_equal(o.cpu().numpy().astype(np.float64), oo)     # x_s = t_s exactly
+        err = np.abs(d.cpu().numpy().astype(np.float64) - dd).max()
+        assert err < 4e-7, (name, err)                                      # a few float32 ulps
+
+
+def test_raygen_rosette_matches_oracle(fgl):
+    ros = synth.rosette_default()
+    poses = synth.random_poses(2, 3, (-1, -1, -1), (1, 1, 1))
+    for ff in (0, 999, 123456789):
+        o, d = fgl.export_rays(ros, poses, first_frame=ff)
+        oo, dd = oracle.pattern_rays(ros, poses, ff)
+        assert np.abs(d.cpu().numpy().astype(np.float64) - dd).max() < 2e-6
+        assert np.array_equal(o.cpu().numpy().astype(np.float64), oo)
+
+
+@pytest.mark.parametrize("mode", ["A", "B"])
+def test_c1_all_rays(fgl, mode):
+    v, rng, tid, _ = _run(fgl, _cfg("C1"), mode=mode)
+    assert np.all(tid >= 0)  # sensor inside a closed sphere: every beam returns
+    _assert_parity(v, rng, tid, label=f"C1 mode {mode}")
+
+
+@pytest.mark.parametrize("leaf_size", [1, 2, 4, 8])
+def test_c1_leaf_sizes_identical(fgl, leaf_size):
+    cfg = _cfg("C1")
+    ref = _scene(fgl, cfg["mesh"]).cast(cfg["poses"], cfg["pattern"])
+    got = _scene(fgl, cfg["mesh"], leaf_size=leaf_size).cast(cfg["poses"], cfg["pattern"])
+    assert torch.equal(ref["tri_id"], got["tri_id"]) and torch.equal(ref["range"], got["range"])
+
+
+def test_bvh_equals_gpu_bruteforce(fgl):
+    """The BVH cast and the naive O(N_r T) GPU cast share the leaf test, so their
+    results must be identical bit for bit: pruning never changes the answer."""
+    for m, n in ((synth.scene_c1(), 20000), (synth.soup(30000, seed=11), 20000)):
+        s = fgl.Scene(m.verts, m.tris)
+        rng = np.random.default_rng(0)
+        c = m.verts.mean(0)
+        o = (c + rng.normal(size=(n, 3)) * 3).astype(np.float32)
+        d = rng.normal(size=(n, 3))
+        d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+        r1, t1 = s.cast_rays(o, d, 0.1, 200.0)
+        r2, t2 = s.cast_rays(o, d, 0.1, 200.0, bruteforce=True)
+        assert torch.equal(t1, t2)
+        assert torch.equal(r1, r2)
+
+
+def test_c2_rooms_sampled(fgl):
+    v, rng, tid, res = _run(fgl, _cfg("C2"), n_sample=2048, seed=2)
+    _assert_parity(v, rng, tid, label="C2")
+    full = res["tri_id"].reshape(-1)
+    # a sensor inside closed rooms sees walls in every direction (doors lead to other rooms)
+    assert (full >= 0).float().mean().item() > 0.999
+
+
+def test_c2_throughput_batch_sampled(fgl):
+    v, rng, tid, _ = _run(fgl, _cfg("C2", poses=8), n_sample=1024, seed=3)
+    _assert_parity(v, rng, tid, label="C2x8")
+
+
+def test_c3_terrain_sampled(fgl):
+    v, rng, tid, _ = _run(fgl, _cfg("C3"), n_sample=384, seed=4)
+    _assert_parity(v, rng, tid, label="C3")
+
+
+def test_c4_rosette_sampled(fgl):
+    cfg = _cfg("C4", poses=5)
+    v, rng, tid, _ = _run(fgl, cfg, n_sample=1500, seed=5, first_frame=17)
+    _assert_parity(v, rng, tid, label="C4")
+    va, rnga, tida, _ = _run(fgl, cfg, n_sample=1500, seed=5, first_frame=17, mode="A")
+    _assert_parity(va, rnga, tida, label="C4 mode A")
+
+
+def test_c5_multi_pose_sampled(fgl):
+    cfg = _cfg("C5", poses=4)
+    v, rng, tid, _ = _run(fgl, cfg, n_sample=384, seed=6)
+    _assert_parity(v, rng, tid, label="C5")
+
+
+def test_soup_random_rays_and_ragged_tiles(fgl):
+    m = synth.soup(100_000, seed=7)
+    s = fgl.Scene(m.verts, m.tris)
+    rng = np.random.default_rng(1)
+    R = 1000 + 17  # ragged last tile
+    o = rng.uniform(-2, 12, size=(R, 3)).astype(np.float32)
+    tgt = m.verts[m.tris[rng.integers(0, m.T, R)]].mean(1)
+    d = (tgt - o)
+    d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
+    r, t = s.cast_rays(o, d, 0.0, 1e3)
+    v = oracle.cast_and_classify(m.verts, m.tris, o.astype(np.float64), d.astype(np.float64), 0.0, 1e3)
+    _assert_parity(v, r.cpu().numpy(), t.cpu().numpy(), label="soup")
+
+
+# ---------------------------------------------------------------------------------------------
+def test_edge_cases(fgl):
+    V = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0]], np.float32)
+    Tr = np.array([[0, 1, 2], [1, 3, 2]], np.int32)
+    s = fgl.Scene(V, Tr)
+    o = np.array([[0.25, 0.25, 2], [0.75, 0.75, 2], [0.5, 0.5, 2], [3, 3, 2], [0.25, 0.25, -3], [0.25, 0.25, 2]],
+                 np.float32)
+    d = np.array([[0, 0, -1], [0, 0, -1], [0, 0, -1], [0, 0, -1], [0, 0, 1], [0, 0, 1]], np.float32)
+    r, t = s.cast_rays(o, d, 0.1, 200.0)
+    t = t.cpu().numpy().tolist()
+    r = r.cpu().numpy()
+    assert t == [0, 1, 0, -1, 0, -1]          # interior, interior, shared edge -> smaller id, miss,
+    assert r[0] == 2.0 and r[4] == 3.0         # back face (two-sided), pointing away
+    assert np.isinf(r[3]) and np.isinf(r[5])
+    # closed interval: t exactly t_min / t_max hits
+    r, t = s.cast_rays(np.array([[0.25, 0.25, 0.5], [0.25, 0.25, 8.0]], np.float32),
+                       np.array([[0, 0, -1], [0, 0, -1]], np.float32), 0.5, 8.0)
+    assert t.cpu().tolist() == [0, 0]
+    # duplicate triangles: the smaller id wins
+    s2 = fgl.Scene(np.tile(V[:3], (3, 1)), np.arange(9, dtype=np.int32).reshape(3, 3))
+    r, t = s2.cast_rays(np.array([[0.2, 0.3, 1]], np.float32), np.array([[0, 0, -1]], np.float32), 0.1, 10)
+    assert t.item() == 0
+    # single-triangle scene and R = 0 / P = 0
+    s3 = fgl.Scene(V[:3], Tr[:1])
+    r, t = s3.cast_rays(np.array([[0.2, 0.3, 1]], np.float32), np.array([[0, 0, -1]], np.float32), 0.1, 10)
+    assert t.item() == 0 and r.item() == 1.0
+    r, t = s3.cast_rays(np.zeros((0, 3), np.float32), np.zeros((0, 3), np.float32), 0.1, 10)
+    assert r.numel() == 0
+    res = s3.cast(np.zeros((0, 3, 4), np.float32), synth.spinning_preset("VLP16"))
+    assert res["range"].shape == (0, 16, 360)
+
+
+def test_outputs_hit_points_and_counts(fgl):
+    cfg = _cfg("C1")
+    s = _scene(fgl, cfg["mesh"])
+    res = s.cast(cfg["poses"], cfg["pattern"], hit_xyz=True, counts=True)
+    plain = s.cast(cfg["poses"], cfg["pattern"])
+    assert torch.equal(res["tri_id"], plain["tri_id"]) and torch.equal(res["range"], plain["range"])
+    o, d = fgl.export_rays(cfg["pattern"], cfg["poses"])
+    x = res["hit_xyz"].reshape(-1, 3).cpu().numpy().astype(np.float64)
+    t = res["range"].reshape(-1).cpu().numpy().astype(np.float64)
+    ref = o.cpu().numpy() + t[:, None] * d.cpu().numpy()
+    assert np.abs(x - ref).max() < 1e-4                    # ||x* - x_s|| = rho (S:443 invariant)
+    nc = res["node_counts"].cpu().numpy()
+    tc = res["tri_counts"].cpu().numpy()
+    assert nc.min() >= 1 and tc.min() >= 1 and tc.mean() < 64  # K_bar << T (Eq. 22)
+
+
+def test_determinism(fgl):
+    cfg = _cfg("C2", poses=2)
+    s = _scene(fgl, cfg["mesh"])
+    a = s.cast(cfg["poses"], cfg["pattern"])
+    b = s.cast(cfg["poses"], cfg["pattern"])
+    assert torch.equal(a["range"], b["range"]) and torch.equal(a["tri_id"], b["tri_id"])
+
+
+def test_error_reporting(fgl):
+    with pytest.raises(fgl.FglError) as e:
+        fgl.Scene(np.zeros((3, 3), np.float32), np.array([[0, 1, 3]], np.int32))
+    assert e.value.status == 2
+    with pytest.raises(fgl.FglError) as e:
+        fgl.Scene(np.array([[0, 0, np.nan]] * 3, np.float32), np.array([[0, 1, 2]], np.int32))
+    assert e.value.status == 2
+    s = fgl.Scene(build=False)
+    with pytest.raises(fgl.FglError) as e:
+        s.upload(np.zeros((3, 3), np.float32), np.zeros((0, 3), np.int32))
+    assert e.value.status == 2
+    m = synth.scene_c1()
+    s.upload(m.verts, m.tris)
+    with pytest.raises(fgl.FglError) as e:
+        s.cast_rays(np.zeros((1, 3), np.float32), np.ones((1, 3), np.float32), 0.1, 1.0)
+    assert e.value.status == 1  # cast before build
+    s.build()
+    bad = synth.Spinning(np.array([0, 5, 1], np.float32), 10)
+    with pytest.raises(fgl.FglError) as e:
+        s.cast(synth.pose((0, 0, 0))[None], bad)
+    assert e.value.status == 1  # non-monotone elevations
+    with pytest.raises(fgl.FglError):
+        s.cast_rays(np.zeros((1, 3), np.float32), np.ones((1, 3), np.float32), 1.0, 0.5)
