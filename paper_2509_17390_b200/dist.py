@@ -1,0 +1,97 @@
+"""Multi-GPU pose sweep: mesh replicated, poses sharded, results all-gathered.
+
+Rays and poses are independent (one thread per beam), so W ranks each build the same
+deterministic LBVH locally (no communication), cast a contiguous block of poses, and exchange
+results with one collective — `all_gather` over NCCL (NVLink / NVSwitch) — chunked so that the
+gather of chunk k overlaps the cast of chunk k+1 on a separate stream.
+
+The shard/chunk arithmetic is plain host logic (tested with gloo, world size 2, on CPU); the
+cast itself is `Scene.cast` (libfgl kernels) unless a test injects `cast_fn`.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+
+def shard_size(P: int, world: int) -> int:
+    """Poses per rank: ceil(P / world) (the last ranks are padded)."""
+    return max(1, math.ceil(P / world)) if P > 0 else 0
+
+
+def shard_range(P: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous pose block [lo, hi) owned by `rank` (may be empty for trailing ranks)."""
+    S = shard_size(P, world)
+    lo = min(P, rank * S)
+    return lo, min(P, lo + S)
+
+
+def chunk_bounds(S: int, chunks: int) -> list[tuple[int, int]]:
+    """Split a shard of S poses into <= chunks contiguous pieces of near-equal size."""
+    if S <= 0:
+        return []
+    chunks = max(1, min(chunks, S))
+    step = math.ceil(S / chunks)
+    return [(a, min(S, a + step)) for a in range(0, S, step)]
+
+
+def sweep(scene, poses: torch.Tensor, pattern, group=None, chunks: int = 4, gather: bool = True,
+          cast_fn=None, first_frame: int = 0):
+    """Cast `pattern` from all P poses across the ranks of `group`.
+
+    Returns dict(range, tri_id) shaped [P][...] on every rank when gather=True, else this rank's
+    shard [hi - lo][...] and its pose range. `cast_fn(poses_chunk, first_frame) -> (range, tri_id)`
+    overrides the cast (tests); by default it is scene.cast."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    P = int(poses.shape[0])
+    S = shard_size(P, world)
+    lo, hi = shard_range(P, world, rank)
+    if cast_fn is None:
+        def cast_fn(p, ff):
+            r = scene.cast(p, pattern, first_frame=ff)
+            return r["range"], r["tri_id"]
+    device = poses.device
+    # this rank's padded shard: real poses [lo, hi), padded with the last real pose (discarded)
+    if hi > lo:
+        idx = torch.arange(lo, lo + S, device=device).clamp_(max=hi - 1)
+    else:
+        idx = torch.zeros(S, dtype=torch.long, device=device)
+    mine = poses.index_select(0, idx)
+    pieces = chunk_bounds(S, chunks)
+    use_streams = device.type == "cuda" and world > 1 and gather
+    comm = torch.cuda.Stream(device=device) if use_streams else None
+    out_r = out_t = None
+    shard_r, shard_t = [], []
+    works = []
+    for (a, b) in pieces:
+        r, t = cast_fn(mine[a:b], first_frame + lo + a)
+        shard_r.append(r)
+        shard_t.append(t)
+        if not gather or world == 1:
+            continue
+        if out_r is None:
+            out_r = torch.empty((world, S) + tuple(r.shape[1:]), dtype=r.dtype, device=r.device)
+            out_t = torch.empty((world, S) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        lr = [out_r[w, a:b] for w in range(world)]
+        lt = [out_t[w, a:b] for w in range(world)]
+        if comm is not None:
+            comm.wait_stream(torch.cuda.current_stream(device))
+            with torch.cuda.stream(comm):
+                works.append(dist.all_gather(lr, r, group=group, async_op=True))
+                works.append(dist.all_gather(lt, t, group=group, async_op=True))
+        else:
+            dist.all_gather(lr, r, group=group)
+            dist.all_gather(lt, t, group=group)
+    for w in works:
+        w.wait()
+    if comm is not None:
+        torch.cuda.current_stream(device).wait_stream(comm)
+    if not gather or world == 1:
+        r = torch.cat(shard_r)[: hi - lo] if shard_r else None
+        t = torch.cat(shard_t)[: hi - lo] if shard_t else None
+        return dict(range=r, tri_id=t, lo=lo, hi=hi)
+    return dict(range=out_r.reshape((world * S,) + tuple(out_r.shape[2:]))[:P],
+                tri_id=out_t.reshape((world * S,) + tuple(out_t.shape[2:]))[:P], lo=0, hi=P)
