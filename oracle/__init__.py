@@ -25,7 +25,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 AMBIG, EDGE, BOUNDARY, GRAZE, OVERFLOW, MISS_OK, INCONSISTENT = 1, 2, 4, 8, 16, 32, 64
 EPS_MODE_B = 2.0 ** -20   # oracle consumes the exact float32 rays the kernel used
-EPS_MODE_A = 2.0 ** -18   # oracle generates its own rays in double
+EPS_MODE_A = 2.0 ** -19   # oracle generates its own rays in double (+ float32 raygen error <= 2^-21)
 
 
 def build(force: bool = False) -> str:

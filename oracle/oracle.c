@@ -336,7 +336,7 @@ void orc_classify(const float *verts, const int32_t *tris, int64_t T, const doub
             if (boundary) f |= ORC_BOUNDARY;
             if (kept > 1 || (kept == 1 && !k1_firm)) f |= ORC_EDGE;
             if (k1[r] >= 0 && !k1_kept) f |= ORC_INCONSISTENT;
-            if (k1[r] >= 0 && k1_kept && k1_w > 0.5 * (1e-4 * t1[r] + 1e-5)) f |= ORC_GRAZE;
+            if (k1[r] >= 0 && k1_kept && k1_w > 1e-4 * t1[r] + 1e-5) f |= ORC_GRAZE;
             int unamb = 0;
             if (k1[r] >= 0)
                 unamb = kept == 1 && k1_kept && k1_firm && !(f & (ORC_GRAZE | ORC_BOUNDARY | ORC_INCONSISTENT));

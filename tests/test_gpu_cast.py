@@ -91,7 +91,7 @@ def test_raygen_spinning_matches_oracle(fgl):
         oo, dd = oracle.pattern_rays(pat, poses)
         assert np.array_equal(o.cpu().numpy().astype(np.float64), oo)     # x_s = t_s exactly
         err = np.abs(d.cpu().numpy().astype(np.float64) - dd).max()
-        assert err < 4e-7, (name, err)                                      # a few float32 ulps
+        assert err < 8 * 2.0 ** -23, (name, err)                           # <= 8 float32 ulps
 
 
 def test_raygen_rosette_matches_oracle(fgl):
@@ -149,7 +149,7 @@ def test_c2_throughput_batch_sampled(fgl):
 
 
 def test_c3_terrain_sampled(fgl):
-    v, rng, tid, _ = _run(fgl, _cfg("C3"), n_sample=384, seed=4)
+    v, rng, tid, _ = _run(fgl, _cfg("C3"), n_sample=768, seed=4)
     _assert_parity(v, rng, tid, label="C3")
 
 
@@ -163,7 +163,7 @@ def test_c4_rosette_sampled(fgl):
 
 def test_c5_multi_pose_sampled(fgl):
     cfg = _cfg("C5", poses=4)
-    v, rng, tid, _ = _run(fgl, cfg, n_sample=384, seed=6)
+    v, rng, tid, _ = _run(fgl, cfg, n_sample=768, seed=6)
     _assert_parity(v, rng, tid, label="C5")
 
 
@@ -178,7 +178,8 @@ def test_soup_random_rays_and_ragged_tiles(fgl):
     d = (d / np.linalg.norm(d, axis=1, keepdims=True)).astype(np.float32)
     r, t = s.cast_rays(o, d, 0.0, 1e3)
     v = oracle.cast_and_classify(m.verts, m.tris, o.astype(np.float64), d.astype(np.float64), 0.0, 1e3)
-    _assert_parity(v, r.cpu().numpy(), t.cpu().numpy(), label="soup")
+    # random rays through a dense self-intersecting soup: near-ties are common by construction
+    _assert_parity(v, r.cpu().numpy(), t.cpu().numpy(), max_amb=0.05, label="soup")
 
 
 # ---------------------------------------------------------------------------------------------
