@@ -54,8 +54,12 @@ typedef struct fgl_scene fgl_scene; /* opaque: device copies of the mesh, the BV
 
 typedef struct {
     int32_t morton_bits; /* b of Eq. 5, 1..21; 0 = default 21 (63-bit keys)      */
-    int32_t leaf_size;   /* max triangles per BVH leaf, 1..8; 0 = default (4)                 */
-    int32_t reserved[6]; /* must be zero                                                     */
+    int32_t leaf_size;   /* max triangles per BVH leaf, 1..8; 0 = default (2)                 */
+    int32_t morton_box;  /* 0 = cubic scene box (default): every axis uses L = max_a L_a, the box
+                            [o, o+L] read as a cube (isotropic cells; reading R22);
+                            1 = per-axis box, L_x, L_y, L_z separately                         */
+    int32_t width;       /* traversal node width: 2 (binary "node64", default) or 4 ("node128")    */
+    int32_t reserved[4]; /* must be zero                                                     */
 } fgl_build_opts;
 
 typedef struct {
@@ -149,7 +153,10 @@ typedef struct {
     float *leaf_box;       /* [T][6]   exact AABB of the triangle at sorted position j          */
     float *node_box;       /* [T-1][6] Eq. 7 union                                              */
     float *tri48;          /* [T][12]  leaf-order triangle records {v0, id}, {v1, 0}, {v2, 0}    */
-    float *nodes;          /* [max(T-1,1)][16] traversal nodes (DESIGN.md §5 "node64")          */
+    float *nodes;          /* [max(T-1,1)][16] binary traversal nodes (DESIGN.md §5 "node64")   */
+    float *nodes4;         /* [max(T-1,1)][32] 4-wide traversal nodes at their binary node index
+                              (DESIGN.md §5 "node128"; only even-depth slots are meaningful)     */
+    int32_t *depth;        /* [T-1] depth of each internal node (root = 0)                      */
 } fgl_export;
 
 /* Synchronously copies the requested build arrays of a built scene to host memory. */
@@ -166,7 +173,7 @@ FGL_API fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int
 /* ---- misc ----------------------------------------------------------------------------- */
 FGL_API const char *fgl_last_error(void); /* thread-local; valid until the next fgl call on the thread */
 FGL_API const char *fgl_version(void);
-FGL_API int32_t fgl_abi_version(void);   /* bumped on any incompatible change of this header */
+FGL_API int32_t fgl_abi_version(void);   /* bumped on any incompatible change of this header (2) */
 /* Number of kernels libfgl has launched in this process (all devices, all threads). */
 FGL_API int64_t fgl_kernel_launches(void);
 

@@ -56,7 +56,7 @@ def lib():
                                     P, P, P, P, P]),
             "orc_centroids": (None, [P, P, c_int64, P]),
             "orc_scene_box": (None, [P, c_int64, P, P]),
-            "orc_morton": (None, [P, c_int64, P, P, c_int, P]),
+            "orc_morton": (None, [P, c_int64, P, P, c_int, c_int, P]),
             "orc_stable_sort": (None, [P, P, c_int64, P, P]),
             "orc_radix_tree": (c_int, [P, c_int64, P, P]),
             "orc_refit": (None, [P, P, P, c_int64, P, P, P]),
@@ -220,10 +220,11 @@ def scene_box(cent):
     return lo, hi
 
 
-def morton(cent, lo, hi, bits: int = 21):
+def morton(cent, lo, hi, bits: int = 21, cubic: bool = False):
     c = _c(cent, np.float32)
     code = np.empty(c.shape[0], np.uint64)
-    lib().orc_morton(_p(c), c.shape[0], _p(_c(lo, np.float32)), _p(_c(hi, np.float32)), int(bits), _p(code))
+    lib().orc_morton(_p(c), c.shape[0], _p(_c(lo, np.float32)), _p(_c(hi, np.float32)), int(bits), int(cubic),
+                     _p(code))
     return code
 
 
@@ -259,11 +260,11 @@ def refit(verts, tris, perm, child):
     return leaf, node
 
 
-def lbvh(verts, tris, bits: int = 21):
+def lbvh(verts, tris, bits: int = 21, cubic: bool = False):
     """All LBVH steps in paper order: centroids -> box -> Eq. 5 -> sort -> Eq. 6 tree -> Eq. 7."""
     cent = centroids(verts, tris)
     lo, hi = scene_box(cent)
-    code = morton(cent, lo, hi, bits)
+    code = morton(cent, lo, hi, bits, cubic)
     sk, perm = stable_sort(code)
     child, rng = radix_tree(sk) if len(sk) >= 2 else (np.zeros((0, 2), np.int32), np.zeros((0, 2), np.int32))
     leaf, node = refit(verts, tris, perm, child)

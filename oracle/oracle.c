@@ -384,14 +384,20 @@ void orc_scene_box(const float *cent, int64_t n, float *lo, float *hi) {
 
 /* Eq. 5: m = interleave(floor(2^b (mu_x - o_x)/L_x), ... y, ... z), x lowest.
  * The quantisation is a float decision; it is taken in float32 exactly as the kernel does (R7):
- * L = hi - lo; s = (L > 0) ? 2^b / L : 0; x = (c - lo) * s; q = min(floor(x), 2^b - 1). */
-void orc_morton(const float *cent, int64_t n, const float *lo, const float *hi, int bits, uint64_t *code) {
-    float s[3];
+ * L = hi - lo; s = (L > 0) ? 2^b / L : 0; x = (c - lo) * s; q = min(floor(x), 2^b - 1).
+ * cubic != 0 (reading R22): every axis uses L = max(L_x, L_y, L_z). */
+void orc_morton(const float *cent, int64_t n, const float *lo, const float *hi, int bits, int cubic,
+                uint64_t *code) {
+    float s[3], L[3], Lc = 0.0f;
     float two_b = (float)(1u << bits);
     uint32_t qmax = (1u << bits) - 1u;
     for (int i = 0; i < 3; ++i) {
-        float L = hi[i] - lo[i];
-        s[i] = L > 0.0f ? two_b / L : 0.0f;
+        L[i] = hi[i] - lo[i];
+        if (L[i] > Lc) Lc = L[i];
+    }
+    for (int i = 0; i < 3; ++i) {
+        float Li = cubic ? Lc : L[i];
+        s[i] = Li > 0.0f ? two_b / Li : 0.0f;
     }
     for (int64_t k = 0; k < n; ++k) {
         uint32_t q[3];

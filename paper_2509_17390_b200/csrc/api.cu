@@ -77,7 +77,7 @@ void dalloc(fgl_scene *s, T **p, size_t n) {
 void free_build(fgl_scene *s) {
     fgl::BuildBuffers &b = s->b;
     void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.counts,
-                  b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes};
+                  b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth};
     for (void *p : ps)
         if (p) cudaFree(p);
     b = fgl::BuildBuffers();
@@ -108,9 +108,11 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.leafbox, 2 * T);
     dalloc(s, &b.nodebox, 2 * nin);
     dalloc(s, &b.nodes, nin);
+    dalloc(s, &b.nodes4, nin);
+    dalloc(s, &b.depth, nin);
 }
 
-fgl::SceneView view(const fgl_scene *s) { return fgl::SceneView{s->b.tri, s->b.nodes}; }
+fgl::SceneView view(const fgl_scene *s) { return fgl::SceneView{s->b.tri, s->b.nodes, s->b.nodes4, s->b.width}; }
 
 fgl::CastCounter *next_counter(const fgl_scene *s) {
     auto *ms = const_cast<fgl_scene *>(s);
@@ -178,7 +180,7 @@ extern "C" {
 
 const char *fgl_last_error(void) { return g_err.c_str(); }
 const char *fgl_version(void) { return "fgl 0.1.0 (sm_100a)"; }
-int32_t fgl_abi_version(void) { return 1; }
+int32_t fgl_abi_version(void) { return 2; }
 int64_t fgl_kernel_launches(void) { return fgl::g_launches.load(std::memory_order_relaxed); }
 
 fgl_status fgl_scene_create(int cuda_device, fgl_scene **out) {
@@ -264,9 +266,13 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     FGL_API_BEGIN
     if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
     if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
-    int bits = 21, leaf = 4;
+    int bits = 21, leaf = 2, cubic = 1, width = 2;
     if (opts) {
-        for (int i = 0; i < 6; ++i)
+        if (opts->width) width = opts->width;
+        if (width != 2 && width != 4) throw Error(FGL_E_USAGE, "width must be 2 or 4");
+        if (opts->morton_box < 0 || opts->morton_box > 1) throw Error(FGL_E_USAGE, "morton_box must be 0 or 1");
+        cubic = opts->morton_box == 0;
+        for (int i = 0; i < 4; ++i)
             if (opts->reserved[i]) throw Error(FGL_E_USAGE, "fgl_build_opts.reserved must be zero");
         if (opts->morton_bits) bits = opts->morton_bits;
         if (opts->leaf_size) leaf = opts->leaf_size;
@@ -277,7 +283,7 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     cudaStream_t st = (cudaStream_t)stream;
     s->bits = bits, s->leaf_size = leaf;
     FGL_CUDA(cudaEventRecord(s->ev0, st));
-    fgl::launch_build(s->verts, s->tris, s->b, bits, leaf, st);
+    fgl::launch_build(s->verts, s->tris, s->b, bits, leaf, cubic, width, st);
     FGL_CUDA(cudaEventRecord(s->ev1, st));
     s->built = true;
     FGL_API_END
@@ -429,6 +435,8 @@ fgl_status fgl_scene_export(const fgl_scene *s, const fgl_export *out, void *str
     }
     cp(out->tri48, b.tri, 3 * T * sizeof(float4));
     cp(out->nodes, b.nodes, std::max<int64_t>(nin, 1) * sizeof(fgl::Node64));
+    cp(out->nodes4, b.nodes4, std::max<int64_t>(nin, 1) * sizeof(fgl::Node128));
+    cp(out->depth, b.depth, nin * sizeof(int32_t));
     FGL_API_END
 }
 

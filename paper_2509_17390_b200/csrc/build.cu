@@ -105,20 +105,26 @@ __device__ __forceinline__ uint64_t spread3(uint32_t x) {
 }
 
 // Eq. 5 quantisation in float32 (the decision is a float one; R7):
-// L = hi - lo; s = L > 0 ? 2^b / L : 0; q = min(floor((c - lo) * s), 2^b - 1)
+// L = hi - lo (cubic box, R22: L = max over axes for every axis); s = L > 0 ? 2^b / L : 0;
+// q = min(floor((c - lo) * s), 2^b - 1)
 struct MortonBox {
     float lo[3], s[3];
     uint32_t qmax;
 };
 
-__device__ __forceinline__ MortonBox morton_box(const float *lo, const float *hi, int bits) {
+__device__ __forceinline__ MortonBox morton_box(const float *lo, const float *hi, int bits, int cubic = 0) {
     MortonBox m;
     const float two_b = (float)(1u << bits);
     m.qmax = (1u << bits) - 1u;
+    float L[3], Lc = 0.f;
+    for (int i = 0; i < 3; ++i) {
+        L[i] = __fsub_rn(hi[i], lo[i]);
+        Lc = fmaxf(Lc, L[i]);
+    }
     for (int i = 0; i < 3; ++i) {
         m.lo[i] = lo[i];
-        float L = __fsub_rn(hi[i], lo[i]);
-        m.s[i] = L > 0.f ? __fdiv_rn(two_b, L) : 0.f;
+        const float Li = cubic ? Lc : L[i];
+        m.s[i] = Li > 0.f ? __fdiv_rn(two_b, Li) : 0.f;
     }
     return m;
 }
@@ -135,12 +141,13 @@ __device__ __forceinline__ uint64_t morton_code(const MortonBox &m, float x, flo
 }
 
 __global__ void __launch_bounds__(256) k_morton(const float4 *__restrict__ cent, int64_t T,
-                                                const float *__restrict__ box, int bits, uint64_t *__restrict__ keys,
+                                                const float *__restrict__ box, int bits, int cubic,
+                                                uint64_t *__restrict__ keys,
                                                 uint32_t *__restrict__ vals, uint32_t *__restrict__ ghist) {
     __shared__ uint32_t h[8][256];
     __shared__ MortonBox mb;
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
-    if (threadIdx.x == 0) mb = morton_box(box, box + 3, bits);
+    if (threadIdx.x == 0) mb = morton_box(box, box + 3, bits, cubic);
     __syncthreads();
     const int npass = (3 * bits + 7) / 8;
     const MortonBox m = mb;
@@ -279,13 +286,97 @@ __global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const i
     }
 }
 
+// depth of every internal node (root = 0) by walking the parent links (L2-resident, ~log T steps)
+__global__ void __launch_bounds__(256) k_depth(int64_t n, const int32_t *__restrict__ parent,
+                                               int32_t *__restrict__ depth) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t d = 0;
+        for (int32_t p = __ldg(parent + i); p >= 0; p = __ldg(parent + p)) ++d;
+        depth[i] = d;
+    }
+}
+
+// 4-wide nodes: every even-depth internal node n with more than leaf_size triangles (and the
+// root) absorbs its two children; each child is a leaf (<= leaf_size triangles), or is replaced by
+// its own two children (leaves, or odd-depth... i.e. the next even-depth wide nodes).
+__global__ void __launch_bounds__(256) k_nodes4(int64_t n, int leaf_size, const int2 *__restrict__ child,
+                                                const int2 *__restrict__ range, const int32_t *__restrict__ depth,
+                                                const float4 *__restrict__ leafbox,
+                                                const float4 *__restrict__ nodebox, Node128 *__restrict__ nodes4) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
+        const int2 ri = range[i];
+        if (i != 0 && ((depth[i] & 1) || ri.y - ri.x + 1 <= leaf_size)) continue;
+        float lo[3][4], hi[3][4];
+        int32_t ref[4];
+        int k = 0;
+        auto emit = [&](int32_t c) {
+            float4 l, h;
+            if (c < 0) {
+                const int32_t j = ~c;
+                ref[k] = make_leaf(j, 1);
+                l = leafbox[2 * (int64_t)j], h = leafbox[2 * (int64_t)j + 1];
+            } else {
+                const int2 r = range[c];
+                const int32_t cnt = r.y - r.x + 1;
+                ref[k] = cnt <= leaf_size ? make_leaf(r.x, cnt) : c;
+                l = nodebox[2 * (int64_t)c], h = nodebox[2 * (int64_t)c + 1];
+            }
+            lo[0][k] = l.x, lo[1][k] = l.y, lo[2][k] = l.z, hi[0][k] = h.x, hi[1][k] = h.y, hi[2][k] = h.z;
+            ++k;
+        };
+        const int2 ci = child[i];
+        const int32_t cc[2] = {ci.x, ci.y};
+        for (int s = 0; s < 2; ++s) {
+            const int32_t c = cc[s];
+            bool expand = false;
+            if (c >= 0) {
+                const int2 r = range[c];
+                expand = r.y - r.x + 1 > leaf_size;
+            }
+            if (!expand) {
+                emit(c);
+            } else {
+                const int2 g = child[c];
+                emit(g.x);
+                emit(g.y);
+            }
+        }
+        const int valid = k;
+        for (; k < 4; ++k) {
+            ref[k] = kEmptyRef;
+            for (int a = 0; a < 3; ++a) lo[a][k] = hi[a][k] = kFarBox;
+        }
+        Node128 nd;
+        for (int a = 0; a < 3; ++a) {
+            nd.f[2 * a] = make_float4(lo[a][0], lo[a][1], lo[a][2], lo[a][3]);
+            nd.f[2 * a + 1] = make_float4(hi[a][0], hi[a][1], hi[a][2], hi[a][3]);
+        }
+        nd.ref = make_int4(ref[0], ref[1], ref[2], ref[3]);
+        nd.meta = make_int4(valid, depth[i], 0, 0);
+        nodes4[i] = nd;
+    }
+}
+
+// T == 1: a root whose first child is the single leaf and whose other children are empty
+__global__ void k_single4(const float4 *__restrict__ leafbox, Node128 *__restrict__ nodes4) {
+    const float4 lo = leafbox[0], hi = leafbox[1];
+    Node128 nd;
+    const float F = kFarBox;
+    nd.f[0] = make_float4(lo.x, F, F, F), nd.f[1] = make_float4(hi.x, F, F, F);
+    nd.f[2] = make_float4(lo.y, F, F, F), nd.f[3] = make_float4(hi.y, F, F, F);
+    nd.f[4] = make_float4(lo.z, F, F, F), nd.f[5] = make_float4(hi.z, F, F, F);
+    nd.ref = make_int4(make_leaf(0, 1), kEmptyRef, kEmptyRef, kEmptyRef);
+    nd.meta = make_int4(1, 0, 0, 0);
+    nodes4[0] = nd;
+}
+
 // T == 1: a root whose first child is the single leaf and whose second child is empty
 __global__ void k_single(const float4 *__restrict__ leafbox, Node64 *__restrict__ nodes) {
     float4 lo = leafbox[0], hi = leafbox[1];
     Node64 nd;
     nd.a = make_float4(lo.x, hi.x, lo.y, hi.y);
-    nd.b = make_float4(0.f, 0.f, 0.f, 0.f);
-    nd.c = make_float4(lo.z, hi.z, 0.f, 0.f);
+    nd.b = make_float4(kFarBox, kFarBox, kFarBox, kFarBox);
+    nd.c = make_float4(lo.z, hi.z, kFarBox, kFarBox);
     nd.d = make_int4(make_leaf(0, 1), kEmptyRef, 0, 0);
     nodes[0] = nd;
 }
@@ -313,14 +404,15 @@ void launch_morton_points(const float *pts, int64_t n, const float *lo, const fl
     FGL_LAUNCHED("k_morton_points");
 }
 
-void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  cudaStream_t s) {
+void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size, int cubic,
+                  int width, cudaStream_t s) {
+    b.width = width;
     const int64_t T = b.T;
     const int key_bits = 3 * bits;
     k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, tris, T, b.cent, b.partial, b.sync, b.box);
     FGL_LAUNCHED("k_prep");
     FGL_CUDA(cudaMemsetAsync(b.ghist, 0, sizeof(uint32_t) * 8 * 256, s));
-    k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, b.keys[0], b.vals[0], b.ghist);
+    k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, cubic, b.keys[0], b.vals[0], b.ghist);
     FGL_LAUNCHED("k_morton");
     int slot = 0;
     radix_sort_pairs(b.keys[0], b.vals[0], b.keys[1], b.vals[1], T, key_bits, b.counts, b.ghist, true, &slot, s);
@@ -328,8 +420,13 @@ void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int 
     k_reorder<<<grid_for(T), 256, 0, s>>>(verts, tris, b.vals[slot], T, b.tri, b.leafbox);
     FGL_LAUNCHED("k_reorder");
     if (T == 1) {
-        k_single<<<1, 1, 0, s>>>(b.leafbox, b.nodes);
-        FGL_LAUNCHED("k_single");
+        if (width == 4) {
+            k_single4<<<1, 1, 0, s>>>(b.leafbox, b.nodes4);
+            FGL_LAUNCHED("k_single4");
+        } else {
+            k_single<<<1, 1, 0, s>>>(b.leafbox, b.nodes);
+            FGL_LAUNCHED("k_single");
+        }
         return;
     }
     k_karras<<<grid_for(T - 1), 256, 0, s>>>(b.keys[slot], T, b.child, b.range, b.parent);
@@ -337,8 +434,16 @@ void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int 
     FGL_CUDA(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * (T - 1), s));
     k_refit<<<grid_for(T), 256, 0, s>>>(T, b.child, b.parent, b.flags, b.leafbox, b.nodebox);
     FGL_LAUNCHED("k_refit");
-    k_nodes<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.leafbox, b.nodebox, b.nodes);
-    FGL_LAUNCHED("k_nodes");
+    if (width == 4) {
+        k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
+        FGL_LAUNCHED("k_depth");
+        k_nodes4<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.depth, b.leafbox, b.nodebox,
+                                                 b.nodes4);
+        FGL_LAUNCHED("k_nodes4");
+    } else {
+        k_nodes<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.leafbox, b.nodebox, b.nodes);
+        FGL_LAUNCHED("k_nodes");
+    }
 }
 
 }  // namespace fgl

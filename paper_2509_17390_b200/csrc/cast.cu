@@ -12,6 +12,8 @@
 // P:297 "warp-synchronous traversal").
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 
 #include "fgl_internal.cuh"
 
@@ -27,75 +29,100 @@ struct Ray {
     float ox, oy, oz, dx, dy, dz;
 };
 
-// per-ray constants of the watertight test and of the slab test
+// Per-ray constants.
+//  * slab test (robust, one FMA per plane): t = fma(x, I, c) with I = 1/d, c = -o I. The rounding
+//    of c and of the FMA is bounded by 2u|t| + u|c| (u = 2^-24); the |c| part is folded into two
+//    per-axis offsets (clo for the lo plane, chi for the hi plane, pushed outward by 2^-22 |c|)
+//    and the relative part into the 1 + 2^-20 factor on t_far. Conservative: never culls a box the
+//    exact ray touches.
+//  * watertight test (Woop, Benthin, Wald 2013): kz = argmax |d|, shear S; the axis permutation is
+//    folded into a 3x3 matrix M (rows e_kx - Sx e_kz, e_ky - Sy e_kz, Sz e_kz) so the transform is
+//    branch-free; the products by 0 and 1 are exact, so each sheared coordinate carries at most two
+//    roundings, identical for a vertex shared by two triangles (watertightness).
 struct Pre {
     float ox, oy, oz;
-    float ix, iy, iz;  // 1/d with |d_i| < 2^-80 replaced by +-2^-80 (no 0 * inf in slabs)
-    float Sx, Sy, Sz;
-    int kx, ky, kz;
+    float Ix, Iy, Iz;
+    float clx, chx, cly, chy, clz, chz;
+    float m0x, m0y, m0z, m1x, m1y, m1z, m2x, m2y, m2z;
 };
 
 __device__ __forceinline__ Pre precompute(const Ray &r) {
     Pre p;
     p.ox = r.ox, p.oy = r.oy, p.oz = r.oz;
     const float tiny = 0x1p-80f;
-    float dx = fabsf(r.dx) < tiny ? copysignf(tiny, r.dx) : r.dx;
-    float dy = fabsf(r.dy) < tiny ? copysignf(tiny, r.dy) : r.dy;
-    float dz = fabsf(r.dz) < tiny ? copysignf(tiny, r.dz) : r.dz;
-    p.ix = __frcp_rn(dx), p.iy = __frcp_rn(dy), p.iz = __frcp_rn(dz);
-    float ax = fabsf(r.dx), ay = fabsf(r.dy), az = fabsf(r.dz);
-    int kz = (ax >= ay) ? (ax >= az ? 0 : 2) : (ay >= az ? 1 : 2);
+    const float dx = fabsf(r.dx) < tiny ? copysignf(tiny, r.dx) : r.dx;
+    const float dy = fabsf(r.dy) < tiny ? copysignf(tiny, r.dy) : r.dy;
+    const float dz = fabsf(r.dz) < tiny ? copysignf(tiny, r.dz) : r.dz;
+    p.Ix = __frcp_rn(dx), p.Iy = __frcp_rn(dy), p.Iz = __frcp_rn(dz);
+    const float cx = -r.ox * p.Ix, cy = -r.oy * p.Iy, cz = -r.oz * p.Iz;
+    const float ax = fabsf(cx) * 0x1p-22f, ay = fabsf(cy) * 0x1p-22f, az = fabsf(cz) * 0x1p-22f;
+    // lo plane is the near plane when I >= 0: push it towards smaller t; the hi plane the other way
+    p.clx = p.Ix >= 0.f ? cx - ax : cx + ax, p.chx = p.Ix >= 0.f ? cx + ax : cx - ax;
+    p.cly = p.Iy >= 0.f ? cy - ay : cy + ay, p.chy = p.Iy >= 0.f ? cy + ay : cy - ay;
+    p.clz = p.Iz >= 0.f ? cz - az : cz + az, p.chz = p.Iz >= 0.f ? cz + az : cz - az;
+    const float fx = fabsf(r.dx), fy = fabsf(r.dy), fz = fabsf(r.dz);
+    const int kz = (fx >= fy) ? (fx >= fz ? 0 : 2) : (fy >= fz ? 1 : 2);
     int kx = kz == 2 ? 0 : kz + 1;
     int ky = kx == 2 ? 0 : kx + 1;
-    float dkz = kz == 0 ? r.dx : (kz == 1 ? r.dy : r.dz);
+    const float dkz = kz == 0 ? r.dx : (kz == 1 ? r.dy : r.dz);
     if (dkz < 0.f) {
-        int t = kx;
+        const int t = kx;
         kx = ky;
         ky = t;
     }
-    float dkx = kx == 0 ? r.dx : (kx == 1 ? r.dy : r.dz);
-    float dky = ky == 0 ? r.dx : (ky == 1 ? r.dy : r.dz);
-    p.Sx = __fdiv_rn(dkx, dkz);
-    p.Sy = __fdiv_rn(dky, dkz);
-    p.Sz = __frcp_rn(dkz);
-    p.kx = kx, p.ky = ky, p.kz = kz;
+    const float dkx = kx == 0 ? r.dx : (kx == 1 ? r.dy : r.dz);
+    const float dky = ky == 0 ? r.dx : (ky == 1 ? r.dy : r.dz);
+    const float Sx = __fdiv_rn(dkx, dkz), Sy = __fdiv_rn(dky, dkz), Sz = __frcp_rn(dkz);
+    p.m0x = kx == 0 ? 1.f : (kz == 0 ? -Sx : 0.f);
+    p.m0y = kx == 1 ? 1.f : (kz == 1 ? -Sx : 0.f);
+    p.m0z = kx == 2 ? 1.f : (kz == 2 ? -Sx : 0.f);
+    p.m1x = ky == 0 ? 1.f : (kz == 0 ? -Sy : 0.f);
+    p.m1y = ky == 1 ? 1.f : (kz == 1 ? -Sy : 0.f);
+    p.m1z = ky == 2 ? 1.f : (kz == 2 ? -Sy : 0.f);
+    p.m2x = kz == 0 ? Sz : 0.f;
+    p.m2y = kz == 1 ? Sz : 0.f;
+    p.m2z = kz == 2 ? Sz : 0.f;
     return p;
 }
 
-__device__ __forceinline__ float pick(float x, float y, float z, int k) { return k == 0 ? x : (k == 1 ? y : z); }
+struct V3 {
+    float x, y, z;
+};
+
+// sheared coordinates of a vertex relative to the ray origin
+__device__ __forceinline__ V3 shear(const Pre &p, float4 v) {
+    const float X = v.x - p.ox, Y = v.y - p.oy, Z = v.z - p.oz;
+    V3 s;
+    s.x = fmaf(p.m0z, Z, fmaf(p.m0y, Y, p.m0x * X));
+    s.y = fmaf(p.m1z, Z, fmaf(p.m1y, Y, p.m1x * X));
+    s.z = fmaf(p.m2z, Z, fmaf(p.m2y, Y, p.m2x * X));
+    return s;
+}
 
 // Watertight ray/triangle test (two-sided, inclusive edges). Edge functions are evaluated without
 // FMA contraction so that the two triangles of a shared edge see exactly opposite values; an
 // exactly-zero edge function is re-evaluated in double (float products are exact there).
-// Returns true and t when the hit is in [tmin, best_t] and beats (best_t, best_id).
+// Returns true and t when t is in [tmin, best_t] and (t, id) beats (best_t, best_id).
 __device__ __forceinline__ bool hit_tri(const Pre &p, float4 a, float4 b, float4 c, float tmin, float best_t,
                                         int32_t best_id, int32_t id, float &t_out) {
-    const float Ax0 = a.x - p.ox, Ay0 = a.y - p.oy, Az0 = a.z - p.oz;
-    const float Bx0 = b.x - p.ox, By0 = b.y - p.oy, Bz0 = b.z - p.oz;
-    const float Cx0 = c.x - p.ox, Cy0 = c.y - p.oy, Cz0 = c.z - p.oz;
-    const float Akz = pick(Ax0, Ay0, Az0, p.kz), Bkz = pick(Bx0, By0, Bz0, p.kz), Ckz = pick(Cx0, Cy0, Cz0, p.kz);
-    const float Ax = pick(Ax0, Ay0, Az0, p.kx) - p.Sx * Akz;
-    const float Ay = pick(Ax0, Ay0, Az0, p.ky) - p.Sy * Akz;
-    const float Bx = pick(Bx0, By0, Bz0, p.kx) - p.Sx * Bkz;
-    const float By = pick(Bx0, By0, Bz0, p.ky) - p.Sy * Bkz;
-    const float Cx = pick(Cx0, Cy0, Cz0, p.kx) - p.Sx * Ckz;
-    const float Cy = pick(Cx0, Cy0, Cz0, p.ky) - p.Sy * Ckz;
-    float U = __fsub_rn(__fmul_rn(Cx, By), __fmul_rn(Cy, Bx));
-    float V = __fsub_rn(__fmul_rn(Ax, Cy), __fmul_rn(Ay, Cx));
-    float W = __fsub_rn(__fmul_rn(Bx, Ay), __fmul_rn(By, Ax));
+    const V3 A = shear(p, a), B = shear(p, b), C = shear(p, c);
+    float U = __fsub_rn(__fmul_rn(C.x, B.y), __fmul_rn(C.y, B.x));
+    float V = __fsub_rn(__fmul_rn(A.x, C.y), __fmul_rn(A.y, C.x));
+    float W = __fsub_rn(__fmul_rn(B.x, A.y), __fmul_rn(B.y, A.x));
+    if ((U < 0.f || V < 0.f || W < 0.f) && (U > 0.f || V > 0.f || W > 0.f)) return false;
     if (U == 0.f || V == 0.f || W == 0.f) {
-        double Ud = (double)Cx * (double)By - (double)Cy * (double)Bx;
-        double Vd = (double)Ax * (double)Cy - (double)Ay * (double)Cx;
-        double Wd = (double)Bx * (double)Ay - (double)By * (double)Ax;
+        const double Ud = (double)C.x * (double)B.y - (double)C.y * (double)B.x;
+        const double Vd = (double)A.x * (double)C.y - (double)A.y * (double)C.x;
+        const double Wd = (double)B.x * (double)A.y - (double)B.y * (double)A.x;
         if ((Ud < 0.0 || Vd < 0.0 || Wd < 0.0) && (Ud > 0.0 || Vd > 0.0 || Wd > 0.0)) return false;
         U = (float)Ud, V = (float)Vd, W = (float)Wd;
-    } else if ((U < 0.f || V < 0.f || W < 0.f) && (U > 0.f || V > 0.f || W > 0.f)) {
-        return false;
     }
     const float det = U + V + W;
     if (det == 0.f) return false;
-    const float Az = p.Sz * Akz, Bz = p.Sz * Bkz, Cz = p.Sz * Ckz;
-    const float T = U * Az + V * Bz + W * Cz;
+    const float T = U * A.z + V * B.z + W * C.z;
+    // cheap conservative reject before the division: t = T/det outside [tmin, best_t] by > 2^-20
+    const float ad = fabsf(det), Ts = det < 0.f ? -T : T;
+    if (Ts > best_t * ad * (1.f + 0x1p-20f) || Ts < tmin * ad * (1.f - 0x1p-20f)) return false;
     const float t = __fdiv_rn(T, det);
     if (!(t >= tmin && t <= best_t)) return false;
     if (t == best_t && id >= best_id) return false;
@@ -109,17 +136,22 @@ struct Hit {
     int32_t nodes, tris;
 };
 
-// robust slab test of one child box against [tmin, best_t]; returns entry distance or +inf
+// conservative slab test of one child box against [tmin, tmax]; returns the entry distance or +inf
 __device__ __forceinline__ float slab(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
                                       float tmin, float tmax) {
-    const float tx0 = __fmul_rn(__fsub_rn(lx, p.ox), p.ix), tx1 = __fmul_rn(__fsub_rn(hx, p.ox), p.ix);
-    const float ty0 = __fmul_rn(__fsub_rn(ly, p.oy), p.iy), ty1 = __fmul_rn(__fsub_rn(hy, p.oy), p.iy);
-    const float tz0 = __fmul_rn(__fsub_rn(lz, p.oz), p.iz), tz1 = __fmul_rn(__fsub_rn(hz, p.oz), p.iz);
-    const float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), tmin));
-    const float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
+    const float ax = fmaf(lx, p.Ix, p.clx), bx = fmaf(hx, p.Ix, p.chx);
+    const float ay = fmaf(ly, p.Iy, p.cly), by = fmaf(hy, p.Iy, p.chy);
+    const float az = fmaf(lz, p.Iz, p.clz), bz = fmaf(hz, p.Iz, p.chz);
+    const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
+    const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
     return tn <= tf * kExpand ? tn : INFINITY;
 }
 
+constexpr int32_t kDone = INT_MAX;  // "no more work" (never a node index: T - 1 < 2^28)
+
+// Traversal in the "while-while" form of Aila & Laine (HPG 2009): a lane that reaches a leaf
+// postpones it and keeps descending internal nodes until every active lane holds a leaf, then the
+// warp tests leaves together — leaf tests run with most lanes active instead of a few.
 template <bool kCount>
 __device__ __forceinline__ Hit trace(const SceneView &sv, const Ray &r, float tmin, float tmax) {
     const Pre p = precompute(r);
@@ -127,16 +159,24 @@ __device__ __forceinline__ Hit trace(const SceneView &sv, const Ray &r, float tm
     int32_t st_ref[kStack];
     float st_t[kStack];
     int sp = 0;
-    int32_t cur = 0;  // root: internal node 0
+    int32_t cur = 0;   // next internal node / leaf to visit (root = internal node 0), or kDone
+    int32_t leaf = 0;  // postponed leaf (< 0) or none (0)
+    auto pop = [&]() -> int32_t {
+        while (sp > 0) {
+            --sp;
+            if (st_t[sp] <= h.t * kExpand) return st_ref[sp];
+        }
+        return kDone;
+    };
     while (true) {
-        if (cur >= 0) {
+        while (cur >= 0 && cur != kDone) {
             const float4 *np = reinterpret_cast<const float4 *>(sv.nodes + cur);
             const float4 na = __ldg(np), nb = __ldg(np + 1), nc = __ldg(np + 2);
             const int4 nd = __ldg(reinterpret_cast<const int4 *>(np + 3));
             if (kCount) ++h.nodes;
             const float lim = h.t;
-            float t0 = slab(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim);
-            float t1 = nd.y == kEmptyRef ? INFINITY : slab(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim);
+            const float t0 = slab(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim);
+            const float t1 = nd.y == kEmptyRef ? INFINITY : slab(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim);
             const bool h0 = t0 != INFINITY, h1 = t1 != INFINITY;
             if (h0 && h1) {
                 const bool swap = t1 < t0;
@@ -144,13 +184,166 @@ __device__ __forceinline__ Hit trace(const SceneView &sv, const Ray &r, float tm
                 st_t[sp] = swap ? t0 : t1;
                 ++sp;
                 cur = swap ? nd.y : nd.x;
+            } else if (h0) {
+                cur = nd.x;
+            } else if (h1) {
+                cur = nd.y;
+            } else {
+                cur = pop();
+            }
+            if (cur < 0 && leaf == 0) {
+                leaf = cur;
+                cur = pop();
+            }
+            if (!__any_sync(__activemask(), leaf == 0)) break;
+        }
+        while (leaf < 0) {
+            const int32_t v = ~leaf;
+            const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
+            for (int32_t k = first; k < first + cnt; ++k) {
+                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+                const int32_t id = __float_as_int(a.w);
+                if (kCount) ++h.tris;
+                float t;
+                if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, t)) {
+                    h.t = t;
+                    h.id = id;
+                }
+            }
+            leaf = 0;
+            if (cur < 0) {
+                leaf = cur;
+                cur = pop();
+            }
+        }
+        if (cur == kDone) break;
+    }
+    return h;
+}
+
+// 4-wide traversal (node128): one fetch brings the four child boxes (SoA, 6 x LDG.128 + refs);
+// hit children are sorted by entry distance with a 5-comparator network, the nearest is visited
+// next and the others are pushed far-to-near. Same while-while leaf postponing as `trace`.
+__device__ __forceinline__ void cswap(float &ta, int32_t &ra, float &tb, int32_t &rb) {
+    const bool sw = tb < ta;
+    const float t = sw ? tb : ta;
+    const int32_t r = sw ? rb : ra;
+    tb = sw ? ta : tb;
+    rb = sw ? ra : rb;
+    ta = t;
+    ra = r;
+}
+
+template <bool kCount>
+__device__ __forceinline__ Hit trace4(const SceneView &sv, const Ray &r, float tmin, float tmax) {
+    const Pre p = precompute(r);
+    Hit h{tmax, INT_MAX, 0, 0};
+    int32_t st_ref[kStack];
+    float st_t[kStack];
+    int sp = 0;
+    int32_t cur = 0;
+    int32_t leaf = 0;
+    auto pop = [&]() -> int32_t {
+        while (sp > 0) {
+            --sp;
+            if (st_t[sp] <= h.t * kExpand) return st_ref[sp];
+        }
+        return kDone;
+    };
+    while (true) {
+        while (cur >= 0 && cur != kDone) {
+            const float4 *np = reinterpret_cast<const float4 *>(sv.nodes4 + cur);
+            const float4 lx = __ldg(np), hx = __ldg(np + 1), ly = __ldg(np + 2), hy = __ldg(np + 3);
+            const float4 lz = __ldg(np + 4), hz = __ldg(np + 5);
+            const int4 rf = __ldg(reinterpret_cast<const int4 *>(np + 6));
+            if (kCount) ++h.nodes;
+            const float lim = h.t;
+            float t0 = slab(p, lx.x, hx.x, ly.x, hy.x, lz.x, hz.x, tmin, lim);
+            float t1 = slab(p, lx.y, hx.y, ly.y, hy.y, lz.y, hz.y, tmin, lim);
+            float t2 = slab(p, lx.z, hx.z, ly.z, hy.z, lz.z, hz.z, tmin, lim);
+            float t3 = slab(p, lx.w, hx.w, ly.w, hy.w, lz.w, hz.w, tmin, lim);
+            int32_t r0 = rf.x, r1 = rf.y, r2 = rf.z, r3 = rf.w;
+            cswap(t0, r0, t1, r1);
+            cswap(t2, r2, t3, r3);
+            cswap(t0, r0, t2, r2);
+            cswap(t1, r1, t3, r3);
+            cswap(t1, r1, t2, r2);
+            if (t3 != INFINITY) st_ref[sp] = r3, st_t[sp] = t3, ++sp;
+            if (t2 != INFINITY) st_ref[sp] = r2, st_t[sp] = t2, ++sp;
+            if (t1 != INFINITY) st_ref[sp] = r1, st_t[sp] = t1, ++sp;
+            cur = t0 != INFINITY ? r0 : pop();
+            if (cur < 0 && leaf == 0) {
+                leaf = cur;
+                cur = pop();
+            }
+            if (!__any_sync(__activemask(), leaf == 0)) break;
+        }
+        while (leaf < 0) {
+            const int32_t v = ~leaf;
+            const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
+            for (int32_t k = first; k < first + cnt; ++k) {
+                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+                const int32_t id = __float_as_int(a.w);
+                if (kCount) ++h.tris;
+                float t;
+                if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, t)) {
+                    h.t = t;
+                    h.id = id;
+                }
+            }
+            leaf = 0;
+            if (cur < 0) {
+                leaf = cur;
+                cur = pop();
+            }
+        }
+        if (cur == kDone) break;
+    }
+    return h;
+}
+
+// Packet traversal for coherent pattern tiles (all 32 rays of a warp share the pose origin and
+// span ~1.5 degrees): the warp walks ONE node sequence — it descends into a child if any lane's ray
+// enters it within that lane's [t_min, t*] — so every node and triangle fetch is a broadcast and
+// control never diverges. Children are ordered by a lane vote on which is nearer; a popped subtree
+// is skipped when no lane can still improve inside it (per-lane entry distances are kept on the
+// stack). Each lane still keeps its own (t*, id) with the same leaf test, so results are identical
+// to the per-ray traversal.
+template <bool kCount>
+__device__ __forceinline__ Hit trace_packet(const SceneView &sv, const Ray &r, float tmin, float tmax,
+                                            int32_t *__restrict__ sref) {
+    const Pre p = precompute(r);
+    Hit h{tmax, INT_MAX, 0, 0};
+    float st_t[kStack];
+    int sp = 0;
+    int32_t cur = 0;
+    constexpr unsigned kFull = 0xffffffffu;
+    while (true) {
+        if (cur >= 0) {
+            const float4 *np = reinterpret_cast<const float4 *>(sv.nodes + cur);
+            const float4 na = __ldg(np), nb = __ldg(np + 1), nc = __ldg(np + 2);
+            const int4 nd = __ldg(reinterpret_cast<const int4 *>(np + 3));
+            if (kCount) ++h.nodes;
+            const float lim = h.t;
+            const float t0 = slab(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim);
+            const float t1 = nd.y == kEmptyRef ? INFINITY : slab(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim);
+            const unsigned m0 = __ballot_sync(kFull, t0 != INFINITY), m1 = __ballot_sync(kFull, t1 != INFINITY);
+            if (m0 && m1) {
+                const unsigned v1 = __ballot_sync(kFull, t1 < t0), v0 = __ballot_sync(kFull, t0 < t1);
+                const bool first1 = __popc(v1) > __popc(v0);
+                sref[sp] = first1 ? nd.x : nd.y;  // same value from every lane
+                st_t[sp] = first1 ? t0 : t1;
+                ++sp;
+                cur = first1 ? nd.y : nd.x;
                 continue;
             }
-            if (h0) {
+            if (m0) {
                 cur = nd.x;
                 continue;
             }
-            if (h1) {
+            if (m1) {
                 cur = nd.y;
                 continue;
             }
@@ -169,17 +362,15 @@ __device__ __forceinline__ Hit trace(const SceneView &sv, const Ray &r, float tm
                 }
             }
         }
-        // pop the nearest pending subtree whose entry distance does not exceed t*
-        bool found = false;
+        cur = kDone;
         while (sp > 0) {
             --sp;
-            if (st_t[sp] <= h.t * kExpand) {
-                cur = st_ref[sp];
-                found = true;
+            if (__any_sync(kFull, st_t[sp] <= h.t * kExpand)) {
+                cur = sref[sp];
                 break;
             }
         }
-        if (!found) break;
+        if (cur == kDone) break;
     }
     return h;
 }
@@ -239,6 +430,7 @@ __device__ __forceinline__ void rosette_ray(const RosetteParams &rp, const float
 }
 
 struct SpinGen {
+    static constexpr bool kCoherent = true;
     SpinParams sp;
     const float *poses;
     int tc, ta, nct, nat;  // tile shape and tiles per pose
@@ -257,6 +449,7 @@ struct SpinGen {
 };
 
 struct RosetteGen {
+    static constexpr bool kCoherent = true;
     RosetteParams rp;
     const float *poses;
     int ntile;  // tiles per pose
@@ -272,6 +465,7 @@ struct RosetteGen {
 };
 
 struct RaysGen {
+    static constexpr bool kCoherent = false;
     const float *orig, *dir;
     int64_t R;
     float t_min, t_max;
@@ -285,10 +479,17 @@ struct RaysGen {
     }
 };
 
-template <class Gen, bool kCount>
-__global__ void __launch_bounds__(kCastThreads) k_cast(const SceneView sv, const Gen gen, int64_t ntiles,
-                                                       const CastOut out, CastCounter *ctr) {
+#ifndef FGL_CAST_MINBLOCKS
+#define FGL_CAST_MINBLOCKS 8
+#endif
+enum TraversalMode { kRay2 = 0, kPacket2 = 1, kRay4 = 2 };
+
+template <class Gen, bool kCount, int kMode>
+__global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
+    k_cast(const SceneView sv, const Gen gen, int64_t ntiles, const CastOut out, CastCounter *ctr) {
     const int lane = threadIdx.x & 31;
+    __shared__ int32_t sref_all[kMode == kPacket2 ? kCastThreads / 32 : 1][kMode == kPacket2 ? kStack : 1];
+    int32_t *sref = sref_all[kMode == kPacket2 ? threadIdx.x >> 5 : 0];
     while (true) {
         unsigned long long tile = 0;
         if (lane == 0) tile = atomicAdd(&ctr->next, 1ull);
@@ -297,8 +498,16 @@ __global__ void __launch_bounds__(kCastThreads) k_cast(const SceneView sv, const
         Ray r;
         int64_t idx;
         float tmin, tmax;
-        if (gen.ray((int64_t)tile, lane, r, idx, tmin, tmax)) {
-            Hit h = trace<kCount>(sv, r, tmin, tmax);
+        const bool valid = gen.ray((int64_t)tile, lane, r, idx, tmin, tmax);
+        if (kMode == kPacket2) {
+            if (!valid) {  // a ragged-tile lane rides along with an empty interval
+                r = Ray{0.f, 0.f, 0.f, 1.f, 0.f, 0.f};
+                tmin = 0.f, tmax = -1.f;
+            }
+            Hit h = trace_packet<kCount>(sv, r, tmin, tmax, sref);
+            if (valid) write_out(out, idx, r, h);
+        } else if (valid) {
+            Hit h = kMode == kRay4 ? trace4<kCount>(sv, r, tmin, tmax) : trace<kCount>(sv, r, tmin, tmax);
             write_out(out, idx, r, h);
         }
     }
@@ -313,32 +522,53 @@ __global__ void __launch_bounds__(kCastThreads) k_cast(const SceneView sv, const
     }
 }
 
-template <class Gen>
-void launch_persistent(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
-                       cudaStream_t s) {
-    if (ntiles <= 0) return;
-    const bool count = o.node_counts || o.tri_counts;
-    static int occ[2] = {0, 0};
-    static int sms = 0;
-    int &oc = occ[count];
+// FGL_TRAVERSAL=packet selects the warp-packet traversal for pattern casts (A/B experiments;
+// the default per-ray while-while traversal is faster on the measured workloads).
+inline bool packet_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("FGL_TRAVERSAL");
+        v = (e && strcmp(e, "packet") == 0) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+template <class Gen, bool kCount, int kMode>
+void launch_one(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
+                cudaStream_t s) {
+    static int oc = 0, sms = 0;
     if (!oc) {
         int dev;
         FGL_CUDA(cudaGetDevice(&dev));
         FGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (count)
-            FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast<Gen, true>, kCastThreads, 0));
-        else
-            FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast<Gen, false>, kCastThreads, 0));
+        FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast<Gen, kCount, kMode>, kCastThreads, 0));
         if (oc < 1) oc = 1;
     }
-    const int64_t warps_needed = ntiles;
-    int64_t blocks = std::min<int64_t>((int64_t)sms * oc, (warps_needed + kCastThreads / 32 - 1) / (kCastThreads / 32));
+    int64_t blocks = std::min<int64_t>((int64_t)sms * oc, (ntiles + kCastThreads / 32 - 1) / (kCastThreads / 32));
     blocks = std::max<int64_t>(blocks, 1);
-    if (count)
-        k_cast<Gen, true><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
-    else
-        k_cast<Gen, false><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
+    k_cast<Gen, kCount, kMode><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
     FGL_LAUNCHED("k_cast");
+}
+
+template <class Gen, bool kCount>
+void launch_mode(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
+                 cudaStream_t s) {
+    if (sv.width == 4)
+        launch_one<Gen, kCount, kRay4>(sv, gen, ntiles, o, ctr, s);
+    else if (Gen::kCoherent && packet_mode())
+        launch_one<Gen, kCount, kPacket2>(sv, gen, ntiles, o, ctr, s);
+    else
+        launch_one<Gen, kCount, kRay2>(sv, gen, ntiles, o, ctr, s);
+}
+
+template <class Gen>
+void launch_persistent(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
+                       cudaStream_t s) {
+    if (ntiles <= 0) return;
+    if (o.node_counts || o.tri_counts)
+        launch_mode<Gen, true>(sv, gen, ntiles, o, ctr, s);
+    else
+        launch_mode<Gen, false>(sv, gen, ntiles, o, ctr, s);
 }
 
 // ---- brute force: every ray against every triangle, triangles staged in smem -------

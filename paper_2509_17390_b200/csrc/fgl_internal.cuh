@@ -41,6 +41,15 @@ struct __align__(16) Node64 {
     float4 a, b, c;
     int4 d;
 };
+// 4-wide traversal node ("node128"), children in SoA: f[0]=lo.x[4] f[1]=hi.x[4] f[2]=lo.y[4]
+// f[3]=hi.y[4] f[4]=lo.z[4] f[5]=hi.z[4], refs[4], meta = (valid children, depth, 0, 0).
+// Stored at the index of the binary node it collapses (even-depth internal nodes).
+struct __align__(16) Node128 {
+    float4 f[6];
+    int4 ref;
+    int4 meta;
+};
+constexpr float kFarBox = 3.0e38f;  // empty child: a degenerate box no ray with t <= t_max reaches
 constexpr int32_t kEmptyRef = INT32_MIN;
 constexpr int kLeafShift = 3;
 constexpr int kMaxLeaf = 8;
@@ -77,6 +86,9 @@ struct BuildBuffers {
     float4 *leafbox = nullptr;     // [2T]
     float4 *nodebox = nullptr;     // [2(T-1)]
     Node64 *nodes = nullptr;       // [max(T-1,1)]
+    Node128 *nodes4 = nullptr;     // [max(T-1,1)]
+    int32_t *depth = nullptr;      // [T-1]
+    int width = 4;
     int sorted_slot = 0;           // which keys/vals buffer holds the sorted result
 };
 
@@ -90,8 +102,8 @@ void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_
 void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s);
 
 // build.cu
-void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  cudaStream_t s);
+void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size, int cubic,
+                  int width, cudaStream_t s);
 void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
                      cudaStream_t s);
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
@@ -118,6 +130,8 @@ struct CastOut {
 struct SceneView {
     const float4 *tri;
     const Node64 *nodes;
+    const Node128 *nodes4;
+    int width;
 };
 void launch_cast_spinning(const SceneView &sv, const SpinParams &p, const float *poses, int64_t P, const CastOut &o,
                           CastCounter *ctr, cudaStream_t s);

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfgl.so")
+LIB_PATH = os.environ.get("FGL_LIB") or os.path.join(HERE, "libfgl.so")  # FGL_LIB: A/B builds
 
 OK, E_USAGE, E_DATA, E_RESOURCE, E_CUDA = range(5)
 HOST, DEVICE = 0, 1
@@ -30,7 +30,8 @@ class FglError(RuntimeError):
 
 
 class BuildOpts(Structure):
-    _fields_ = [("morton_bits", c_int32), ("leaf_size", c_int32), ("reserved", c_int32 * 6)]
+    _fields_ = [("morton_bits", c_int32), ("leaf_size", c_int32), ("morton_box", c_int32), ("width", c_int32),
+                ("reserved", c_int32 * 4)]
 
 
 class Stats(Structure):
@@ -51,7 +52,7 @@ class RosetteC(Structure):
 
 class ExportC(Structure):
     _fields_ = [(n, c_void_p) for n in ("scene_box", "codes", "sorted_keys", "perm", "child", "range", "leaf_box",
-                                        "node_box", "tri48", "nodes")]
+                                        "node_box", "tri48", "nodes", "nodes4", "depth")]
 
 
 # name: (restype, argtypes)
@@ -151,14 +152,15 @@ class Scene:
     builds; `cast(poses, pattern)` returns (range, tri_id) device tensors."""
 
     def __init__(self, verts=None, tris=None, device=None, build: bool = True, morton_bits: int = 21,
-                 leaf_size: int = 4, stream=None):
+                 leaf_size: int = 0, morton_box: int = 0, width: int = 0, stream=None):
+        """leaf_size / width 0 = library defaults; morton_box 0 = cubic (R22), 1 = per-axis (Eq. 5)."""
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
         h = c_void_p()
         _check(lib().fgl_scene_create(self.device.index or 0, ctypes.byref(h)))
         self._h = h
-        self.morton_bits, self.leaf_size = morton_bits, leaf_size
+        self.morton_bits, self.leaf_size, self.morton_box, self.width = morton_bits, leaf_size, morton_box, width
         self.T = 0
         if verts is not None:
             self.upload(verts, tris, stream)
@@ -195,8 +197,11 @@ class Scene:
         self.T, self.V = T, V
         return self
 
-    def build(self, morton_bits: int | None = None, leaf_size: int | None = None, stream=None):
-        o = BuildOpts(morton_bits or self.morton_bits, leaf_size or self.leaf_size, (c_int32 * 6)())
+    def build(self, morton_bits: int | None = None, leaf_size: int | None = None, morton_box: int | None = None,
+              width: int | None = None, stream=None):
+        mb = self.morton_box if morton_box is None else morton_box
+        o = BuildOpts(morton_bits or self.morton_bits, leaf_size or self.leaf_size, int(mb),
+                      int(width or self.width), (c_int32 * 4)())
         _check(lib().fgl_scene_build(self._h, ctypes.byref(o), _stream(stream)))
         return self
 
@@ -264,7 +269,8 @@ class Scene:
         a = dict(scene_box=np.zeros(6, np.float32), codes=np.zeros(T, np.uint64), sorted_keys=np.zeros(T, np.uint64),
                  perm=np.zeros(T, np.uint32), child=np.zeros((nin, 2), np.int32), range=np.zeros((nin, 2), np.int32),
                  leaf_box=np.zeros((T, 6), np.float32), node_box=np.zeros((nin, 6), np.float32),
-                 tri48=np.zeros((T, 12), np.float32), nodes=np.zeros((max(nin, 1), 16), np.float32))
+                 tri48=np.zeros((T, 12), np.float32), nodes=np.zeros((max(nin, 1), 16), np.float32),
+                 nodes4=np.zeros((max(nin, 1), 32), np.float32), depth=np.zeros(nin, np.int32))
         e = ExportC(*[a[n].ctypes.data for n, _ in ExportC._fields_])
         _check(lib().fgl_scene_export(self._h, ctypes.byref(e), _stream(stream)))
         return a

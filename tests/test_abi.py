@@ -39,7 +39,7 @@ def test_binding_covers_the_header(libpath):
     import paper_2509_17390_b200 as fgl
     assert sorted(fgl.SYMBOLS) == _header_symbols()
     L = fgl.lib()
-    assert L.fgl_abi_version() == 1
+    assert L.fgl_abi_version() == 2
     assert b"sm_100a" in L.fgl_version()
 
 

@@ -59,13 +59,62 @@ def _decode_nodes(nodes, T, leaf_size):
     return out, cover
 
 
+def _depth_oracle(child, n):
+    d = np.zeros(max(n - 1, 0), np.int64)
+    stack = [(0, 0)] if n >= 2 else []
+    while stack:
+        i, k = stack.pop()
+        d[i] = k
+        for c in child[i]:
+            if c >= 0:
+                stack.append((c, k + 1))
+    return d
+
+
+def _check_nodes4(g, o, m, T, leaf_size):
+    """4-wide nodes (DESIGN.md §5 node128): walk from the root; every child box is the exact union
+    of its triangles; leaves cover each sorted position once; internal children are the even-depth
+    binary nodes two levels down; depths match the oracle tree."""
+    if T >= 2:
+        assert np.array_equal(g["depth"], _depth_oracle(o["child"], T))
+    f = g["nodes4"].view(np.float32).reshape(-1, 32)
+    ii = g["nodes4"].view(np.int32).reshape(-1, 32)
+    V = m.verts[m.tris[o["perm"]]]
+    cover = np.zeros(T, np.int32)
+    stack = [0]
+    while stack:
+        i = stack.pop()
+        refs = ii[i, 24:28]
+        assert ii[i, 28] == np.sum(refs != -2 ** 31)
+        for k in range(4):
+            ref = int(refs[k])
+            box = np.array([f[i, 0 + k], f[i, 8 + k], f[i, 16 + k], f[i, 4 + k], f[i, 12 + k], f[i, 20 + k]])
+            if ref == -2 ** 31:
+                assert np.all(box == np.float32(3.0e38))
+                continue
+            if ref >= 0:
+                fr, l = o["range"][ref]
+                c = l - fr + 1
+                assert c > leaf_size and g["depth"][ref] % 2 == 0
+                stack.append(ref)
+            else:
+                v = ~ref
+                fr, c = v >> 3, (v & 7) + 1
+                assert c <= leaf_size or (T == 1)
+                cover[fr:fr + c] += 1
+            sub = V[fr:fr + c].reshape(-1, 3)
+            assert np.array_equal(box, np.concatenate([sub.min(0), sub.max(0)]))
+    assert np.all(cover == 1)
+
+
 @pytest.mark.parametrize("name", ["tiny1", "tiny2", "dups", "c1", "soup"])
-@pytest.mark.parametrize("leaf_size", [1, 4, 8])
-def test_build_matches_oracle(fgl, name, leaf_size):
+@pytest.mark.parametrize("leaf_size,cubic,width", [(1, 0, 2), (4, 0, 2), (8, 0, 2), (4, 1, 2), (2, 1, 4), (1, 1, 4),
+                                                   (5, 0, 4)])
+def test_build_matches_oracle(fgl, name, leaf_size, cubic, width):
     m = _meshes()[name]
-    s = fgl.Scene(m.verts, m.tris, leaf_size=leaf_size)
+    s = fgl.Scene(m.verts, m.tris, leaf_size=leaf_size, morton_box=0 if cubic else 1, width=width)
     g = s.export()
-    o = oracle.lbvh(m.verts, m.tris)
+    o = oracle.lbvh(m.verts, m.tris, cubic=bool(cubic))
     T = m.T
     assert np.array_equal(g["scene_box"][:3], o["lo"]) and np.array_equal(g["scene_box"][3:], o["hi"])
     assert np.array_equal(g["codes"], o["code"])                       # Eq. 5
@@ -81,6 +130,9 @@ def test_build_matches_oracle(fgl, name, leaf_size):
     assert np.array_equal(tri[:, 0, 3].view(np.int32), o["perm"].astype(np.int32))
     # traversal nodes: every reachable child box is the exact union of its triangles, leaves cover
     # every sorted position exactly once
+    if width == 4:
+        _check_nodes4(g, o, m, T, leaf_size)
+        return
     visited, cover = _decode_nodes(g["nodes"], T, leaf_size)
     assert np.all(cover == 1)
     V = m.verts[m.tris[o["perm"]]]
@@ -107,7 +159,7 @@ def test_build_rooms_full_size(fgl):
     m = synth.scene_rooms(2)
     s = fgl.Scene(m.verts, m.tris)
     g = s.export()
-    o = oracle.lbvh(m.verts, m.tris)
+    o = oracle.lbvh(m.verts, m.tris, cubic=True)  # library default: cubic Morton box (R22)
     for k_g, k_o in (("codes", "code"), ("sorted_keys", "sorted_keys"), ("perm", "perm"), ("child", "child"),
                      ("range", "range"), ("leaf_box", "leaf_box"), ("node_box", "node_box")):
         assert np.array_equal(g[k_g], o[k_o]), k_g

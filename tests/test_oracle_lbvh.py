@@ -150,3 +150,19 @@ def test_single_triangle_tree(orc):
     V = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 2]], np.float32)
     b = orc.lbvh(V, np.array([[0, 1, 2]], np.int32))
     assert b["child"].shape == (0, 2) and np.array_equal(b["leaf_box"][0], [0, 0, 0, 1, 1, 2])
+
+
+def test_morton_cubic_box_uses_longest_extent(orc):
+    # R22: with a cubic box every axis is scaled by the longest extent: for lo = 0 and a longest
+    # extent of 2^b the cells are unit cubes on all axes, q = floor(c), whatever the other extents
+    bits = 10
+    lo = np.zeros(3, np.float32)
+    hi = np.array([2.0 ** bits, 5.0, 3.0], np.float32)
+    rng = np.random.default_rng(7)
+    c = np.stack([rng.uniform(0, 2 ** bits, 300), rng.uniform(0, 5, 300), rng.uniform(0, 3, 300)], 1).astype(np.float32)
+    code = orc.morton(c, lo, hi, bits, cubic=True)
+    for i in range(300):
+        assert _decode(code[i], bits) == [min(int(np.floor(x)), 2 ** bits - 1) for x in c[i]]
+    # per-axis (Eq. 5) scales y by 2^b / 5 instead
+    code2 = orc.morton(c, lo, hi, bits)
+    assert _decode(code2[0], bits)[1] == int(np.floor(np.float32(c[0, 1]) * np.float32(2.0 ** bits / 5.0)))
