@@ -42,6 +42,7 @@ def _args():
                     help="full = upload+build+cast per step (default); cast = cast only on a prebuilt scene")
     ap.add_argument("--leaf-size", type=int, default=0, help="0 = library default")
     ap.add_argument("--width", type=int, default=0, help="BVH node width 2 or 4 (0 = library default)")
+    ap.add_argument("--morton-bits", type=int, default=0, help="b of Eq. 5 (0 = library default)")
     ap.add_argument("--morton-box", type=int, default=0, help="0 = cubic (R22, default), 1 = per-axis (Eq. 5)")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -238,7 +239,8 @@ def main():
     tris_d = torch.from_numpy(m.tris).to(dev)
     poses_d = torch.from_numpy(np.ascontiguousarray(cfg["poses_rank"])).to(dev)
     stream = torch.cuda.current_stream()
-    scene = fgl.Scene(verts_d, tris_d, device=dev, leaf_size=a.leaf_size, morton_box=a.morton_box, width=a.width)
+    scene = fgl.Scene(verts_d, tris_d, device=dev, leaf_size=a.leaf_size, morton_box=a.morton_box, width=a.width,
+                      morton_bits=a.morton_bits)
     out = scene.cast(poses_d, pat)
     shape = tuple(out["range"].shape)
     gather = None
@@ -310,7 +312,8 @@ def main():
         rh = torch.empty(shape, dtype=torch.float32).pin_memory()
         ih = torch.empty(shape, dtype=torch.int32).pin_memory()
         pd = torch.empty_like(poses_d)
-        sc2 = fgl.Scene(device=dev, leaf_size=a.leaf_size, morton_box=a.morton_box, width=a.width)
+        sc2 = fgl.Scene(device=dev, leaf_size=a.leaf_size, morton_box=a.morton_box, width=a.width,
+                        morton_bits=a.morton_bits)
 
         def e2e_step():
             sc2.upload(vh, th)                               # H2D mesh (pinned) + validation

@@ -53,7 +53,7 @@ enum { FGL_HOST = 0, FGL_DEVICE = 1 };
 typedef struct fgl_scene fgl_scene; /* opaque: device copies of the mesh, the BVH and scratch */
 
 typedef struct {
-    int32_t morton_bits; /* b of Eq. 5, 1..21; 0 = default 21 (63-bit keys)      */
+    int32_t morton_bits; /* b of Eq. 5, 1..21; 0 = default 16 (48-bit keys, R7)     */
     int32_t leaf_size;   /* max triangles per BVH leaf, 1..8; 0 = default (2)                 */
     int32_t morton_box;  /* 0 = cubic scene box (default): every axis uses L = max_a L_a, the box
                             [o, o+L] read as a cube (isotropic cells; reading R22);
@@ -167,7 +167,7 @@ FGL_API fgl_status fgl_scene_export(const fgl_scene *scene, const fgl_export *ou
 FGL_API fgl_status fgl_morton_codes(const float *points, int64_t n, const float *lo, const float *hi, int32_t bits,
                             uint64_t *codes, void *cuda_stream);
 /* Stable LSD radix sort of (key, value) pairs in place, on the low key_bits bits of the keys
- * (1..64). Allocates its scratch with cudaMallocAsync on the stream. */
+ * (1..64), n < 2^30. Allocates its scratch with cudaMallocAsync on the stream. */
 FGL_API fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key_bits, void *cuda_stream);
 
 /* ---- misc ----------------------------------------------------------------------------- */

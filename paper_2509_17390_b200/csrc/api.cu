@@ -76,7 +76,7 @@ void dalloc(fgl_scene *s, T **p, size_t n) {
 
 void free_build(fgl_scene *s) {
     fgl::BuildBuffers &b = s->b;
-    void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.counts,
+    void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.sort_status, b.sort_tiles,
                   b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth};
     for (void *p : ps)
         if (p) cudaFree(p);
@@ -99,7 +99,9 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.vals[0], T);
     dalloc(s, &b.vals[1], T);
     dalloc(s, &b.ghist, 8 * 256);
-    dalloc(s, &b.counts, (size_t)256 * fgl::sort_tile_blocks(T));
+    dalloc(s, &b.sort_status, (size_t)256 * fgl::sort_tile_blocks(T));
+    FGL_CUDA(cudaMemset(b.sort_status, 0, sizeof(uint64_t) * 256 * fgl::sort_tile_blocks(T)));
+    dalloc(s, &b.sort_tiles, 8);
     dalloc(s, &b.tri, 3 * T);
     dalloc(s, &b.child, nin);
     dalloc(s, &b.range, nin);
@@ -266,7 +268,7 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     FGL_API_BEGIN
     if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
     if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
-    int bits = 21, leaf = 2, cubic = 1, width = 2;
+    int bits = 16, leaf = 2, cubic = 1, width = 2;
     if (opts) {
         if (opts->width) width = opts->width;
         if (width != 2 && width != 4) throw Error(FGL_E_USAGE, "width must be 2 or 4");
@@ -455,25 +457,31 @@ fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key
     FGL_API_BEGIN
     if (n < 0) throw Error(FGL_E_USAGE, "n must be >= 0");
     if (key_bits < 1 || key_bits > 64) throw Error(FGL_E_USAGE, "key_bits must be in [1, 64]");
-    if (n > (int64_t)UINT32_MAX) throw Error(FGL_E_USAGE, "n too large");
+    if (n >= (int64_t(1) << 30)) throw Error(FGL_E_USAGE, "n must be < 2^30");
     if (n <= 1) return FGL_OK;
     if (!keys || !vals) throw Error(FGL_E_USAGE, "NULL pointer argument");
     cudaStream_t st = (cudaStream_t)stream;
     uint64_t *k1 = nullptr;
-    uint32_t *v1 = nullptr, *counts = nullptr, *ghist = nullptr;
+    uint32_t *v1 = nullptr, *tiles = nullptr, *ghist = nullptr;
+    uint64_t *status = nullptr;
     FGL_CUDA(cudaMallocAsync((void **)&k1, n * sizeof(uint64_t), st));
     FGL_CUDA(cudaMallocAsync((void **)&v1, n * sizeof(uint32_t), st));
-    FGL_CUDA(cudaMallocAsync((void **)&counts, (size_t)256 * fgl::sort_tile_blocks(n) * sizeof(uint32_t), st));
+    const size_t nstat = (size_t)256 * fgl::sort_tile_blocks(n);
+    FGL_CUDA(cudaMallocAsync((void **)&status, nstat * sizeof(uint64_t), st));
+    FGL_CUDA(cudaMemsetAsync(status, 0, nstat * sizeof(uint64_t), st));
+    FGL_CUDA(cudaMallocAsync((void **)&tiles, 8 * sizeof(uint32_t), st));
     FGL_CUDA(cudaMallocAsync((void **)&ghist, 8 * 256 * sizeof(uint32_t), st));
     int slot = 0;
-    fgl::radix_sort_pairs(keys, vals, k1, v1, n, key_bits, counts, ghist, false, &slot, st);
+    uint32_t epoch = 0;
+    fgl::radix_sort_pairs(keys, vals, k1, v1, n, key_bits, status, tiles, ghist, false, &epoch, &slot, st);
     if (slot == 1) {
         FGL_CUDA(cudaMemcpyAsync(keys, k1, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
         FGL_CUDA(cudaMemcpyAsync(vals, v1, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
     }
     cudaFreeAsync(k1, st);
     cudaFreeAsync(v1, st);
-    cudaFreeAsync(counts, st);
+    cudaFreeAsync(status, st);
+    cudaFreeAsync(tiles, st);
     cudaFreeAsync(ghist, st);
     FGL_API_END
 }

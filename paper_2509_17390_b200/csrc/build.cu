@@ -9,6 +9,8 @@
 //   refit    : Eq. 7 bottom-up union with atomic arrival counters
 //   nodes    : traversal nodes (both child boxes per node; subtrees of <= leaf_size triangles
 //              become leaves), laid out in Karras (Morton) order ("Morton order").
+#include <cuda/atomic>
+
 #include "fgl_internal.cuh"
 
 namespace fgl {
@@ -176,27 +178,12 @@ __global__ void k_morton_points(const float *__restrict__ pts, int64_t n, BoxArg
         codes[k] = morton_code(m, pts[3 * k], pts[3 * k + 1], pts[3 * k + 2]);
 }
 
-// tri48 record j = triangle perm[j]: {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}; leaf box j
-__global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, const int32_t *__restrict__ tris,
-                                                 const uint32_t *__restrict__ perm, int64_t T,
-                                                 float4 *__restrict__ tri, float4 *__restrict__ leafbox) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < T; j += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t k = perm[j];
-        float3 a = ldv(verts, __ldg(tris + 3 * (int64_t)k)), b = ldv(verts, __ldg(tris + 3 * (int64_t)k + 1)),
-               c = ldv(verts, __ldg(tris + 3 * (int64_t)k + 2));
-        tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
-        tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
-        tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
-        leafbox[2 * j] = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
-        leafbox[2 * j + 1] = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
-    }
-}
-
-// LCP of augmented keys code_i || i (sorted position fallback for equal codes; R7); -1 outside
-__device__ __forceinline__ int delta(const uint64_t *__restrict__ k, int64_t n, int64_t i, int64_t j) {
+// LCP of augmented keys code_i || i (sorted position fallback for equal codes; R7); -1 outside.
+// ki = k[i] is passed in (loaded once per thread).
+__device__ __forceinline__ int delta(const uint64_t *__restrict__ k, int64_t n, int64_t i, uint64_t ki, int64_t j) {
     if (j < 0 || j >= n) return -1;
-    uint64_t a = __ldg(k + i), b = __ldg(k + j);
-    if (a != b) return __clzll((long long)(a ^ b));
+    const uint64_t b = __ldg(k + j);
+    if (ki != b) return __clzll((long long)(ki ^ b));
     return 64 + __clz((int)((uint32_t)i ^ (uint32_t)j));
 }
 
@@ -204,19 +191,20 @@ __device__ __forceinline__ int delta(const uint64_t *__restrict__ k, int64_t n, 
 __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, int64_t n, int2 *__restrict__ child,
                                                 int2 *__restrict__ range, int32_t *__restrict__ parent) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
-        const int d = (delta(k, n, i, i + 1) - delta(k, n, i, i - 1)) >= 0 ? 1 : -1;
-        const int dmin = delta(k, n, i, i - d);
+        const uint64_t ki = __ldg(k + i);
+        const int d = (delta(k, n, i, ki, i + 1) - delta(k, n, i, ki, i - 1)) >= 0 ? 1 : -1;
+        const int dmin = delta(k, n, i, ki, i - d);
         int64_t lmax = 2;
-        while (delta(k, n, i, i + lmax * d) > dmin) lmax <<= 1;
+        while (delta(k, n, i, ki, i + lmax * d) > dmin) lmax <<= 1;
         int64_t l = 0;
         for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
-            if (delta(k, n, i, i + (l + t) * d) > dmin) l += t;
+            if (delta(k, n, i, ki, i + (l + t) * d) > dmin) l += t;
         const int64_t j = i + l * d;
-        const int dnode = delta(k, n, i, j);
+        const int dnode = delta(k, n, i, ki, j);
         int64_t s = 0, t = l;
         do {
             t = (t + 1) >> 1;
-            if (delta(k, n, i, i + (s + t) * d) > dnode) s += t;
+            if (delta(k, n, i, ki, i + (s + t) * d) > dnode) s += t;
         } while (t > 1);
         const int64_t g = i + s * d + (d < 0 ? -1 : 0);
         const int64_t f = i < j ? i : j, last = i < j ? j : i;
@@ -230,59 +218,68 @@ __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, 
     }
 }
 
-__device__ __forceinline__ void ldbox(const float4 *p, float4 &lo, float4 &hi) {
-    lo = __ldcg(p);
-    hi = __ldcg(p + 1);
-}
-
-// Eq. 7 bottom-up: each leaf climbs; the second thread to reach a node writes the union
-__global__ void __launch_bounds__(256) k_refit(int64_t n, const int2 *__restrict__ child,
-                                               const int32_t *__restrict__ parent, int32_t *__restrict__ flags,
-                                               const float4 *__restrict__ leafbox, float4 *__restrict__ nodebox) {
+// Fused leaf-order gather + Eq. 7 bottom-up refit + binary traversal nodes. Thread j:
+//   tri48[j] = triangle perm[j] {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}; leaf box j (exact min/max);
+//   then climbs: at each parent the FIRST arriving child stops (acq_rel arrival counter), the
+//   second computes B(n) = B(left) U B(right) (Eq. 7) from its own box (registers) and the
+//   sibling's (L2), stores it, and — width 2 — writes the node64 of that parent (children that
+//   cover <= leaf_size triangles become leaves).
+__global__ void __launch_bounds__(256) k_reorder_refit(const float *__restrict__ verts,
+                                                       const int32_t *__restrict__ tris,
+                                                       const uint32_t *__restrict__ perm, int64_t n, int leaf_size,
+                                                       const int2 *__restrict__ child, const int2 *__restrict__ range,
+                                                       const int32_t *__restrict__ parent, int32_t *__restrict__ flags,
+                                                       float4 *__restrict__ tri, float4 *__restrict__ leafbox,
+                                                       float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = perm[j];
+        const float3 a = ldv(verts, __ldg(tris + 3 * (int64_t)k)), b = ldv(verts, __ldg(tris + 3 * (int64_t)k + 1)),
+                     c = ldv(verts, __ldg(tris + 3 * (int64_t)k + 2));
+        tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
+        tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
+        tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
+        float4 lo = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
+        float4 hi = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
+        __stcg(leafbox + 2 * j, lo);
+        __stcg(leafbox + 2 * j + 1, hi);
+        if (n == 1) continue;
+        int32_t cur = ~(int32_t)j;  // child reference of the subtree whose box is in (lo, hi)
+        int32_t cf = (int32_t)j, cl = (int32_t)j;
         int32_t p = parent[(n - 1) + j];
         while (p >= 0) {
-            __threadfence();
-            if (atomicAdd(&flags[p], 1) == 0) break;
-            int2 c = __ldcg(&child[p]);
-            float4 l0, h0, l1, h1;
-            ldbox(c.x >= 0 ? nodebox + 2 * (int64_t)c.x : leafbox + 2 * (int64_t)(~c.x), l0, h0);
-            ldbox(c.y >= 0 ? nodebox + 2 * (int64_t)c.y : leafbox + 2 * (int64_t)(~c.y), l1, h1);
-            __stcg(nodebox + 2 * (int64_t)p, make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.f));
-            __stcg(nodebox + 2 * (int64_t)p + 1, make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.f));
-            p = parent[p];
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const int2 *__restrict__ child,
-                                               const int2 *__restrict__ range, const float4 *__restrict__ leafbox,
-                                               const float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
-        int2 c = child[i];
-        int32_t ref[2];
-        float4 lo[2], hi[2];
-        int32_t cc[2] = {c.x, c.y};
-        for (int s = 0; s < 2; ++s) {
-            if (cc[s] < 0) {
-                int32_t j = ~cc[s];
-                ref[s] = make_leaf(j, 1);
-                lo[s] = leafbox[2 * (int64_t)j];
-                hi[s] = leafbox[2 * (int64_t)j + 1];
-            } else {
-                int2 r = range[cc[s]];
-                int32_t cnt = r.y - r.x + 1;
-                ref[s] = cnt <= leaf_size ? make_leaf(r.x, cnt) : cc[s];
-                lo[s] = nodebox[2 * (int64_t)cc[s]];
-                hi[s] = nodebox[2 * (int64_t)cc[s] + 1];
+            // read-only topology first (overlaps the arrival atomic)
+            const int2 cp = __ldg(child + p);
+            const int2 rp = __ldg(range + p);
+            const int32_t pp = __ldg(parent + p);
+            // release-only arrival: our box stores (leafbox / nodebox) are ordered before it; the
+            // second arriver reads the sibling's box from L2 (ld.cg), never a stale L1 line
+            int32_t old;
+            asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(flags + p) : "memory");
+            if (old == 0) break;
+            const bool left = cp.x == cur;
+            const int32_t sib = left ? cp.y : cp.x;
+            const float4 *sb = sib >= 0 ? nodebox + 2 * (int64_t)sib : leafbox + 2 * (int64_t)(~sib);
+            const float4 slo = __ldcg(sb), shi = __ldcg(sb + 1);
+            const float4 nlo = make_float4(fminf(lo.x, slo.x), fminf(lo.y, slo.y), fminf(lo.z, slo.z), 0.f);
+            const float4 nhi = make_float4(fmaxf(hi.x, shi.x), fmaxf(hi.y, shi.y), fmaxf(hi.z, shi.z), 0.f);
+            __stcg(nodebox + 2 * (int64_t)p, nlo);
+            __stcg(nodebox + 2 * (int64_t)p + 1, nhi);
+            if (nodes) {
+                // child refs: leaves, subtrees of <= leaf_size triangles collapse to leaves
+                const int32_t sf = left ? cl + 1 : rp.x, sl = left ? rp.y : cf - 1;
+                const int32_t mref = (cur < 0 || cl - cf + 1 <= leaf_size) ? make_leaf(cf, cl - cf + 1) : cur;
+                const int32_t sref = (sib < 0 || sl - sf + 1 <= leaf_size) ? make_leaf(sf, sl - sf + 1) : sib;
+                const float4 l0 = left ? lo : slo, h0 = left ? hi : shi, l1 = left ? slo : lo, h1 = left ? shi : hi;
+                Node64 nd;
+                nd.a = make_float4(l0.x, h0.x, l0.y, h0.y);
+                nd.b = make_float4(l1.x, h1.x, l1.y, h1.y);
+                nd.c = make_float4(l0.z, h0.z, l1.z, h1.z);
+                nd.d = make_int4(left ? mref : sref, left ? sref : mref, 0, 0);
+                nodes[p] = nd;
             }
+            lo = nlo, hi = nhi, cur = p, cf = rp.x, cl = rp.y;
+            p = pp;
         }
-        Node64 nd;
-        nd.a = make_float4(lo[0].x, hi[0].x, lo[0].y, hi[0].y);
-        nd.b = make_float4(lo[1].x, hi[1].x, lo[1].y, hi[1].y);
-        nd.c = make_float4(lo[0].z, hi[0].z, lo[1].z, hi[1].z);
-        nd.d = make_int4(ref[0], ref[1], 0, 0);
-        nodes[i] = nd;
     }
 }
 
@@ -415,11 +412,13 @@ void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int 
     k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, cubic, b.keys[0], b.vals[0], b.ghist);
     FGL_LAUNCHED("k_morton");
     int slot = 0;
-    radix_sort_pairs(b.keys[0], b.vals[0], b.keys[1], b.vals[1], T, key_bits, b.counts, b.ghist, true, &slot, s);
+    radix_sort_pairs(b.keys[0], b.vals[0], b.keys[1], b.vals[1], T, key_bits, b.sort_status, b.sort_tiles, b.ghist, true,
+                     &b.sort_epoch, &slot, s);
     b.sorted_slot = slot;
-    k_reorder<<<grid_for(T), 256, 0, s>>>(verts, tris, b.vals[slot], T, b.tri, b.leafbox);
-    FGL_LAUNCHED("k_reorder");
     if (T == 1) {
+        k_reorder_refit<<<1, 32, 0, s>>>(verts, tris, b.vals[slot], T, leaf_size, b.child, b.range, b.parent,
+                                         b.flags, b.tri, b.leafbox, b.nodebox, nullptr);
+        FGL_LAUNCHED("k_reorder_refit");
         if (width == 4) {
             k_single4<<<1, 1, 0, s>>>(b.leafbox, b.nodes4);
             FGL_LAUNCHED("k_single4");
@@ -432,17 +431,15 @@ void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int 
     k_karras<<<grid_for(T - 1), 256, 0, s>>>(b.keys[slot], T, b.child, b.range, b.parent);
     FGL_LAUNCHED("k_karras");
     FGL_CUDA(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * (T - 1), s));
-    k_refit<<<grid_for(T), 256, 0, s>>>(T, b.child, b.parent, b.flags, b.leafbox, b.nodebox);
-    FGL_LAUNCHED("k_refit");
+    k_reorder_refit<<<grid_for(T), 256, 0, s>>>(verts, tris, b.vals[slot], T, leaf_size, b.child, b.range, b.parent,
+                                                b.flags, b.tri, b.leafbox, b.nodebox, width == 2 ? b.nodes : nullptr);
+    FGL_LAUNCHED("k_reorder_refit");
     if (width == 4) {
         k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
         FGL_LAUNCHED("k_depth");
         k_nodes4<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.depth, b.leafbox, b.nodebox,
                                                  b.nodes4);
         FGL_LAUNCHED("k_nodes4");
-    } else {
-        k_nodes<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.leafbox, b.nodebox, b.nodes);
-        FGL_LAUNCHED("k_nodes");
     }
 }
 

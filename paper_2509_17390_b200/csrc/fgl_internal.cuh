@@ -77,7 +77,9 @@ struct BuildBuffers {
     uint64_t *keys[2] = {nullptr, nullptr};
     uint32_t *vals[2] = {nullptr, nullptr};
     uint32_t *ghist = nullptr;     // [8][256] digit histograms
-    uint32_t *counts = nullptr;    // [256][nblk] per-block digit counts / offsets
+    uint64_t *sort_status = nullptr;  // [nblk][256] look-back status words (epoch | flag | count)
+    uint32_t *sort_tiles = nullptr;   // [8] per-pass tile counters
+    uint32_t sort_epoch = 0;
     float4 *tri = nullptr;         // [3T] tri48 in leaf order
     int2 *child = nullptr;         // [T-1]
     int2 *range = nullptr;         // [T-1]
@@ -98,7 +100,8 @@ constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
 // sort.cu
 int sort_tile_blocks(int64_t n);
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
-                      uint32_t *counts, uint32_t *ghist, bool ghist_ready, int *result_slot, cudaStream_t s);
+                      uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready, uint32_t *epoch,
+                      int *result_slot, cudaStream_t s);
 void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s);
 
 // build.cu

@@ -1,13 +1,15 @@
 // Stable LSD radix sort of (u64 key, u32 value) pairs, 8-bit digits — the "radix sort run
 // massively in parallel" of PAPER.md §IV-A, written for sm_100a.
 //
-// Per digit pass (reduce-then-scan):
-//   upsweep   : each 4096-key tile counts its digits -> counts[digit][tile]
-//   scan      : one CTA per digit turns its column into global output offsets
-//               (base = keys with a smaller digit, from the all-pass histogram)
-//   downsweep : each tile re-reads its keys, ranks them stably (warp match + per-warp counters,
-//               warps in key order) and scatters key and value to their final positions.
-// The all-pass digit histogram is produced once (fused into the Morton kernel for the build).
+// One kernel per digit pass, single-pass "onesweep" style (decoupled look-back; Merrill & Garland
+// 2016, Adinets & Merrill 2022): a CTA takes the next 4096-key tile from an atomic tile counter,
+// ranks its keys stably (warp match + per-warp digit counters, warps in key order), publishes its
+// per-digit counts, looks back over earlier tiles' published prefixes to find its global offsets
+// (base = keys with a smaller digit, from the all-pass histogram computed once up front — fused
+// into the Morton kernel for the build) and scatters keys and values: one read and one write of
+// each key per pass. Status words carry a per-pass epoch so they never need clearing.
+#include <cuda/atomic>
+
 #include "fgl_internal.cuh"
 
 namespace fgl {
@@ -15,9 +17,13 @@ namespace fgl {
 namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;                      // keys per thread
-constexpr int kTile = kThreads * kItems;        // 4096 keys per tile
+#ifndef FGL_SORT_ITEMS
+#define FGL_SORT_ITEMS 16
+#endif
+constexpr int kItems = FGL_SORT_ITEMS;          // keys per thread
+constexpr int kTile = kThreads * kItems;        // keys per tile
 constexpr int kWarpSpan = kTile / kWarps;       // 512 contiguous keys per warp
+constexpr uint64_t kAgg = 1ull << 30, kPrefix = 2ull << 30, kValMask = (1ull << 30) - 1;
 
 __global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t *__restrict__ keys, int64_t n, int npass,
                                                          uint32_t *__restrict__ ghist) {
@@ -35,108 +41,92 @@ __global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t *__restr
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_upsweep(const uint64_t *__restrict__ keys, int64_t n, int shift,
-                                                      uint32_t *__restrict__ counts, int nblk) {
-    __shared__ uint32_t h[256];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    int64_t base = (int64_t)blockIdx.x * kTile;
-#pragma unroll 4
-    for (int i = 0; i < kItems; ++i) {
-        int64_t idx = base + i * kThreads + threadIdx.x;
-        if (idx < n) atomicAdd(&h[(keys[idx] >> shift) & 0xFF], 1u);
-    }
-    __syncthreads();
-    counts[(int64_t)threadIdx.x * nblk + blockIdx.x] = h[threadIdx.x];
-}
-
-// one CTA per digit: exclusive scan of counts[d][0..nblk) plus the digit's global base
-__global__ void __launch_bounds__(1024) k_scan(uint32_t *__restrict__ counts, int nblk,
-                                               const uint32_t *__restrict__ hist) {
-    __shared__ uint32_t warp_sum[32];
-    __shared__ uint32_t s_base;
-    const int d = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (w == 0) {
-        uint32_t s = 0;
-        for (int i = lane; i < d; i += 32) s += hist[i];
-        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) s_base = s;
-    }
-    __syncthreads();
-    uint32_t carry = s_base;
-    uint32_t *col = counts + (int64_t)d * nblk;
-    for (int start = 0; start < nblk; start += 1024) {
-        int i = start + threadIdx.x;
-        uint32_t v = i < nblk ? col[i] : 0u;
+__global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restrict__ kin,
+                                                       const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
+                                                       uint32_t *__restrict__ vout, int64_t n, int shift,
+                                                       const uint32_t *__restrict__ hist, uint64_t *status,
+                                                       uint32_t *tile_ctr, uint32_t epoch) {
+    __shared__ uint32_t wh[kWarps][256];
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_wsum[kWarps];
+    __shared__ uint32_t s_tile;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&wh[0][0])[i] = 0;
+    // global base of each digit: exclusive scan of this pass's histogram
+    {
+        const uint32_t v = hist[threadIdx.x];
         uint32_t x = v;
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        if (lane == 31) warp_sum[w] = x;
+        if (lane == 31) s_wsum[w] = x;
         __syncthreads();
-        if (w == 0) {
-            uint32_t s = warp_sum[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            warp_sum[lane] = s;
-        }
-        __syncthreads();
-        uint32_t excl = carry + (w ? warp_sum[w - 1] : 0u) + x - v;
-        if (i < nblk) col[i] = excl;
-        carry += warp_sum[31];
-        __syncthreads();
+        uint32_t off = 0;
+        for (int ww = 0; ww < w; ++ww) off += s_wsum[ww];
+        s_base[threadIdx.x] = off + x - v;
     }
-}
-
-__global__ void __launch_bounds__(kThreads) k_downsweep(const uint64_t *__restrict__ kin,
-                                                        const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
-                                                        uint32_t *__restrict__ vout, int64_t n, int shift,
-                                                        const uint32_t *__restrict__ offsets, int nblk) {
-    __shared__ uint32_t wh[kWarps][256];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&wh[0][0])[i] = 0;
     __syncthreads();
+    const uint32_t tile = s_tile;
     const uint32_t lt = (1u << lane) - 1u;
-    const int64_t base = (int64_t)blockIdx.x * kTile + (int64_t)w * kWarpSpan;
+    const int64_t base = (int64_t)tile * kTile + (int64_t)w * kWarpSpan;
     uint64_t key[kItems];
     uint32_t val[kItems];
     uint32_t rank[kItems];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-        int64_t idx = base + i * 32 + lane;
-        bool ok = idx < n;
+        const int64_t idx = base + i * 32 + lane;
+        const bool ok = idx < n;
         key[i] = ok ? kin[idx] : 0ull;
         val[i] = ok ? vin[idx] : 0u;
-        uint32_t d = ok ? (uint32_t)((key[i] >> shift) & 0xFF) : 256u + lane;  // invalid lanes match nobody
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
-        uint32_t before = ok ? wh[w][d] : 0u;
+        const uint32_t d = ok ? (uint32_t)((key[i] >> shift) & 0xFF) : 256u + lane;  // invalid lanes match nobody
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t before = ok ? wh[w][d] : 0u;
         __syncwarp();
         if (ok && (peers & lt) == 0) wh[w][d] = before + __popc(peers);
         __syncwarp();
         rank[i] = before + __popc(peers & lt);
     }
     __syncthreads();
-    // exclusive prefix over warps (warps own consecutive key ranges), digit per thread
+    // per digit (one thread each): tile count, exclusive prefix over warps, decoupled look-back
     {
         const int d = threadIdx.x;
-        uint32_t s = offsets[(int64_t)d * nblk + blockIdx.x];
+        uint32_t cnt = 0;
 #pragma unroll
         for (int ww = 0; ww < kWarps; ++ww) {
-            uint32_t c = wh[ww][d];
-            wh[ww][d] = s;
-            s += c;
+            const uint32_t c = wh[ww][d];
+            wh[ww][d] = cnt;
+            cnt += c;
         }
+        const uint64_t ep = (uint64_t)epoch << 32;
+        // status words carry their own payload, so relaxed (L2-coherent) accesses suffice
+        cuda::atomic_ref<uint64_t, cuda::thread_scope_device> mine(status[(int64_t)tile * 256 + d]);
+        uint32_t excl = 0;
+        if (tile == 0) {
+            mine.store(ep | kPrefix | cnt, cuda::std::memory_order_relaxed);
+        } else {
+            mine.store(ep | kAgg | cnt, cuda::std::memory_order_relaxed);
+            int64_t t = (int64_t)tile - 1;
+            while (t >= 0) {
+                cuda::atomic_ref<uint64_t, cuda::thread_scope_device> prev(status[t * 256 + d]);
+                const uint64_t v = prev.load(cuda::std::memory_order_relaxed);
+                if ((v >> 32) != epoch || (v & (kAgg | kPrefix)) == 0) continue;  // not published yet
+                excl += (uint32_t)(v & kValMask);
+                if (v & kPrefix) break;
+                --t;
+            }
+            mine.store(ep | kPrefix | (excl + cnt), cuda::std::memory_order_relaxed);
+        }
+        s_base[d] += excl;
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
-        int64_t idx = base + i * 32 + lane;
+        const int64_t idx = base + i * 32 + lane;
         if (idx < n) {
-            uint32_t d = (uint32_t)((key[i] >> shift) & 0xFF);
-            uint32_t pos = wh[w][d] + rank[i];
+            const uint32_t d = (uint32_t)((key[i] >> shift) & 0xFF);
+            const uint32_t pos = s_base[d] + wh[w][d] + rank[i];
             kout[pos] = key[i];
             vout[pos] = val[i];
         }
@@ -156,24 +146,23 @@ void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *g
 }
 
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
-                      uint32_t *counts, uint32_t *ghist, bool ghist_ready, int *result_slot, cudaStream_t s) {
+                      uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready, uint32_t *epoch,
+                      int *result_slot, cudaStream_t s) {
     *result_slot = 0;
     if (n <= 1) return;
-    if (n > (int64_t)UINT32_MAX) throw Error(1, "radix sort: n too large");
+    if (n >= (int64_t)kValMask) throw Error(1, "radix sort: n must be < 2^30");
     if (!ghist_ready) digit_histograms(keys0, n, key_bits, ghist, s);
     const int npass = (key_bits + 7) / 8;
     const int nblk = sort_tile_blocks(n);
+    FGL_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t) * 8, s));
     uint64_t *k[2] = {keys0, keys1};
     uint32_t *v[2] = {vals0, vals1};
     int cur = 0;
     for (int p = 0; p < npass; ++p) {
-        const int shift = 8 * p;
-        k_upsweep<<<nblk, kThreads, 0, s>>>(k[cur], n, shift, counts, nblk);
-        FGL_LAUNCHED("k_upsweep");
-        k_scan<<<256, 1024, 0, s>>>(counts, nblk, ghist + 256 * p);
-        FGL_LAUNCHED("k_scan");
-        k_downsweep<<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, shift, counts, nblk);
-        FGL_LAUNCHED("k_downsweep");
+        if (++*epoch == 0) ++*epoch;  // epoch 0 marks never-written status words
+        k_onesweep<<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, 8 * p, ghist + 256 * p, status,
+                                             tile_ctr + p, *epoch);
+        FGL_LAUNCHED("k_onesweep");
         cur ^= 1;
     }
     *result_slot = cur;

@@ -151,7 +151,7 @@ class Scene:
     """A triangle mesh on one GPU with its LBVH. `Scene(verts, tris)` uploads (validating) and
     builds; `cast(poses, pattern)` returns (range, tri_id) device tensors."""
 
-    def __init__(self, verts=None, tris=None, device=None, build: bool = True, morton_bits: int = 21,
+    def __init__(self, verts=None, tris=None, device=None, build: bool = True, morton_bits: int = 0,
                  leaf_size: int = 0, morton_box: int = 0, width: int = 0, stream=None):
         """leaf_size / width 0 = library defaults; morton_box 0 = cubic (R22), 1 = per-axis (Eq. 5)."""
         if device is None:
