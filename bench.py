@@ -140,6 +140,24 @@ def _peaks():
         return 6650.0, "fallback"
 
 
+# Algorithmic FP32 operations of the cast: a slab test of one box is 6 plane
+# distances (1 FMA each) + 6 per-axis min/max + 6 entry/exit reductions + 1 compare = 19; a binary
+# node tests 2 boxes. The watertight triangle test is 9 translations + 27 shear ops + 9 edge-function
+# ops + 6 sign tests + 2 (det) + 3 (T) + 1 division + 3 interval/tie compares = 60.
+OPS_NODE = 38
+OPS_TRI = 60
+
+
+def _alu_peak_tops():
+    """FP32 lane throughput: 148 SMs x 4 SMSPs x 32 lanes x max SM clock (B200_PROFILING.md)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
+    except Exception:
+        mhz = 1965.0
+    return 148 * 128 * mhz * 1e6 / 1e12
+
+
 def _ncu_traffic(config: str):
     """dram read+write bytes per launch of the cast kernel from the committed ncu summary."""
     try:
@@ -299,8 +317,10 @@ def main():
     n_nodes = cres["node_counts"].double().mean().item()
     n_tris = cres["tri_counts"].double().mean().item()
     bytes_per_ray = 64.0 * n_nodes + 48.0 * n_tris + 8.0
-    peak, peak_kind = _peaks()
-    achieved = bytes_per_ray * rays_rank / (cms / 1000) / 1e9
+    hbm_peak, peak_kind = _peaks()
+    ops_per_ray = OPS_NODE * n_nodes + OPS_TRI * n_tris
+    alu_peak = _alu_peak_tops()
+    achieved = ops_per_ray * rays_rank / (cms / 1000) / 1e12
     traffic = _ncu_traffic(a.config)
 
     # --- e2e through the public API with host buffers --------------------------------------
@@ -365,11 +385,17 @@ def main():
             "frames_per_s": P * world / (ms / 1000),
             "cast_rays_per_s": total_rays / (cms / 1000), "cast_ms": cms, "build_ms": st["build_ms"],
             "nodes_per_ray": n_nodes, "tris_per_ray": n_tris,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_cast",
-                         "note": f"algorithmic bytes/ray = 64*nodes + 48*tris + 8 = {bytes_per_ray:.0f} B; "
-                                 f"peak {peak_kind} (MEASURED_PEAKS.json hbm_gbs); cast time from CUDA events "
-                                 f"on the launch stream"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                         "frac": achieved / alu_peak, "traffic": traffic, "kernel": "k_cast",
+                         "note": f"issue-bound traversal (ncu: ~75% issue-slot use, DRAM idle, L2 hit ~85%): "
+                                 f"algorithmic FP32 ops/ray = {OPS_NODE}*nodes + {OPS_TRI}*tris = {ops_per_ray:.0f} "
+                                 f"(DESIGN.md §6); peak = 148 SM x 128 FP32 lanes x 1.965 GHz (unit counts + max "
+                                 f"clock); t_cast from CUDA events on the launch stream; traffic = ncu DRAM bytes "
+                                 f"per launch (profiles/ncu_summary.json)"},
+            "memory": {"algorithmic_bytes_per_ray": bytes_per_ray,
+                       "achieved_gbs": bytes_per_ray * rays_rank / (cms / 1000) / 1e9,
+                       "hbm_peak_gbs": hbm_peak, "hbm_peak_kind": peak_kind,
+                       "note": "node (64 B) + triangle (48 B) fetches + 8 B output per ray, mostly L1/L2-served"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

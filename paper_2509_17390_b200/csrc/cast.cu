@@ -533,20 +533,154 @@ inline bool packet_mode() {
     return v == 1;
 }
 
+// Per-ray BVH2 traversal with dynamic ray fetch (Aila & Laine 2009, "persistent threads" with
+// replacement of terminated rays): a lane whose ray is done idles only until at least kRefill
+// lanes of its warp are idle; then the idle lanes take the next rays of the warp's current 32-ray
+// tile (and of the next tile from the global counter when it runs out). Rays stay in tile order,
+// so a warp holds angular neighbours from at most two adjacent tiles. The traversal itself is the
+// while-while loop of `trace` (same slab and leaf tests, same (t, id) rule), executed one outer
+// iteration at a time so that the refill check runs between leaf batches.
+#ifndef FGL_REFILL
+#define FGL_REFILL 32
+#endif
+template <class Gen, bool kCount>
+__global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
+    k_cast_dyn(const SceneView sv, const Gen gen, int64_t ntiles, const CastOut out, CastCounter *ctr) {
+    constexpr unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    uint64_t st[kStack];  // (entry t bits << 32) | node ref
+    int sp = 0;
+    int32_t cur = kDone, leaf = 0;
+    Pre p;
+    Hit h{0.f, INT_MAX, 0, 0};
+    Ray r;
+    int64_t idx = 0;
+    float tmin = 0.f;
+    bool active = false;
+    unsigned long long wtile = 0;
+    int wpos = 32;  // rays of the warp's current tile already handed out
+    bool exhausted = false;
+    while (true) {
+        const unsigned idle = __ballot_sync(kFull, !active);
+        if (idle == kFull && exhausted) break;
+        if (!exhausted && __popc(idle) >= (idle == kFull ? 1 : FGL_REFILL)) {
+            const int need = __popc(idle), rank = __popc(idle & lt);
+            const int avail = 32 - wpos;
+            unsigned long long tile = wtile;
+            int slot = wpos + rank;
+            if (need > avail) {
+                unsigned long long nt = 0;
+                if (lane == 0) nt = atomicAdd(&ctr->next, 1ull);
+                nt = __shfl_sync(kFull, nt, 0);
+                if (rank >= avail) tile = nt, slot = rank - avail;
+                wtile = nt;
+                wpos = need - avail;
+                if (nt >= (unsigned long long)ntiles) exhausted = true;
+            } else {
+                wpos += need;
+            }
+            if (!active && tile < (unsigned long long)ntiles) {
+                float tmax;
+                if (gen.ray((int64_t)tile, slot, r, idx, tmin, tmax)) {
+                    p = precompute(r);
+                    h = Hit{tmax, INT_MAX, 0, 0};
+                    sp = 0, cur = 0, leaf = 0;
+                    active = true;
+                }
+            }
+        }
+        if (!active) continue;
+        // ---- one outer iteration of the while-while traversal ----
+        auto pop = [&]() -> int32_t {
+            while (sp > 0) {
+                --sp;
+                if (__uint_as_float((uint32_t)(st[sp] >> 32)) <= h.t * kExpand) return (int32_t)(uint32_t)st[sp];
+            }
+            return kDone;
+        };
+        while (cur >= 0 && cur != kDone) {
+            const float4 *np = reinterpret_cast<const float4 *>(sv.nodes + cur);
+            const float4 na = __ldg(np), nb = __ldg(np + 1), nc = __ldg(np + 2);
+            const int4 nd = __ldg(reinterpret_cast<const int4 *>(np + 3));
+            if (kCount) ++h.nodes;
+            const float lim = h.t;
+            const float t0 = slab(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim);
+            const float t1 = slab(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim);
+            const bool h0 = t0 != INFINITY, h1 = t1 != INFINITY;
+            if (h0 && h1) {
+                const bool swap = t1 < t0;
+                st[sp++] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
+                cur = swap ? nd.y : nd.x;
+            } else if (h0) {
+                cur = nd.x;
+            } else if (h1) {
+                cur = nd.y;
+            } else {
+                cur = pop();
+            }
+            if (cur < 0 && leaf == 0) {
+                leaf = cur;
+                cur = pop();
+            }
+            if (!__any_sync(__activemask(), leaf == 0)) break;
+        }
+        while (leaf < 0) {
+            const int32_t v = ~leaf;
+            const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
+            for (int32_t k = first; k < first + cnt; ++k) {
+                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+                const int32_t id = __float_as_int(a.w);
+                if (kCount) ++h.tris;
+                float t;
+                if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, t)) {
+                    h.t = t;
+                    h.id = id;
+                }
+            }
+            leaf = 0;
+            if (cur < 0) {
+                leaf = cur;
+                cur = pop();
+            }
+        }
+        if (cur == kDone) {
+            write_out(out, idx, r, h);
+            active = false;
+        }
+    }
+    if (lane == 0) {
+        const unsigned int total = gridDim.x * (blockDim.x >> 5);
+        if (atomicAdd(&ctr->done, 1u) == total - 1) {
+            ctr->next = 0ull;
+            ctr->done = 0u;
+            __threadfence();
+        }
+    }
+}
+
 template <class Gen, bool kCount, int kMode>
 void launch_one(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
                 cudaStream_t s) {
     static int oc = 0, sms = 0;
+    constexpr bool kDyn = kMode == kRay2;
     if (!oc) {
         int dev;
         FGL_CUDA(cudaGetDevice(&dev));
         FGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast<Gen, kCount, kMode>, kCastThreads, 0));
+        if (kDyn)
+            FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast_dyn<Gen, kCount>, kCastThreads, 0));
+        else
+            FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast<Gen, kCount, kMode>, kCastThreads, 0));
         if (oc < 1) oc = 1;
     }
     int64_t blocks = std::min<int64_t>((int64_t)sms * oc, (ntiles + kCastThreads / 32 - 1) / (kCastThreads / 32));
     blocks = std::max<int64_t>(blocks, 1);
-    k_cast<Gen, kCount, kMode><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
+    if (kDyn)
+        k_cast_dyn<Gen, kCount><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
+    else
+        k_cast<Gen, kCount, kMode><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
     FGL_LAUNCHED("k_cast");
 }
 
@@ -650,7 +784,10 @@ void launch_cast_spinning(const SceneView &sv, const SpinParams &p, const float 
     SpinGen g;
     g.sp = p;
     g.poses = poses;
-    g.tc = p.channels >= 4 ? 4 : (p.channels >= 2 ? 2 : 1);
+#ifndef FGL_TILE_C
+#define FGL_TILE_C 4
+#endif
+    g.tc = p.channels >= FGL_TILE_C ? FGL_TILE_C : (p.channels >= 4 ? 4 : (p.channels >= 2 ? 2 : 1));
     g.ta = 32 / g.tc;
     g.nct = (p.channels + g.tc - 1) / g.tc;
     g.nat = (p.columns + g.ta - 1) / g.ta;
