@@ -77,7 +77,7 @@ void dalloc(fgl_scene *s, T **p, size_t n) {
 void free_build(fgl_scene *s) {
     fgl::BuildBuffers &b = s->b;
     void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.sort_status, b.sort_tiles,
-                  b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth};
+                  b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth, b.agg};
     for (void *p : ps)
         if (p) cudaFree(p);
     b = fgl::BuildBuffers();
@@ -111,6 +111,11 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.nodebox, 2 * nin);
     dalloc(s, &b.nodes, nin);
     dalloc(s, &b.nodes4, nin);
+    {
+        int64_t m = T, tot = 0;
+        for (int k = 0; k < 10; ++k) tot += (m = (m + 7) / 8);
+        dalloc(s, &b.agg, 2 * tot);
+    }
     dalloc(s, &b.depth, nin);
 }
 

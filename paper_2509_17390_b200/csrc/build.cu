@@ -218,68 +218,129 @@ __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, 
     }
 }
 
-// Fused leaf-order gather + Eq. 7 bottom-up refit + binary traversal nodes. Thread j:
-//   tri48[j] = triangle perm[j] {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}; leaf box j (exact min/max);
-//   then climbs: at each parent the FIRST arriving child stops (acq_rel arrival counter), the
-//   second computes B(n) = B(left) U B(right) (Eq. 7) from its own box (registers) and the
-//   sibling's (L2), stores it, and — width 2 — writes the node64 of that parent (children that
-//   cover <= leaf_size triangles become leaves).
-__global__ void __launch_bounds__(256) k_reorder_refit(const float *__restrict__ verts,
-                                                       const int32_t *__restrict__ tris,
-                                                       const uint32_t *__restrict__ perm, int64_t n, int leaf_size,
-                                                       const int2 *__restrict__ child, const int2 *__restrict__ range,
-                                                       const int32_t *__restrict__ parent, int32_t *__restrict__ flags,
-                                                       float4 *__restrict__ tri, float4 *__restrict__ leafbox,
-                                                       float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+// Leaf-order gather: tri48[j] = triangle perm[j] {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}, its exact
+// box leafbox[j], and the union of every 8 consecutive leaf boxes (agg[0], 8-lane reduction).
+__device__ __forceinline__ void warp_union(float4 &lo, float4 &hi) {
+    for (int o = 4; o; o >>= 1) {
+        lo.x = fminf(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
+        lo.y = fminf(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
+        lo.z = fminf(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
+        hi.x = fmaxf(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
+        hi.y = fmaxf(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
+        hi.z = fmaxf(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
+    }
+}
+
+constexpr float kInf = __builtin_huge_valf();
+
+__global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, const int32_t *__restrict__ tris,
+                                                 const uint32_t *__restrict__ perm, int64_t n,
+                                                 float4 *__restrict__ tri, float4 *__restrict__ leafbox,
+                                                 float4 *__restrict__ agg) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
+    if (j < n) {
         const uint32_t k = perm[j];
         const float3 a = ldv(verts, __ldg(tris + 3 * (int64_t)k)), b = ldv(verts, __ldg(tris + 3 * (int64_t)k + 1)),
                      c = ldv(verts, __ldg(tris + 3 * (int64_t)k + 2));
         tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
         tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
         tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
-        float4 lo = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
-        float4 hi = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
-        __stcg(leafbox + 2 * j, lo);
-        __stcg(leafbox + 2 * j + 1, hi);
-        if (n == 1) continue;
-        int32_t cur = ~(int32_t)j;  // child reference of the subtree whose box is in (lo, hi)
-        int32_t cf = (int32_t)j, cl = (int32_t)j;
-        int32_t p = parent[(n - 1) + j];
-        while (p >= 0) {
-            // read-only topology first (overlaps the arrival atomic)
-            const int2 cp = __ldg(child + p);
-            const int2 rp = __ldg(range + p);
-            const int32_t pp = __ldg(parent + p);
-            // release-only arrival: our box stores (leafbox / nodebox) are ordered before it; the
-            // second arriver reads the sibling's box from L2 (ld.cg), never a stale L1 line
-            int32_t old;
-            asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(flags + p) : "memory");
-            if (old == 0) break;
-            const bool left = cp.x == cur;
-            const int32_t sib = left ? cp.y : cp.x;
-            const float4 *sb = sib >= 0 ? nodebox + 2 * (int64_t)sib : leafbox + 2 * (int64_t)(~sib);
-            const float4 slo = __ldcg(sb), shi = __ldcg(sb + 1);
-            const float4 nlo = make_float4(fminf(lo.x, slo.x), fminf(lo.y, slo.y), fminf(lo.z, slo.z), 0.f);
-            const float4 nhi = make_float4(fmaxf(hi.x, shi.x), fmaxf(hi.y, shi.y), fmaxf(hi.z, shi.z), 0.f);
-            __stcg(nodebox + 2 * (int64_t)p, nlo);
-            __stcg(nodebox + 2 * (int64_t)p + 1, nhi);
-            if (nodes) {
-                // child refs: leaves, subtrees of <= leaf_size triangles collapse to leaves
-                const int32_t sf = left ? cl + 1 : rp.x, sl = left ? rp.y : cf - 1;
-                const int32_t mref = (cur < 0 || cl - cf + 1 <= leaf_size) ? make_leaf(cf, cl - cf + 1) : cur;
-                const int32_t sref = (sib < 0 || sl - sf + 1 <= leaf_size) ? make_leaf(sf, sl - sf + 1) : sib;
-                const float4 l0 = left ? lo : slo, h0 = left ? hi : shi, l1 = left ? slo : lo, h1 = left ? shi : hi;
-                Node64 nd;
-                nd.a = make_float4(l0.x, h0.x, l0.y, h0.y);
-                nd.b = make_float4(l1.x, h1.x, l1.y, h1.y);
-                nd.c = make_float4(l0.z, h0.z, l1.z, h1.z);
-                nd.d = make_int4(left ? mref : sref, left ? sref : mref, 0, 0);
-                nodes[p] = nd;
-            }
-            lo = nlo, hi = nhi, cur = p, cf = rp.x, cl = rp.y;
-            p = pp;
+        lo = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
+        hi = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
+        leafbox[2 * j] = lo;
+        leafbox[2 * j + 1] = hi;
+    }
+    warp_union(lo, hi);
+    if ((threadIdx.x & 7) == 0 && j < n) {
+        agg[2 * (j >> 3)] = lo;
+        agg[2 * (j >> 3) + 1] = hi;
+    }
+}
+
+// next aggregate level: union of every 8 consecutive boxes of the level below
+__global__ void __launch_bounds__(256) k_aggregate(const float4 *__restrict__ in, int64_t n_in,
+                                                   float4 *__restrict__ out) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
+    if (j < n_in) lo = in[2 * j], hi = in[2 * j + 1];
+    warp_union(lo, hi);
+    if ((threadIdx.x & 7) == 0 && j < n_in) out[2 * (j >> 3)] = lo, out[2 * (j >> 3) + 1] = hi;
+}
+
+constexpr int kMaxAgg = 10;  // 8^10 > 2^28 triangles
+// level 0 = leaf boxes [n]; levels 1..nlev-1 = unions of 8^k consecutive leaves, stored one after
+// the other in `agg` (level k has ceil(n / 8^k) entries)
+struct AggLevels {
+    const float4 *leaf, *agg;
+    int64_t n;
+    int nlev;
+};
+
+__device__ __forceinline__ void acc(float4 &lo, float4 &hi, const float4 *p, int64_t i) {
+    const float4 l = __ldg(p + 2 * i), h = __ldg(p + 2 * i + 1);
+    lo.x = fminf(lo.x, l.x), lo.y = fminf(lo.y, l.y), lo.z = fminf(lo.z, l.z);
+    hi.x = fmaxf(hi.x, h.x), hi.y = fmaxf(hi.y, h.y), hi.z = fmaxf(hi.z, h.z);
+}
+
+// Eq. 7 by its closed form: the box of a node covering sorted leaves [a, b] is the union of their
+// boxes (exact: min/max do not round). Evaluated with the 8-ary aggregates: at most 7 + 7 reads per
+// level (independent loads, unrolled), <= 8 at the top level.
+__device__ __forceinline__ void range_box(const AggLevels &L, int64_t a, int64_t b, float4 &lo, float4 &hi) {
+    lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
+    int64_t A = a, B = b + 1;  // half-open, in units of the current level
+    int64_t cnt = L.n, off = -1;
+    for (int lv = 0; lv < L.nlev && A < B; ++lv) {
+        const float4 *p = lv == 0 ? L.leaf : L.agg + 2 * off;
+        off = lv == 0 ? 0 : off + cnt;
+        cnt = (cnt + 7) / 8;
+        if (lv + 1 < L.nlev) {
+            const int64_t rem = B - A;
+            const int nf = (int)(((8 - (A & 7)) & 7) < rem ? ((8 - (A & 7)) & 7) : rem);
+#pragma unroll
+            for (int k = 0; k < 7; ++k)
+                if (k < nf) acc(lo, hi, p, A + k);
+            A += nf;
+            const int64_t rem2 = B - A;
+            const int nb = (int)((B & 7) < rem2 ? (B & 7) : rem2);
+#pragma unroll
+            for (int k = 0; k < 7; ++k)
+                if (k < nb) acc(lo, hi, p, B - 1 - k);
+            B -= nb;
+            A >>= 3, B >>= 3;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (A + k < B) acc(lo, hi, p, A + k);
         }
+    }
+}
+
+// Binary traversal nodes (node64) and the Eq. 7 node boxes, one thread per internal node, no
+// inter-thread dependencies: children boxes from range_box; subtrees of <= leaf_size triangles
+// become leaves.
+__global__ void __launch_bounds__(256) k_nodes_scan(int64_t n, int leaf_size, const int2 *__restrict__ child,
+                                                    const int2 *__restrict__ range, AggLevels L,
+                                                    float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    const int2 c = child[i], r = range[i];
+    const int32_t g = c.x >= 0 ? c.x : ~c.x;  // split: left child covers [f, g], right [g + 1, l]
+    float4 l0, h0, l1, h1;
+    range_box(L, r.x, g, l0, h0);
+    range_box(L, g + 1, r.y, l1, h1);
+    nodebox[2 * i] = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.f);
+    nodebox[2 * i + 1] = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.f);
+    if (nodes) {
+        const int32_t n0 = g - r.x + 1, n1 = r.y - g;
+        const int32_t ref0 = (c.x < 0 || n0 <= leaf_size) ? make_leaf(r.x, n0) : c.x;
+        const int32_t ref1 = (c.y < 0 || n1 <= leaf_size) ? make_leaf(g + 1, n1) : c.y;
+        Node64 nd;
+        nd.a = make_float4(l0.x, h0.x, l0.y, h0.y);
+        nd.b = make_float4(l1.x, h1.x, l1.y, h1.y);
+        nd.c = make_float4(l0.z, h0.z, l1.z, h1.z);
+        nd.d = make_int4(ref0, ref1, 0, 0);
+        nodes[i] = nd;
     }
 }
 
@@ -415,10 +476,20 @@ void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int 
     radix_sort_pairs(b.keys[0], b.vals[0], b.keys[1], b.vals[1], T, key_bits, b.sort_status, b.sort_tiles, b.ghist, true,
                      &b.sort_epoch, &slot, s);
     b.sorted_slot = slot;
+    // leaf-order records, leaf boxes and the 32-ary box aggregates used by the refit
+    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, tris, b.vals[slot], T, b.tri, b.leafbox, b.agg);
+    FGL_LAUNCHED("k_reorder");
+    AggLevels L;
+    L.leaf = b.leafbox;
+    L.agg = b.agg;
+    L.n = T;
+    L.nlev = 2;
+    for (int64_t m = (T + 7) / 8, off = 0; m > 8 && L.nlev <= kMaxAgg; off += m, m = (m + 7) / 8) {
+        k_aggregate<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(b.agg + 2 * off, m, b.agg + 2 * (off + m));
+        FGL_LAUNCHED("k_aggregate");
+        ++L.nlev;
+    }
     if (T == 1) {
-        k_reorder_refit<<<1, 32, 0, s>>>(verts, tris, b.vals[slot], T, leaf_size, b.child, b.range, b.parent,
-                                         b.flags, b.tri, b.leafbox, b.nodebox, nullptr);
-        FGL_LAUNCHED("k_reorder_refit");
         if (width == 4) {
             k_single4<<<1, 1, 0, s>>>(b.leafbox, b.nodes4);
             FGL_LAUNCHED("k_single4");
@@ -430,10 +501,9 @@ void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int 
     }
     k_karras<<<grid_for(T - 1), 256, 0, s>>>(b.keys[slot], T, b.child, b.range, b.parent);
     FGL_LAUNCHED("k_karras");
-    FGL_CUDA(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * (T - 1), s));
-    k_reorder_refit<<<grid_for(T), 256, 0, s>>>(verts, tris, b.vals[slot], T, leaf_size, b.child, b.range, b.parent,
-                                                b.flags, b.tri, b.leafbox, b.nodebox, width == 2 ? b.nodes : nullptr);
-    FGL_LAUNCHED("k_reorder_refit");
+    k_nodes_scan<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, leaf_size, b.child, b.range, L, b.nodebox,
+                                                                width == 2 ? b.nodes : nullptr);
+    FGL_LAUNCHED("k_nodes_scan");
     if (width == 4) {
         k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
         FGL_LAUNCHED("k_depth");

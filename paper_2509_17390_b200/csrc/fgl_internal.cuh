@@ -87,6 +87,7 @@ struct BuildBuffers {
     int32_t *flags = nullptr;      // [T-1]
     float4 *leafbox = nullptr;     // [2T]
     float4 *nodebox = nullptr;     // [2(T-1)]
+    float4 *agg = nullptr;         // 8-ary box aggregates, level after level (unions of 8^k leaves)
     Node64 *nodes = nullptr;       // [max(T-1,1)]
     Node128 *nodes4 = nullptr;     // [max(T-1,1)]
     int32_t *depth = nullptr;      // [T-1]
