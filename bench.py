@@ -44,6 +44,7 @@ def _args():
     ap.add_argument("--width", type=int, default=0, help="BVH node width 2 or 4 (0 = library default)")
     ap.add_argument("--morton-bits", type=int, default=0, help="b of Eq. 5 (0 = library default)")
     ap.add_argument("--morton-box", type=int, default=0, help="0 = cubic (R22, default), 1 = per-axis (Eq. 5)")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -270,7 +271,7 @@ def main():
 
     def step(cast_ev=None):
         if a.mode == "full":
-            scene.upload(verts_d, tris_d)        # A1 (D2D copy + validation)
+            scene.upload(verts_d, tris_d, sync=False)  # A1 (D2D copy + validation, checked after the run)
             scene.build()                        # A2-A7
         if cast_ev:
             cast_ev[0].record(stream)
@@ -284,6 +285,23 @@ def main():
     for _ in range(a.warmup):
         step()
     torch.cuda.synchronize()
+    use_graph = not a.no_graph and world == 1
+    graph = None
+    if use_graph:
+        # the whole step (upload copies, ~20 build kernels, the cast) as one CUDA graph
+        gev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        for _ in range(a.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     K = a.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -296,13 +314,30 @@ def main():
             if flush is not None:
                 flush.zero_()                    # evict L2 between timed steps (not timed)
             ev[i][0].record(stream)
-            step(cev[i])
+            if graph is not None:
+                graph.replay()
+            else:
+                step(cev[i])
             ev[i][1].record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
     launches = fgl.kernel_launches() - launches0
+    scene.check()  # validation result of the (asynchronous) uploads
     step_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    if graph is not None:
+        # graph replays launch the same kernels as the eager step: count them from one eager step,
+        # and time the cast part with events on eager casts of the same inputs
+        l0 = fgl.kernel_launches()
+        step()
+        launches = (fgl.kernel_launches() - l0) * K
+        for i in range(K):
+            if flush is not None:
+                flush.zero_()
+            cev[i][0].record(stream)
+            scene.cast(poses_d, pat, out=out)
+            cev[i][1].record(stream)
+        torch.cuda.synchronize()
     cast_ms = [e[0].elapsed_time(e[1]) for e in cev]
     ms = statistics.mean(step_ms)
     cms = statistics.mean(cast_ms)
@@ -381,6 +416,7 @@ def main():
                        if a.mode == "full" else "cast only (prebuilt scene)",
                        "triangles": m.T, "rays_per_step": total_rays, "poses_per_step": P * world,
                        "l2": "flushed between steps (256 MiB memset, untimed)" if flush is not None else "not flushed",
+                       "launch": "one CUDA graph replay per step" if graph is not None else "eager launches",
                        "parallelism": f"dp{world} (poses sharded, mesh replicated)"},
             "frames_per_s": P * world / (ms / 1000),
             "cast_rays_per_s": total_rays / (cms / 1000), "cast_ms": cms, "build_ms": st["build_ms"],

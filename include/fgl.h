@@ -48,7 +48,7 @@ typedef enum {
     FGL_E_CUDA = 4      /* any CUDA runtime error; the message carries cudaGetErrorString    */
 } fgl_status;
 
-enum { FGL_HOST = 0, FGL_DEVICE = 1 };
+enum { FGL_HOST = 0, FGL_DEVICE = 1, FGL_ASYNC = 4 /* or'ed into ptr_kind: see upload */ };
 
 typedef struct fgl_scene fgl_scene; /* opaque: device copies of the mesh, the BVH and scratch */
 
@@ -97,7 +97,10 @@ FGL_API void fgl_scene_destroy(fgl_scene *scene);
 /* Copy the mesh M = {tri_k} into scene-owned device memory and validate it:
  * verts: float32 [V][3]; tris: int32 [T][3], 0 <= index < V. ptr_kind says whether both pointers
  * are FGL_HOST or FGL_DEVICE. Synchronises `cuda_stream` to report FGL_E_DATA (T = 0, an index out
- * of range, a non-finite vertex). Invalidates any previous build. T must be < 2^28. */
+ * of range, a non-finite vertex). Invalidates any previous build. T must be < 2^28.
+ * With FGL_ASYNC or'ed into ptr_kind the call does not synchronise (graph-capturable): the
+ * validation result stays on the device and fgl_scene_check reports it; until then the build and
+ * casts stay memory-safe (indices are clamped) but their results are unspecified for bad meshes. */
 FGL_API fgl_status fgl_scene_upload_mesh(fgl_scene *scene, const float *verts, int64_t V, const int32_t *tris,
                                  int64_t T, int ptr_kind, void *cuda_stream);
 
@@ -106,6 +109,9 @@ FGL_API fgl_status fgl_scene_upload_mesh(fgl_scene *scene, const float *verts, i
  * (Eq. 6) -> bottom-up refit (Eq. 7) -> triangle records reordered into leaf order -> traversal
  * nodes. opts may be NULL (defaults). Does no host synchronisation. */
 FGL_API fgl_status fgl_scene_build(fgl_scene *scene, const fgl_build_opts *opts, void *cuda_stream);
+
+/* Synchronises `cuda_stream` and returns FGL_E_DATA if the last upload failed validation. */
+FGL_API fgl_status fgl_scene_check(fgl_scene *scene, void *cuda_stream);
 
 /* Fills *out. Synchronises on the last build's end event (for build_ms and the scene box). */
 FGL_API fgl_status fgl_scene_stats(fgl_scene *scene, fgl_stats *out);

@@ -236,6 +236,8 @@ fgl_status fgl_scene_upload_mesh(fgl_scene *s, const float *verts, int64_t V, co
                                  int ptr_kind, void *stream) {
     FGL_API_BEGIN
     if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    const bool async = (ptr_kind & FGL_ASYNC) != 0;
+    ptr_kind &= ~FGL_ASYNC;
     if (ptr_kind != FGL_HOST && ptr_kind != FGL_DEVICE) throw Error(FGL_E_USAGE, "ptr_kind must be FGL_HOST or FGL_DEVICE");
     if (T <= 0) throw Error(FGL_E_DATA, "mesh has no triangles (T = 0)");
     if (V <= 0) throw Error(FGL_E_DATA, "mesh has no vertices");
@@ -262,6 +264,20 @@ fgl_status fgl_scene_upload_mesh(fgl_scene *s, const float *verts, int64_t V, co
     FGL_CUDA(cudaMemcpyAsync(s->verts, verts, sizeof(float) * 3 * V, kind, st));
     FGL_CUDA(cudaMemcpyAsync(s->tris, tris, sizeof(int32_t) * 3 * T, kind, st));
     fgl::launch_validate(s->verts, V, s->tris, T, s->vflag, st);
+    if (async) return FGL_OK;
+    FGL_CUDA(cudaMemcpyAsync(s->hflag, s->vflag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    FGL_CUDA(cudaStreamSynchronize(st));
+    if (*s->hflag & 1u) throw Error(FGL_E_DATA, "triangle index out of range [0, V)");
+    if (*s->hflag & 2u) throw Error(FGL_E_DATA, "non-finite vertex coordinate");
+    FGL_API_END
+}
+
+fgl_status fgl_scene_check(fgl_scene *s, void *stream) {
+    FGL_API_BEGIN
+    if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
     FGL_CUDA(cudaMemcpyAsync(s->hflag, s->vflag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
     FGL_CUDA(cudaStreamSynchronize(st));
     if (*s->hflag & 1u) throw Error(FGL_E_DATA, "triangle index out of range [0, V)");
@@ -289,9 +305,12 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     DeviceGuard g(s->dev);
     cudaStream_t st = (cudaStream_t)stream;
     s->bits = bits, s->leaf_size = leaf;
-    FGL_CUDA(cudaEventRecord(s->ev0, st));
-    fgl::launch_build(s->verts, s->tris, s->b, bits, leaf, cubic, width, st);
-    FGL_CUDA(cudaEventRecord(s->ev1, st));
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    FGL_CUDA(cudaStreamIsCapturing(st, &cap));
+    const bool timed = cap == cudaStreamCaptureStatusNone;  // build_ms is not recorded inside a graph
+    if (timed) FGL_CUDA(cudaEventRecord(s->ev0, st));
+    fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, st);
+    if (timed) FGL_CUDA(cudaEventRecord(s->ev1, st));
     s->built = true;
     FGL_API_END
 }
@@ -371,7 +390,7 @@ fgl_status fgl_cast_rays_bruteforce(const fgl_scene *s, const float *orig, const
     if (R == 0) return FGL_OK;
     if (!orig || !dir || !range || !tri_id) throw Error(FGL_E_USAGE, "NULL pointer argument");
     DeviceGuard g(s->dev);
-    fgl::launch_cast_bruteforce(s->verts, s->tris, s->T, orig, dir, R, t_min, t_max, range, tri_id,
+    fgl::launch_cast_bruteforce(s->verts, s->V, s->tris, s->T, orig, dir, R, t_min, t_max, range, tri_id,
                                 (cudaStream_t)stream);
     FGL_API_END
 }

@@ -29,6 +29,9 @@ __global__ void k_validate(const float *__restrict__ verts, int64_t V, const int
     if (bad) atomicOr(flag, bad);
 }
 
+// vertex gather with the index clamped to [0, V) (memory-safe before validation is checked)
+__device__ __forceinline__ int32_t clampv(int32_t i, int64_t V) { return i < 0 ? 0 : (i >= V ? (int32_t)(V - 1) : i); }
+
 __device__ __forceinline__ float3 ldv(const float *__restrict__ verts, int32_t i) {
     return make_float3(__ldg(verts + 3 * (int64_t)i), __ldg(verts + 3 * (int64_t)i + 1), __ldg(verts + 3 * (int64_t)i + 2));
 }
@@ -47,12 +50,14 @@ __device__ __forceinline__ float warp_max(float v) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) k_prep(const float *__restrict__ verts, const int32_t *__restrict__ tris,
+__global__ void __launch_bounds__(256) k_prep(const float *__restrict__ verts, int64_t V,
+                                              const int32_t *__restrict__ tris,
                                               int64_t T, float4 *__restrict__ cent, float *__restrict__ partial,
                                               unsigned int *sync, float *__restrict__ box) {
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < T; k += (int64_t)gridDim.x * blockDim.x) {
-        int32_t i0 = __ldg(tris + 3 * k), i1 = __ldg(tris + 3 * k + 1), i2 = __ldg(tris + 3 * k + 2);
+        const int32_t i0 = clampv(__ldg(tris + 3 * k), V), i1 = clampv(__ldg(tris + 3 * k + 1), V),
+                      i2 = clampv(__ldg(tris + 3 * k + 2), V);
         float3 a = ldv(verts, i0), b = ldv(verts, i1), c = ldv(verts, i2);
         float4 m = make_float4(centroid1(a.x, b.x, c.x), centroid1(a.y, b.y, c.y), centroid1(a.z, b.z, c.z), 0.f);
         cent[k] = m;
@@ -233,7 +238,8 @@ __device__ __forceinline__ void warp_union(float4 &lo, float4 &hi) {
 
 constexpr float kInf = __builtin_huge_valf();
 
-__global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, const int32_t *__restrict__ tris,
+__global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, int64_t V,
+                                                 const int32_t *__restrict__ tris,
                                                  const uint32_t *__restrict__ perm, int64_t n,
                                                  float4 *__restrict__ tri, float4 *__restrict__ leafbox,
                                                  float4 *__restrict__ agg) {
@@ -241,8 +247,9 @@ __global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts
     float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
     if (j < n) {
         const uint32_t k = perm[j];
-        const float3 a = ldv(verts, __ldg(tris + 3 * (int64_t)k)), b = ldv(verts, __ldg(tris + 3 * (int64_t)k + 1)),
-                     c = ldv(verts, __ldg(tris + 3 * (int64_t)k + 2));
+        const float3 a = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k), V)),
+                     b = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 1), V)),
+                     c = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 2), V));
         tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
         tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
         tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
@@ -462,12 +469,12 @@ void launch_morton_points(const float *pts, int64_t n, const float *lo, const fl
     FGL_LAUNCHED("k_morton_points");
 }
 
-void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size, int cubic,
-                  int width, cudaStream_t s) {
+void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
+                  int cubic, int width, cudaStream_t s) {
     b.width = width;
     const int64_t T = b.T;
     const int key_bits = 3 * bits;
-    k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, tris, T, b.cent, b.partial, b.sync, b.box);
+    k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
     FGL_LAUNCHED("k_prep");
     FGL_CUDA(cudaMemsetAsync(b.ghist, 0, sizeof(uint32_t) * 8 * 256, s));
     k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, cubic, b.keys[0], b.vals[0], b.ghist);
@@ -477,7 +484,7 @@ void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int 
                      &b.sort_epoch, &slot, s);
     b.sorted_slot = slot;
     // leaf-order records, leaf boxes and the 32-ary box aggregates used by the refit
-    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, tris, b.vals[slot], T, b.tri, b.leafbox, b.agg);
+    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, b.vals[slot], T, b.tri, b.leafbox, b.agg);
     FGL_LAUNCHED("k_reorder");
     AggLevels L;
     L.leaf = b.leafbox;

@@ -707,7 +707,7 @@ void launch_persistent(const SceneView &sv, const Gen &gen, int64_t ntiles, cons
 
 // ---- brute force: every ray against every triangle, triangles staged in smem -------
 constexpr int kBfThreads = 128;
-__global__ void __launch_bounds__(kBfThreads) k_bruteforce(const float *__restrict__ verts,
+__global__ void __launch_bounds__(kBfThreads) k_bruteforce(const float *__restrict__ verts, int64_t V,
                                                            const int32_t *__restrict__ tris, int64_t T,
                                                            const float *__restrict__ orig,
                                                            const float *__restrict__ dir, int64_t R, float tmin,
@@ -728,7 +728,8 @@ __global__ void __launch_bounds__(kBfThreads) k_bruteforce(const float *__restri
         const int64_t k = base + threadIdx.x;
         if (k < T) {
             for (int v = 0; v < 3; ++v) {
-                const int32_t vi = tris[3 * k + v];
+                int32_t vi = tris[3 * k + v];
+                vi = vi < 0 ? 0 : (vi >= V ? (int32_t)(V - 1) : vi);
                 st[threadIdx.x][v] = make_float4(verts[3 * (int64_t)vi], verts[3 * (int64_t)vi + 1],
                                                  verts[3 * (int64_t)vi + 2], 0.f);
             }
@@ -809,11 +810,12 @@ void launch_cast_rays(const SceneView &sv, const float *orig, const float *dir, 
     launch_persistent(sv, g, (R + 31) / 32, o, ctr, s);
 }
 
-void launch_cast_bruteforce(const float *verts, const int32_t *tris, int64_t T, const float *orig, const float *dir,
-                            int64_t R, float t_min, float t_max, float *range, int32_t *tri_id, cudaStream_t s) {
+void launch_cast_bruteforce(const float *verts, int64_t V, const int32_t *tris, int64_t T, const float *orig,
+                            const float *dir, int64_t R, float t_min, float t_max, float *range, int32_t *tri_id,
+                            cudaStream_t s) {
     if (R <= 0) return;
-    k_bruteforce<<<(unsigned)((R + kBfThreads - 1) / kBfThreads), kBfThreads, 0, s>>>(verts, tris, T, orig, dir, R,
-                                                                                       t_min, t_max, range, tri_id);
+    k_bruteforce<<<(unsigned)((R + kBfThreads - 1) / kBfThreads), kBfThreads, 0, s>>>(verts, V, tris, T, orig, dir,
+                                                                                       R, t_min, t_max, range, tri_id);
     FGL_LAUNCHED("k_bruteforce");
 }
 

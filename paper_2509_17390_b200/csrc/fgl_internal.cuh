@@ -106,8 +106,8 @@ void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_
 void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s);
 
 // build.cu
-void launch_build(const float *verts, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size, int cubic,
-                  int width, cudaStream_t s);
+void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
+                  int cubic, int width, cudaStream_t s);
 void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
                      cudaStream_t s);
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
@@ -143,7 +143,8 @@ void launch_cast_rosette(const SceneView &sv, const RosetteParams &p, const floa
                          const CastOut &o, CastCounter *ctr, cudaStream_t s);
 void launch_cast_rays(const SceneView &sv, const float *orig, const float *dir, int64_t R, float t_min, float t_max,
                       const CastOut &o, CastCounter *ctr, cudaStream_t s);
-void launch_cast_bruteforce(const float *verts, const int32_t *tris, int64_t T, const float *orig, const float *dir,
+void launch_cast_bruteforce(const float *verts, int64_t V, const int32_t *tris, int64_t T, const float *orig,
+                            const float *dir,
                             int64_t R, float t_min, float t_max, float *range, int32_t *tri_id, cudaStream_t s);
 void launch_export_spinning(const SpinParams &p, const float *poses, int64_t P, float *orig, float *dir,
                             cudaStream_t s);

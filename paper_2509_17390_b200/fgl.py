@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FGL_LIB") or os.path.join(HERE, "libfgl.so")  # FGL_LIB: A/B builds
 
 OK, E_USAGE, E_DATA, E_RESOURCE, E_CUDA = range(5)
-HOST, DEVICE = 0, 1
+HOST, DEVICE, ASYNC = 0, 1, 4
 
 
 class FglError(RuntimeError):
@@ -62,6 +62,7 @@ _SIGS = {
     "fgl_scene_upload_mesh": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int, c_void_p]),
     "fgl_scene_build": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fgl_scene_stats": (c_int, [c_void_p, POINTER(Stats)]),
+    "fgl_scene_check": (c_int, [c_void_p, c_void_p]),
     "fgl_cast_spinning": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p]),
     "fgl_cast_rosette": (c_int, [c_void_p, POINTER(RosetteC), c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
@@ -179,7 +180,9 @@ class Scene:
     __del__ = close
 
     # ---- upload / build -------------------------------------------------------------------
-    def upload(self, verts, tris, stream=None):
+    def upload(self, verts, tris, stream=None, sync: bool = True):
+        """Copy + validate the mesh. sync=False: no host synchronisation (CUDA-graph capturable);
+        call check() to surface a validation error."""
         on_dev = isinstance(verts, torch.Tensor) and verts.is_cuda
         if on_dev:
             v = verts.to(torch.float32).contiguous()
@@ -193,7 +196,7 @@ class Scene:
             kind, pv, pt = HOST, v.ctypes.data, t.ctypes.data
         V = int(v.shape[0]) if v.ndim > 1 else int(v.size) // 3
         T = int(t.shape[0]) if t.ndim > 1 else int(t.size) // 3
-        _check(lib().fgl_scene_upload_mesh(self._h, pv, V, pt, T, kind, _stream(stream)))
+        _check(lib().fgl_scene_upload_mesh(self._h, pv, V, pt, T, kind | (0 if sync else ASYNC), _stream(stream)))
         self.T, self.V = T, V
         return self
 
@@ -203,6 +206,11 @@ class Scene:
         o = BuildOpts(morton_bits or self.morton_bits, leaf_size or self.leaf_size, int(mb),
                       int(width or self.width), (c_int32 * 4)())
         _check(lib().fgl_scene_build(self._h, ctypes.byref(o), _stream(stream)))
+        return self
+
+    def check(self, stream=None):
+        """Synchronise and raise FglError if the last upload failed validation."""
+        _check(lib().fgl_scene_check(self._h, _stream(stream)))
         return self
 
     def stats(self) -> dict:
