@@ -259,6 +259,34 @@ class Scene:
             res["node_counts"], res["tri_counts"] = nc, tc
         return res
 
+    def cast_to_host(self, poses, pattern, range_out: torch.Tensor, tri_id_out: torch.Tensor, chunks: int = 8,
+                     first_frame: int = 0, copy_stream=None, scratch=None):
+        """Cast and stream the results to (pinned) host tensors, overlapping the device-to-host copy
+        of chunk k with the cast of chunk k+1 (the copy runs on `copy_stream`). Returns when the
+        copies are enqueued; the caller synchronises. `scratch` (optional) = dict(range, tri_id)
+        device tensors of the full output shape, reused across calls."""
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        cs = copy_stream or torch.cuda.Stream(device=dev)
+        poses = _dev(poses, torch.float32, dev).reshape(-1, 3, 4)
+        P = int(poses.shape[0])
+        if scratch is None:
+            scratch = dict(range=torch.empty(range_out.shape, dtype=torch.float32, device=dev),
+                           tri_id=torch.empty(tri_id_out.shape, dtype=torch.int32, device=dev))
+        step = max(1, -(-P // max(1, chunks)))
+        for a in range(0, P, step):
+            b = min(P, a + step)
+            self.cast(poses[a:b], pattern, first_frame=first_frame + a,
+                      out=dict(range=scratch["range"][a:b], tri_id=scratch["tri_id"][a:b]))
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            cs.wait_event(ev)
+            with torch.cuda.stream(cs):
+                range_out[a:b].copy_(scratch["range"][a:b], non_blocking=True)
+                tri_id_out[a:b].copy_(scratch["tri_id"][a:b], non_blocking=True)
+        cur.wait_stream(cs)
+        return range_out, tri_id_out
+
     def cast_rays(self, orig, dir, t_min: float, t_max: float, bruteforce: bool = False, stream=None):
         o = _dev(orig, torch.float32, self.device, (-1, 3))
         d = _dev(dir, torch.float32, self.device, (-1, 3))

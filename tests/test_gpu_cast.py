@@ -290,3 +290,26 @@ def test_error_reporting(fgl):
     assert e.value.status == 1  # non-monotone elevations
     with pytest.raises(fgl.FglError):
         s.cast_rays(np.zeros((1, 3), np.float32), np.ones((1, 3), np.float32), 1.0, 0.5)
+
+
+def test_cast_to_host_pipelined_matches_cast(fgl):
+    cfg = _cfg("C2", poses=8)
+    s = _scene(fgl, cfg["mesh"])
+    ref = s.cast(cfg["poses"], cfg["pattern"])
+    rh = torch.empty(tuple(ref["range"].shape), dtype=torch.float32).pin_memory()
+    ih = torch.empty(tuple(ref["tri_id"].shape), dtype=torch.int32).pin_memory()
+    for chunks in (1, 3, 8):
+        rh.fill_(0)
+        ih.fill_(0)
+        s.cast_to_host(cfg["poses"], cfg["pattern"], rh, ih, chunks=chunks)
+        torch.cuda.synchronize()
+        assert torch.equal(rh, ref["range"].cpu()) and torch.equal(ih, ref["tri_id"].cpu())
+
+
+def test_async_upload_reports_bad_mesh_at_check(fgl):
+    s = fgl.Scene(build=False)
+    s.upload(np.zeros((3, 3), np.float32), np.array([[0, 1, 7]], np.int32), sync=False)
+    s.build()  # memory-safe (clamped indices) even though the mesh is invalid
+    with pytest.raises(fgl.FglError) as e:
+        s.check()
+    assert e.value.status == 2
