@@ -45,6 +45,8 @@ def _args():
     ap.add_argument("--morton-bits", type=int, default=0, help="b of Eq. 5 (0 = library default)")
     ap.add_argument("--morton-box", type=int, default=0, help="0 = cubic (R22, default), 1 = per-axis (Eq. 5)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
+    ap.add_argument("--no-gather", action="store_true", help="N > 1: skip the A12 all-gather (pure weak scaling)")
+    ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1: chunks overlapping cast and all-gather")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -263,10 +265,15 @@ def main():
     out = scene.cast(poses_d, pat)
     shape = tuple(out["range"].shape)
     gather = None
-    if world > 1:
-        g_rng = torch.empty((world,) + shape, dtype=torch.float32, device=dev)
-        g_tid = torch.empty((world,) + shape, dtype=torch.int32, device=dev)
-        gather = (g_rng, g_tid)
+    chunks = max(1, min(a.gather_chunks, P))
+    if world > 1 and not a.no_gather:
+        assert P % chunks == 0, "--poses must be a multiple of --gather-chunks"
+        Pc = P // chunks
+        # chunk-major gathered layout: g[c][r] = rank r's poses [c*Pc, (c+1)*Pc)
+        g_rng = torch.empty((chunks, world, Pc) + shape[1:], dtype=torch.float32, device=dev)
+        g_tid = torch.empty((chunks, world, Pc) + shape[1:], dtype=torch.int32, device=dev)
+        gather = (g_rng, g_tid, Pc)
+        comm = torch.cuda.Stream(device=dev)
     flush = None if a.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def step(cast_ev=None):
@@ -275,12 +282,24 @@ def main():
             scene.build()                        # A2-A7
         if cast_ev:
             cast_ev[0].record(stream)
-        scene.cast(poses_d, pat, out=out)        # A8-A11
+        if gather is None:
+            scene.cast(poses_d, pat, out=out)    # A8-A11
+        else:
+            # A8-A11 chunk by chunk; A12 all-gather of chunk c (NCCL, side stream) overlaps the cast of c+1
+            Pc = gather[2]
+            works = []
+            for c in range(chunks):
+                sl = slice(c * Pc, (c + 1) * Pc)
+                scene.cast(poses_d[sl], pat, out=dict(range=out["range"][sl], tri_id=out["tri_id"][sl]))
+                comm.wait_stream(stream)
+                with torch.cuda.stream(comm):
+                    works.append(dist.all_gather_into_tensor(gather[0][c], out["range"][sl], async_op=True))
+                    works.append(dist.all_gather_into_tensor(gather[1][c], out["tri_id"][sl], async_op=True))
+            for w in works:
+                w.wait()
+            stream.wait_stream(comm)
         if cast_ev:
             cast_ev[1].record(stream)
-        if gather is not None:                   # A12
-            dist.all_gather_into_tensor(gather[0], out["range"])
-            dist.all_gather_into_tensor(gather[1], out["tri_id"])
 
     for _ in range(a.warmup):
         step()
@@ -416,7 +435,7 @@ def main():
             "value": total_rays / (ms / 1000), "unit": "rays/s", "n_gpus": world, "steps": K, "warmup": a.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": _describe(cfg, P, world), "step": "upload+build+cast" + ("+allgather" if world > 1 else "")
+            "config": {"workload": _describe(cfg, P, world), "step": "upload+build+cast" + ("+allgather" if gather is not None else "")
                        if a.mode == "full" else "cast only (prebuilt scene)",
                        "triangles": m.T, "rays_per_step": total_rays, "poses_per_step": P * world,
                        "l2": "flushed between steps (256 MiB memset, untimed)" if flush is not None else "not flushed",
