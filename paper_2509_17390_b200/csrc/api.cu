@@ -289,7 +289,7 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     FGL_API_BEGIN
     if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
     if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
-    int bits = 16, leaf = 2, cubic = 1, width = 2;
+    int bits = 13, leaf = 2, cubic = 1, width = 2;
     if (opts) {
         if (opts->width) width = opts->width;
         if (width != 2 && width != 4) throw Error(FGL_E_USAGE, "width must be 2 or 4");

@@ -109,7 +109,7 @@ def _check_nodes4(g, o, m, T, leaf_size):
 
 @pytest.mark.parametrize("name", ["tiny1", "tiny2", "dups", "c1", "soup"])
 @pytest.mark.parametrize("leaf_size,cubic,width,bits", [(1, 0, 2, 21), (4, 0, 2, 16), (8, 0, 2, 10), (4, 1, 2, 21),
-                                                        (2, 1, 2, 16), (2, 1, 4, 16), (1, 1, 4, 21), (5, 0, 4, 7)])
+                                                        (2, 1, 2, 13), (2, 1, 4, 16), (1, 1, 4, 21), (5, 0, 4, 7)])
 def test_build_matches_oracle(fgl, name, leaf_size, cubic, width, bits):
     m = _meshes()[name]
     s = fgl.Scene(m.verts, m.tris, leaf_size=leaf_size, morton_box=0 if cubic else 1, width=width, morton_bits=bits)
@@ -159,7 +159,7 @@ def test_build_rooms_full_size(fgl):
     m = synth.scene_rooms(2)
     s = fgl.Scene(m.verts, m.tris)
     g = s.export()
-    o = oracle.lbvh(m.verts, m.tris, bits=16, cubic=True)  # library defaults: b = 16, cubic box (R7, R22)
+    o = oracle.lbvh(m.verts, m.tris, bits=13, cubic=True)  # library defaults: b = 13, cubic box (R7, R22)
     for k_g, k_o in (("codes", "code"), ("sorted_keys", "sorted_keys"), ("perm", "perm"), ("child", "child"),
                      ("range", "range"), ("leaf_box", "leaf_box"), ("node_box", "node_box")):
         assert np.array_equal(g[k_g], o[k_o]), k_g
