@@ -53,7 +53,12 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
     const float dx = fabsf(r.dx) < tiny ? copysignf(tiny, r.dx) : r.dx;
     const float dy = fabsf(r.dy) < tiny ? copysignf(tiny, r.dy) : r.dy;
     const float dz = fabsf(r.dz) < tiny ? copysignf(tiny, r.dz) : r.dz;
+#if FGL_APPROX_PRE
+    // MUFU reciprocals (<= 2 ulp): covered by the slab slack, consistent per ray
+    p.Ix = __fdividef(1.f, dx), p.Iy = __fdividef(1.f, dy), p.Iz = __fdividef(1.f, dz);
+#else
     p.Ix = __frcp_rn(dx), p.Iy = __frcp_rn(dy), p.Iz = __frcp_rn(dz);
+#endif
     const float cx = -r.ox * p.Ix, cy = -r.oy * p.Iy, cz = -r.oz * p.Iz;
     const float ax = fabsf(cx) * 0x1p-22f, ay = fabsf(cy) * 0x1p-22f, az = fabsf(cz) * 0x1p-22f;
     // lo plane is the near plane when I >= 0: push it towards smaller t; the hi plane the other way
@@ -72,7 +77,11 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
     }
     const float dkx = kx == 0 ? r.dx : (kx == 1 ? r.dy : r.dz);
     const float dky = ky == 0 ? r.dx : (ky == 1 ? r.dy : r.dz);
+#if FGL_APPROX_PRE
+    const float Sz = __fdividef(1.f, dkz), Sx = dkx * Sz, Sy = dky * Sz;
+#else
     const float Sx = __fdiv_rn(dkx, dkz), Sy = __fdiv_rn(dky, dkz), Sz = __frcp_rn(dkz);
+#endif
     p.m0x = kx == 0 ? 1.f : (kz == 0 ? -Sx : 0.f);
     p.m0y = kx == 1 ? 1.f : (kz == 1 ? -Sx : 0.f);
     p.m0z = kx == 2 ? 1.f : (kz == 2 ? -Sx : 0.f);
@@ -479,6 +488,12 @@ struct RaysGen {
     }
 };
 
+#ifndef FGL_APPROX_PRE
+#define FGL_APPROX_PRE 0
+#endif
+#ifndef FGL_BRANCHFREE_PUSH
+#define FGL_BRANCHFREE_PUSH 0
+#endif
 #ifndef FGL_CAST_MINBLOCKS
 #define FGL_CAST_MINBLOCKS 8
 #endif
@@ -608,6 +623,15 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
             const float t0 = slab(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim);
             const float t1 = slab(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim);
             const bool h0 = t0 != INFINITY, h1 = t1 != INFINITY;
+#if FGL_BRANCHFREE_PUSH
+            {
+                const bool swap = t1 < t0;  // (only meaningful when both are hit)
+                st[sp] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
+                sp += (h0 && h1) ? 1 : 0;
+                const int32_t nr = (h0 && (!h1 || !swap)) ? nd.x : nd.y;
+                cur = (h0 || h1) ? nr : pop();
+            }
+#else
             if (h0 && h1) {
                 const bool swap = t1 < t0;
                 st[sp++] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
@@ -619,6 +643,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
             } else {
                 cur = pop();
             }
+#endif
             if (cur < 0 && leaf == 0) {
                 leaf = cur;
                 cur = pop();

@@ -15,7 +15,10 @@
 namespace fgl {
 
 namespace {
-constexpr int kThreads = 256;
+#ifndef FGL_SORT_THREADS
+#define FGL_SORT_THREADS 256
+#endif
+constexpr int kThreads = FGL_SORT_THREADS;      // >= 256: one look-back thread per digit
 constexpr int kWarps = kThreads / 32;
 #ifndef FGL_SORT_ITEMS
 #define FGL_SORT_ITEMS 16
@@ -55,7 +58,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
     for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&wh[0][0])[i] = 0;
     // global base of each digit: exclusive scan of this pass's histogram
     {
-        const uint32_t v = hist[threadIdx.x];
+        const uint32_t v = threadIdx.x < 256 ? hist[threadIdx.x] : 0u;
         uint32_t x = v;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -65,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
         __syncthreads();
         uint32_t off = 0;
         for (int ww = 0; ww < w; ++ww) off += s_wsum[ww];
-        s_base[threadIdx.x] = off + x - v;
+        if (threadIdx.x < 256) s_base[threadIdx.x] = off + x - v;
     }
     __syncthreads();
     const uint32_t tile = s_tile;
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
     }
     __syncthreads();
     // per digit (one thread each): tile count, exclusive prefix over warps, decoupled look-back
-    {
+    if (threadIdx.x < 256) {
         const int d = threadIdx.x;
         uint32_t cnt = 0;
 #pragma unroll
@@ -107,14 +110,30 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
             mine.store(ep | kPrefix | cnt, cuda::std::memory_order_relaxed);
         } else {
             mine.store(ep | kAgg | cnt, cuda::std::memory_order_relaxed);
+            // look back kWin predecessors per round (independent loads in flight), accumulating
+            // published tile counts until the nearest published inclusive prefix
+            constexpr int kWin = 8;
             int64_t t = (int64_t)tile - 1;
-            while (t >= 0) {
-                cuda::atomic_ref<uint64_t, cuda::thread_scope_device> prev(status[t * 256 + d]);
-                const uint64_t v = prev.load(cuda::std::memory_order_relaxed);
-                if ((v >> 32) != epoch || (v & (kAgg | kPrefix)) == 0) continue;  // not published yet
-                excl += (uint32_t)(v & kValMask);
-                if (v & kPrefix) break;
-                --t;
+            bool done = false;
+            while (!done) {
+                uint64_t v[kWin];
+#pragma unroll
+                for (int k = 0; k < kWin; ++k) {
+                    v[k] = 0;
+                    if (t - k >= 0) {
+                        cuda::atomic_ref<uint64_t, cuda::thread_scope_device> prev(status[(t - k) * 256 + d]);
+                        v[k] = prev.load(cuda::std::memory_order_relaxed);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kWin; ++k) {
+                    if (done || t < 0) break;
+                    if ((v[k] >> 32) != epoch || (v[k] & (kAgg | kPrefix)) == 0) break;  // not yet: re-poll from t
+                    excl += (uint32_t)(v[k] & kValMask);
+                    if (v[k] & kPrefix) done = true;
+                    --t;
+                }
+                if (t < 0) done = true;
             }
             mine.store(ep | kPrefix | (excl + cnt), cuda::std::memory_order_relaxed);
         }

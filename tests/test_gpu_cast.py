@@ -313,3 +313,39 @@ def test_async_upload_reports_bad_mesh_at_check(fgl):
     with pytest.raises(fgl.FglError) as e:
         s.check()
     assert e.value.status == 2
+
+
+@pytest.mark.parametrize("channels,columns", [(13, 101), (1, 7), (3, 33), (64, 2048)])
+def test_spinning_ragged_tiles(fgl, channels, columns):
+    """Tiles are 4 channels x 8 columns (2x16 / 1x32 for fewer channels): ragged edges in both
+    directions must produce every ray exactly once, in the documented output order."""
+    m = synth.scene_c1()
+    pat = synth.Spinning(np.linspace(-20, 10, channels).astype(np.float32), columns, az0_deg=0.7)
+    poses = np.stack([synth.pose((0.3, -0.2, 0.1), yaw=0.2), synth.pose((-1.0, 2.0, -0.5), yaw=-1.0, pitch=0.1)])
+    s = _scene(fgl, m)
+    res = s.cast(poses, pat)
+    assert tuple(res["range"].shape) == (2, channels, columns)
+    rng = res["range"].reshape(-1).cpu().numpy()
+    tid = res["tri_id"].reshape(-1).cpu().numpy()
+    idx = _sample(rng.size, 3000, 9)
+    o, d = fgl.export_rays(pat, poses)
+    o = o.cpu().numpy().astype(np.float64)[idx]
+    d = d.cpu().numpy().astype(np.float64)[idx]
+    v = oracle.cast_and_classify(m.verts, m.tris, o, d, pat.t_min, pat.t_max)
+    _assert_parity(v, rng[idx], tid[idx], label=f"ragged {channels}x{columns}")
+    assert np.all(tid >= 0)  # inside the closed icosphere
+
+
+@pytest.mark.parametrize("n", [1, 31, 1007])
+def test_rosette_ragged_frames(fgl, n):
+    m = synth.scene_c1()
+    ros = synth.Rosette(points_per_frame=n)
+    poses = synth.random_poses(3, 8, (-2, -2, -2), (2, 2, 2))
+    s = _scene(fgl, m)
+    res = s.cast(poses, ros, first_frame=41)
+    assert tuple(res["range"].shape) == (3, n)
+    o, d = fgl.export_rays(ros, poses, first_frame=41)
+    v = oracle.cast_and_classify(m.verts, m.tris, o.cpu().numpy().astype(np.float64),
+                                 d.cpu().numpy().astype(np.float64), ros.t_min, ros.t_max)
+    _assert_parity(v, res["range"].reshape(-1).cpu().numpy(), res["tri_id"].reshape(-1).cpu().numpy(),
+                   label=f"rosette n={n}")
