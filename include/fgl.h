@@ -148,6 +148,28 @@ FGL_API fgl_status fgl_export_rays_spinning(const fgl_spinning *pattern, const f
 FGL_API fgl_status fgl_export_rays_rosette(const fgl_rosette *pattern, const float *poses, int64_t P, int64_t first_frame,
                                    float *orig, float *dir, void *cuda_stream);
 
+/* ---- fused cast + all-gather over peer memory (A12) ------------------------
+ * Device memory owned by the library (allocation bases, so they can be shared by CUDA IPC). */
+FGL_API fgl_status fgl_alloc(int cuda_device, int64_t bytes, void **dev_ptr);
+FGL_API fgl_status fgl_free(void *dev_ptr);
+typedef struct {
+    unsigned char bytes[64];
+} fgl_ipc_handle;
+/* Export an fgl_alloc'ed pointer to another process of the node / open a peer's export in this
+ * process (cudaIpcGetMemHandle / cudaIpcOpenMemHandle with peer access). */
+FGL_API fgl_status fgl_ipc_get_handle(void *dev_ptr, fgl_ipc_handle *out);
+FGL_API fgl_status fgl_ipc_open_handle(int cuda_device, const fgl_ipc_handle *handle, void **dev_ptr);
+FGL_API fgl_status fgl_ipc_close_handle(void *dev_ptr);
+
+/* fgl_cast_spinning whose results are written, from inside the cast kernel, into npeer global
+ * output buffers at ray index first_pose*channels*columns + (local index): rank r of W casts its
+ * pose block and writes straight into every rank's [P_total][C][A] range / tri_id buffers (its own
+ * and the peers' opened with fgl_ipc_open_handle), so the all-gather overlaps the cast tile by
+ * tile over NVLink. 1 <= npeer <= 8. The caller synchronises the ranks before reading. */
+FGL_API fgl_status fgl_cast_spinning_gather(const fgl_scene *scene, const fgl_spinning *pattern, const float *poses,
+                                            int64_t P, int64_t first_pose, float *const *range_bufs,
+                                            int32_t *const *tri_bufs, int32_t npeer, void *cuda_stream);
+
 /* ---- LBVH internals, for parity tests (host destination pointers; each may be NULL) ----- */
 typedef struct {
     float *scene_box;      /* [6]  lo.xyz, hi.xyz                                              */

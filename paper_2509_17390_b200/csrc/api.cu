@@ -178,7 +178,10 @@ fgl::RosetteParams rosette_params(const fgl_rosette *p, int64_t first_frame) {
 
 fgl::CastOut cast_out(float *range, int32_t *tri_id, float *hit, int32_t *nc, int32_t *tc) {
     if (!range || !tri_id) throw Error(FGL_E_USAGE, "range / tri_id output is NULL");
-    return fgl::CastOut{range, tri_id, hit, nc, tc};
+    fgl::CastOut o;
+    memset(&o, 0, sizeof(o));
+    o.range = range, o.tri_id = tri_id, o.hit_xyz = hit, o.node_counts = nc, o.tri_counts = tc;
+    return o;
 }
 
 }  // namespace
@@ -392,6 +395,75 @@ fgl_status fgl_cast_rays_bruteforce(const fgl_scene *s, const float *orig, const
     DeviceGuard g(s->dev);
     fgl::launch_cast_bruteforce(s->verts, s->V, s->tris, s->T, orig, dir, R, t_min, t_max, range, tri_id,
                                 (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_cast_spinning_gather(const fgl_scene *s, const fgl_spinning *pattern, const float *poses, int64_t P,
+                                    int64_t first_pose, float *const *range_bufs, int32_t *const *tri_bufs,
+                                    int32_t npeer, void *stream) {
+    FGL_API_BEGIN
+    check_built(s);
+    fgl::SpinParams sp = spin_params(pattern);
+    if (P < 0 || first_pose < 0) throw Error(FGL_E_USAGE, "P and first_pose must be >= 0");
+    if (npeer < 1 || npeer > fgl::kMaxPeers) throw Error(FGL_E_USAGE, "npeer must be in [1, 8]");
+    if (!range_bufs || !tri_bufs) throw Error(FGL_E_USAGE, "range_bufs / tri_bufs is NULL");
+    if (P == 0) return FGL_OK;
+    if (!poses) throw Error(FGL_E_USAGE, "poses is NULL");
+    fgl::CastOut o;
+    memset(&o, 0, sizeof(o));
+    const int64_t per = (int64_t)sp.channels * sp.columns;
+    // the local copy is peer 0's buffer (this process's own global output)
+    o.range = range_bufs[0] + first_pose * per;
+    o.tri_id = tri_bufs[0] + first_pose * per;
+    o.npeer = npeer - 1;
+    o.out_offset = first_pose * per;
+    for (int w = 1; w < npeer; ++w) {
+        if (!range_bufs[w] || !tri_bufs[w]) throw Error(FGL_E_USAGE, "NULL peer buffer");
+        o.peer_range[w - 1] = range_bufs[w];
+        o.peer_tri[w - 1] = tri_bufs[w];
+    }
+    DeviceGuard g(s->dev);
+    fgl::launch_cast_spinning(view(s), sp, poses, P, o, next_counter(s), (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_alloc(int dev, int64_t bytes, void **p) {
+    FGL_API_BEGIN
+    if (!p || bytes <= 0) throw Error(FGL_E_USAGE, "bad fgl_alloc arguments");
+    DeviceGuard g(dev);
+    FGL_CUDA(cudaMalloc(p, (size_t)bytes));
+    FGL_API_END
+}
+
+fgl_status fgl_free(void *p) {
+    FGL_API_BEGIN
+    if (p) FGL_CUDA(cudaFree(p));
+    FGL_API_END
+}
+
+fgl_status fgl_ipc_get_handle(void *p, fgl_ipc_handle *out) {
+    FGL_API_BEGIN
+    if (!p || !out) throw Error(FGL_E_USAGE, "NULL argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(fgl_ipc_handle), "IPC handle size");
+    cudaIpcMemHandle_t h;
+    FGL_CUDA(cudaIpcGetMemHandle(&h, p));
+    memcpy(out->bytes, &h, sizeof(h));
+    FGL_API_END
+}
+
+fgl_status fgl_ipc_open_handle(int dev, const fgl_ipc_handle *handle, void **p) {
+    FGL_API_BEGIN
+    if (!handle || !p) throw Error(FGL_E_USAGE, "NULL argument");
+    DeviceGuard g(dev);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle->bytes, sizeof(h));
+    FGL_CUDA(cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess));
+    FGL_API_END
+}
+
+fgl_status fgl_ipc_close_handle(void *p) {
+    FGL_API_BEGIN
+    if (p) FGL_CUDA(cudaIpcCloseMemHandle(p));
     FGL_API_END
 }
 

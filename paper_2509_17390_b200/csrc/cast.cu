@@ -396,6 +396,11 @@ __device__ __forceinline__ void write_out(const CastOut &o, int64_t idx, const R
     }
     if (o.node_counts) o.node_counts[idx] = h.nodes;
     if (o.tri_counts) o.tri_counts[idx] = h.tris;
+    // fused all-gather: the same result into every peer's global output (P2P stores over NVLink)
+    for (int w = 0; w < o.npeer; ++w) {
+        o.peer_range[w][o.out_offset + idx] = miss ? INFINITY : h.t;
+        o.peer_tri[w][o.out_offset + idx] = miss ? -1 : h.id;
+    }
 }
 
 // ---- ray generators ---------------------------------------------------------------------------

@@ -125,11 +125,18 @@ struct RosetteParams {
     float half_fov_deg, t_min, t_max;
     int64_t first_frame;
 };
+constexpr int kMaxPeers = 8;
 struct CastOut {
     float *range;
     int32_t *tri_id;
     float *hit_xyz;
     int32_t *node_counts, *tri_counts;
+    // fused cast + all-gather (A12): when npeer > 0, each result is also written at
+    // out_offset + idx into every peer buffer (this process's and peers' over NVLink)
+    int npeer;
+    int64_t out_offset;
+    float *peer_range[kMaxPeers];
+    int32_t *peer_tri[kMaxPeers];
 };
 struct SceneView {
     const float4 *tri;

@@ -37,6 +37,71 @@ def chunk_bounds(S: int, chunks: int) -> list[tuple[int, int]]:
     return [(a, min(S, a + step)) for a in range(0, S, step)]
 
 
+class PeerGather:
+    """Fused cast + all-gather over peer memory (A12, the B200-native alternative to `sweep`'s
+    NCCL pass): every rank owns global [P][...] output buffers allocated by libfgl, the ranks
+    exchange CUDA IPC handles (over `cpu_group`, e.g. gloo), and the cast kernel stores each ray's
+    result into all ranks' buffers (P2P stores over NVLink/NVSwitch) while it traces — no separate
+    collective. Call `cast(...)` with this rank's pose block, then `sync()` before reading."""
+
+    def __init__(self, P: int, pattern, device, cpu_group=None):
+        from . import fgl as _f
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.group = cpu_group
+        self.P = P
+        self.pattern = pattern
+        self.shape = (P, len(pattern.elev_deg), int(pattern.columns))
+        self.device = torch.device(device)
+        self._own = [_f.DeviceBuffer(self.shape, torch.float32, device), _f.DeviceBuffer(self.shape, torch.int32, device)]
+        handles = (self._own[0].ipc_handle(), self._own[1].ipc_handle())
+        allh = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(allh, handles, group=cpu_group)
+        else:
+            allh = [handles]
+        self._peers = []
+        for r, (hr, ht) in enumerate(allh):
+            if r == self.rank:
+                continue
+            self._peers.append((_f.DeviceBuffer.open_ipc(hr, self.shape, torch.float32, device),
+                                _f.DeviceBuffer.open_ipc(ht, self.shape, torch.int32, device)))
+        self.range_ptrs = [self._own[0].ptr] + [p[0].ptr for p in self._peers]
+        self.tri_ptrs = [self._own[1].ptr] + [p[1].ptr for p in self._peers]
+
+    @property
+    def range(self) -> torch.Tensor:
+        return self._own[0].tensor
+
+    @property
+    def tri_id(self) -> torch.Tensor:
+        return self._own[1].tensor
+
+    def shard(self):
+        return shard_range(self.P, self.world, self.rank)
+
+    def cast(self, scene, poses_all: torch.Tensor, stream=None):
+        """Cast this rank's contiguous pose block of `poses_all` ([P][3][4]) into every rank's output."""
+        from . import fgl as _f
+        lo, hi = self.shard()
+        if hi > lo:
+            _f.cast_spinning_gather(scene, poses_all[lo:hi], self.pattern, lo, self.range_ptrs, self.tri_ptrs, stream)
+
+    def sync(self):
+        """Make every rank's writes visible: device sync + barrier over the handle-exchange group."""
+        torch.cuda.synchronize(self.device)
+        if self.world > 1:
+            dist.barrier(group=self.group)
+
+    def close(self):
+        for a, b in self._peers:
+            a.close()
+            b.close()
+        self._peers = []
+        for b in self._own:
+            b.close()
+
+
 def sweep(scene, poses: torch.Tensor, pattern, group=None, chunks: int = 4, gather: bool = True,
           cast_fn=None, first_frame: int = 0):
     """Cast `pattern` from all P poses across the ranks of `group`.

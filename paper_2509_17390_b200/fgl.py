@@ -75,6 +75,13 @@ _SIGS = {
     "fgl_scene_export": (c_int, [c_void_p, POINTER(ExportC), c_void_p]),
     "fgl_morton_codes": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     "fgl_sort_pairs": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
+    "fgl_cast_spinning_gather": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_int64, c_void_p, c_void_p,
+                                         c_int32, c_void_p]),
+    "fgl_alloc": (c_int, [c_int, c_int64, POINTER(c_void_p)]),
+    "fgl_free": (c_int, [c_void_p]),
+    "fgl_ipc_get_handle": (c_int, [c_void_p, c_void_p]),
+    "fgl_ipc_open_handle": (c_int, [c_int, c_void_p, POINTER(c_void_p)]),
+    "fgl_ipc_close_handle": (c_int, [c_void_p]),
     "fgl_last_error": (c_char_p, []),
     "fgl_version": (c_char_p, []),
     "fgl_abi_version": (c_int32, []),
@@ -347,6 +354,65 @@ def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, key_bits: int = 64, strea
     assert keys.is_contiguous() and vals.is_contiguous() and keys.numel() == vals.numel()
     _check(lib().fgl_sort_pairs(keys.data_ptr(), vals.data_ptr(), int(keys.numel()), int(key_bits), _stream(stream)))
     return keys, vals
+
+
+class DeviceBuffer:
+    """Device memory from fgl_alloc (an allocation base, shareable by CUDA IPC) viewed as a torch
+    tensor through __cuda_array_interface__. `ptr` may instead be a peer's buffer opened by IPC."""
+
+    _TYPESTR = {torch.float32: "<f4", torch.int32: "<i4"}
+
+    def __init__(self, shape, dtype, device, ptr: int | None = None, ipc: bool = False):
+        self.shape, self.dtype, self.device = tuple(int(x) for x in shape), dtype, torch.device(device)
+        self.nbytes = int(np.prod(self.shape)) * torch.tensor([], dtype=dtype).element_size()
+        self._own = ptr is None
+        self._ipc = ipc
+        if ptr is None:
+            p = c_void_p()
+            _check(lib().fgl_alloc(self.device.index or 0, max(self.nbytes, 1), ctypes.byref(p)))
+            ptr = p.value
+        self.ptr = int(ptr)
+        self.__cuda_array_interface__ = {"shape": self.shape, "typestr": self._TYPESTR[dtype],
+                                         "data": (self.ptr, False), "version": 2}
+        self.tensor = torch.as_tensor(self, device=self.device)
+
+    def ipc_handle(self) -> bytes:
+        h = (ctypes.c_ubyte * 64)()
+        _check(lib().fgl_ipc_get_handle(self.ptr, ctypes.byref(h)))
+        return bytes(h)
+
+    @classmethod
+    def open_ipc(cls, handle: bytes, shape, dtype, device):
+        h = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+        p = c_void_p()
+        _check(lib().fgl_ipc_open_handle(torch.device(device).index or 0, ctypes.byref(h), ctypes.byref(p)))
+        return cls(shape, dtype, device, ptr=p.value, ipc=True)
+
+    def close(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            try:
+                if self._ipc:
+                    _lib.fgl_ipc_close_handle(self.ptr)
+                elif self._own:
+                    _lib.fgl_free(self.ptr)
+            except Exception:
+                pass
+        self.ptr = None
+
+    __del__ = close
+
+
+def cast_spinning_gather(scene: "Scene", poses, pattern, first_pose: int, range_ptrs, tri_ptrs, stream=None):
+    """Fused cast + all-gather: this rank's poses are cast and each result is stored into every
+    buffer of range_ptrs / tri_ptrs (device pointers; index 0 = this rank's own output) at global
+    pose index first_pose + p."""
+    poses = _dev(poses, torch.float32, scene.device).reshape(-1, 3, 4)
+    s = spinning_struct(pattern)
+    W = len(range_ptrs)
+    rp = (c_void_p * W)(*range_ptrs)
+    tp = (c_void_p * W)(*tri_ptrs)
+    _check(lib().fgl_cast_spinning_gather(scene._h, ctypes.byref(s), poses.data_ptr(), int(poses.shape[0]),
+                                          int(first_pose), rp, tp, W, _stream(stream)))
 
 
 def kernel_launches() -> int:

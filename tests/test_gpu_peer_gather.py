@@ -1,0 +1,87 @@
+"""Fused cast + all-gather over peer memory (A12): two processes share the box's one GPU, exchange
+CUDA IPC handles over gloo, and each casts its pose block straight into both processes' global
+output buffers from inside the cast kernel. Each process's buffer must equal a local cast of all
+poses bit for bit. (Across GPUs the same stores travel over NVLink; this run has one GPU.)"""
+import os
+import socket
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_17390_b200 as fgl
+    from paper_2509_17390_b200 import dist as fdist
+    import synth
+
+    ok = False
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        m = synth.scene_c1()
+        pat = synth.spinning_preset("VLP16", 120)
+        P = 5
+        poses = torch.from_numpy(synth.random_poses(P, 3, (-2, -2, -2), (2, 2, 2))).cuda()
+        scene = fgl.Scene(m.verts, m.tris, device="cuda:0")
+        pg = fdist.PeerGather(P, pat, "cuda:0")
+        pg.range.fill_(float("nan"))
+        pg.tri_id.fill_(-7)
+        pg.sync()
+        pg.cast(scene, poses)
+        pg.sync()
+        ref = scene.cast(poses, pat)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(pg.range, ref["range"]) and torch.equal(pg.tri_id, ref["tri_id"]))
+        pg.sync()
+        pg.close()
+        dist.destroy_process_group()
+    except Exception as e:  # report, do not hang the parent
+        print("worker", rank, "failed:", repr(e))
+    q.put((rank, ok))
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_fused_cast_allgather_two_processes_one_gpu():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+    got = dict(q.get(timeout=10) for _ in procs)
+    assert got == {0: True, 1: True}
+
+
+def test_fused_cast_single_rank_equals_cast():
+    import torch
+
+    import paper_2509_17390_b200 as fgl
+    from paper_2509_17390_b200 import dist as fdist
+    import synth
+
+    m = synth.scene_c1()
+    pat = synth.spinning_preset("VLP16", 360)
+    poses = torch.from_numpy(synth.random_poses(4, 5, (-2, -2, -2), (2, 2, 2))).cuda()
+    scene = fgl.Scene(m.verts, m.tris)
+    pg = fdist.PeerGather(4, pat, "cuda:0")
+    pg.cast(scene, poses)
+    pg.sync()
+    ref = scene.cast(poses, pat)
+    assert torch.equal(pg.range, ref["range"]) and torch.equal(pg.tri_id, ref["tri_id"])
+    pg.close()
