@@ -169,6 +169,15 @@ FGL_API fgl_status fgl_ipc_close_handle(void *dev_ptr);
 FGL_API fgl_status fgl_cast_spinning_gather(const fgl_scene *scene, const fgl_spinning *pattern, const float *poses,
                                             int64_t P, int64_t first_pose, float *const *range_bufs,
                                             int32_t *const *tri_bufs, int32_t npeer, void *cuda_stream);
+/* Device-side completion barrier for the fused gather: `flags` (NULL or [npeer] int32 counters in
+ * fgl_alloc'ed memory, index 0 = this rank's own, the others opened by IPC) are each incremented
+ * by the cast kernel's last warp after a system-scope fence (pass them to
+ * fgl_cast_spinning_gather_signal); fgl_wait_flag makes `cuda_stream` wait until *flag >= target. */
+FGL_API fgl_status fgl_cast_spinning_gather_signal(const fgl_scene *scene, const fgl_spinning *pattern,
+                                                   const float *poses, int64_t P, int64_t first_pose,
+                                                   float *const *range_bufs, int32_t *const *tri_bufs,
+                                                   int32_t *const *flags, int32_t npeer, void *cuda_stream);
+FGL_API fgl_status fgl_wait_flag(const int32_t *flag, int32_t target, void *cuda_stream);
 
 /* ---- LBVH internals, for parity tests (host destination pointers; each may be NULL) ----- */
 typedef struct {

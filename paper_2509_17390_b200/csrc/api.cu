@@ -398,17 +398,17 @@ fgl_status fgl_cast_rays_bruteforce(const fgl_scene *s, const float *orig, const
     FGL_API_END
 }
 
-fgl_status fgl_cast_spinning_gather(const fgl_scene *s, const fgl_spinning *pattern, const float *poses, int64_t P,
-                                    int64_t first_pose, float *const *range_bufs, int32_t *const *tri_bufs,
-                                    int32_t npeer, void *stream) {
+fgl_status fgl_cast_spinning_gather_signal(const fgl_scene *s, const fgl_spinning *pattern, const float *poses,
+                                           int64_t P, int64_t first_pose, float *const *range_bufs,
+                                           int32_t *const *tri_bufs, int32_t *const *flags, int32_t npeer,
+                                           void *stream) {
     FGL_API_BEGIN
     check_built(s);
     fgl::SpinParams sp = spin_params(pattern);
     if (P < 0 || first_pose < 0) throw Error(FGL_E_USAGE, "P and first_pose must be >= 0");
     if (npeer < 1 || npeer > fgl::kMaxPeers) throw Error(FGL_E_USAGE, "npeer must be in [1, 8]");
     if (!range_bufs || !tri_bufs) throw Error(FGL_E_USAGE, "range_bufs / tri_bufs is NULL");
-    if (P == 0) return FGL_OK;
-    if (!poses) throw Error(FGL_E_USAGE, "poses is NULL");
+    if (P > 0 && !poses) throw Error(FGL_E_USAGE, "poses is NULL");
     fgl::CastOut o;
     memset(&o, 0, sizeof(o));
     const int64_t per = (int64_t)sp.channels * sp.columns;
@@ -422,8 +422,33 @@ fgl_status fgl_cast_spinning_gather(const fgl_scene *s, const fgl_spinning *patt
         o.peer_range[w - 1] = range_bufs[w];
         o.peer_tri[w - 1] = tri_bufs[w];
     }
+    if (flags) {
+        o.nsignal = npeer;
+        for (int w = 0; w < npeer; ++w) {
+            if (!flags[w]) throw Error(FGL_E_USAGE, "NULL flag pointer");
+            o.signal[w] = flags[w];
+        }
+    }
     DeviceGuard g(s->dev);
+    if (P == 0) {
+        // nothing to cast: still signal every rank (a 1-tile launch whose only work is the epilogue)
+        if (!flags) return FGL_OK;
+    }
     fgl::launch_cast_spinning(view(s), sp, poses, P, o, next_counter(s), (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_cast_spinning_gather(const fgl_scene *s, const fgl_spinning *pattern, const float *poses, int64_t P,
+                                    int64_t first_pose, float *const *range_bufs, int32_t *const *tri_bufs,
+                                    int32_t npeer, void *stream) {
+    return fgl_cast_spinning_gather_signal(s, pattern, poses, P, first_pose, range_bufs, tri_bufs, nullptr, npeer,
+                                           stream);
+}
+
+fgl_status fgl_wait_flag(const int32_t *flag, int32_t target, void *stream) {
+    FGL_API_BEGIN
+    if (!flag) throw Error(FGL_E_USAGE, "flag is NULL");
+    fgl::launch_wait_flag(flag, target, (cudaStream_t)stream);
     FGL_API_END
 }
 

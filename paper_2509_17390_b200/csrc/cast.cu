@@ -403,6 +403,25 @@ __device__ __forceinline__ void write_out(const CastOut &o, int64_t idx, const R
     }
 }
 
+// Kernel epilogue: the last warp to finish resets the work counter for the next launch using this
+// slot; with a fused all-gather it also signals every rank (own flag included) after a system-scope
+// fence by every warp, so a rank waiting for W signals knows all peers' stores into its buffer landed.
+__device__ __forceinline__ void cast_epilogue(const CastOut &out, CastCounter *ctr, int lane) {
+    if (lane == 0) {
+        if (out.nsignal) __threadfence_system();
+        const unsigned int total = gridDim.x * (blockDim.x >> 5);
+        if (atomicAdd(&ctr->done, 1u) == total - 1) {
+            ctr->next = 0ull;
+            ctr->done = 0u;
+            __threadfence();
+            if (out.nsignal) {
+                __threadfence_system();
+                for (int w = 0; w < out.nsignal; ++w) atomicAdd_system(out.signal[w], 1);
+            }
+        }
+    }
+}
+
 // ---- ray generators ---------------------------------------------------------------------------
 __device__ __forceinline__ void rotate_pose(const float *__restrict__ pose, float sx, float sy, float sz, Ray &r) {
     const float4 r0 = __ldg(reinterpret_cast<const float4 *>(pose));
@@ -532,14 +551,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
         }
     }
     // self-reset: the last warp to finish clears the counter for the next launch using this slot
-    if (lane == 0) {
-        const unsigned int total = gridDim.x * (blockDim.x >> 5);
-        if (atomicAdd(&ctr->done, 1u) == total - 1) {
-            ctr->next = 0ull;
-            ctr->done = 0u;
-            __threadfence();
-        }
-    }
+    cast_epilogue(out, ctr, lane);
 }
 
 // FGL_TRAVERSAL=packet selects the warp-packet traversal for pattern casts (A/B experiments;
@@ -680,14 +692,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
             active = false;
         }
     }
-    if (lane == 0) {
-        const unsigned int total = gridDim.x * (blockDim.x >> 5);
-        if (atomicAdd(&ctr->done, 1u) == total - 1) {
-            ctr->next = 0ull;
-            ctr->done = 0u;
-            __threadfence();
-        }
-    }
+    cast_epilogue(out, ctr, lane);
 }
 
 template <class Gen, bool kCount, int kMode>
@@ -728,7 +733,7 @@ void launch_mode(const SceneView &sv, const Gen &gen, int64_t ntiles, const Cast
 template <class Gen>
 void launch_persistent(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
                        cudaStream_t s) {
-    if (ntiles <= 0) return;
+    if (ntiles <= 0 && !o.nsignal) return;
     if (o.node_counts || o.tri_counts)
         launch_mode<Gen, true>(sv, gen, ntiles, o, ctr, s);
     else
@@ -847,6 +852,18 @@ void launch_cast_bruteforce(const float *verts, int64_t V, const int32_t *tris, 
     k_bruteforce<<<(unsigned)((R + kBfThreads - 1) / kBfThreads), kBfThreads, 0, s>>>(verts, V, tris, T, orig, dir,
                                                                                        R, t_min, t_max, range, tri_id);
     FGL_LAUNCHED("k_bruteforce");
+}
+
+__global__ void k_wait_flag(const int32_t *flag, int32_t target) {
+    if (threadIdx.x == 0) {
+        while (*(volatile const int32_t *)flag < target) __nanosleep(200);
+        __threadfence_system();
+    }
+}
+
+void launch_wait_flag(const int32_t *flag, int32_t target, cudaStream_t s) {
+    k_wait_flag<<<1, 32, 0, s>>>(flag, target);
+    FGL_LAUNCHED("k_wait_flag");
 }
 
 void launch_export_spinning(const SpinParams &p, const float *poses, int64_t P, float *orig, float *dir,

@@ -137,6 +137,9 @@ struct CastOut {
     int64_t out_offset;
     float *peer_range[kMaxPeers];
     int32_t *peer_tri[kMaxPeers];
+    // completion signal: the last warp adds 1 to each of these flags (every rank's, own included)
+    int nsignal;
+    int32_t *signal[kMaxPeers];
 };
 struct SceneView {
     const float4 *tri;
@@ -153,6 +156,7 @@ void launch_cast_rays(const SceneView &sv, const float *orig, const float *dir, 
 void launch_cast_bruteforce(const float *verts, int64_t V, const int32_t *tris, int64_t T, const float *orig,
                             const float *dir,
                             int64_t R, float t_min, float t_max, float *range, int32_t *tri_id, cudaStream_t s);
+void launch_wait_flag(const int32_t *flag, int32_t target, cudaStream_t s);
 void launch_export_spinning(const SpinParams &p, const float *poses, int64_t P, float *orig, float *dir,
                             cudaStream_t s);
 void launch_export_rosette(const RosetteParams &p, const float *poses, int64_t P, float *orig, float *dir,

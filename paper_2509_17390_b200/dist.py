@@ -53,21 +53,27 @@ class PeerGather:
         self.pattern = pattern
         self.shape = (P, len(pattern.elev_deg), int(pattern.columns))
         self.device = torch.device(device)
-        self._own = [_f.DeviceBuffer(self.shape, torch.float32, device), _f.DeviceBuffer(self.shape, torch.int32, device)]
-        handles = (self._own[0].ipc_handle(), self._own[1].ipc_handle())
+        self._own = [_f.DeviceBuffer(self.shape, torch.float32, device), _f.DeviceBuffer(self.shape, torch.int32, device),
+                     _f.DeviceBuffer((8,), torch.int32, device)]
+        self._own[2].tensor.zero_()
+        torch.cuda.synchronize(self.device)
+        self.steps = 0
+        handles = tuple(b.ipc_handle() for b in self._own)
         allh = [None] * self.world
         if self.world > 1:
             dist.all_gather_object(allh, handles, group=cpu_group)
         else:
             allh = [handles]
         self._peers = []
-        for r, (hr, ht) in enumerate(allh):
+        for r, (hr, ht, hf) in enumerate(allh):
             if r == self.rank:
                 continue
             self._peers.append((_f.DeviceBuffer.open_ipc(hr, self.shape, torch.float32, device),
-                                _f.DeviceBuffer.open_ipc(ht, self.shape, torch.int32, device)))
+                                _f.DeviceBuffer.open_ipc(ht, self.shape, torch.int32, device),
+                                _f.DeviceBuffer.open_ipc(hf, (8,), torch.int32, device)))
         self.range_ptrs = [self._own[0].ptr] + [p[0].ptr for p in self._peers]
         self.tri_ptrs = [self._own[1].ptr] + [p[1].ptr for p in self._peers]
+        self.flag_ptrs = [self._own[2].ptr] + [p[2].ptr for p in self._peers]
 
     @property
     def range(self) -> torch.Tensor:
@@ -81,22 +87,31 @@ class PeerGather:
         return shard_range(self.P, self.world, self.rank)
 
     def cast(self, scene, poses_all: torch.Tensor, stream=None):
-        """Cast this rank's contiguous pose block of `poses_all` ([P][3][4]) into every rank's output."""
+        """Cast this rank's contiguous pose block of `poses_all` ([P][3][4]) into every rank's output
+        and signal every rank's completion counter (device side)."""
         from . import fgl as _f
         lo, hi = self.shard()
-        if hi > lo:
-            _f.cast_spinning_gather(scene, poses_all[lo:hi], self.pattern, lo, self.range_ptrs, self.tri_ptrs, stream)
+        _f.cast_spinning_gather(scene, poses_all[lo:hi], self.pattern, lo, self.range_ptrs, self.tri_ptrs,
+                                self.flag_ptrs, stream)
+        self.steps += 1
+
+    def wait(self, stream=None):
+        """Device-side barrier: the stream waits until every rank's cast of this step has signalled
+        (all peer stores into this rank's buffers are then visible)."""
+        from . import fgl as _f
+        _f.wait_flag(self.flag_ptrs[0], self.steps * self.world, stream)
 
     def sync(self):
-        """Make every rank's writes visible: device sync + barrier over the handle-exchange group."""
+        """Host-side completion: device barrier (wait) + stream sync + host barrier."""
+        self.wait()
         torch.cuda.synchronize(self.device)
         if self.world > 1:
             dist.barrier(group=self.group)
 
     def close(self):
-        for a, b in self._peers:
-            a.close()
-            b.close()
+        for bufs in self._peers:
+            for b in bufs:
+                b.close()
         self._peers = []
         for b in self._own:
             b.close()

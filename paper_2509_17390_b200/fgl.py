@@ -77,6 +77,9 @@ _SIGS = {
     "fgl_sort_pairs": (c_int, [c_void_p, c_void_p, c_int64, c_int32, c_void_p]),
     "fgl_cast_spinning_gather": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_int64, c_void_p, c_void_p,
                                          c_int32, c_void_p]),
+    "fgl_cast_spinning_gather_signal": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_int64, c_void_p,
+                                                c_void_p, c_void_p, c_int32, c_void_p]),
+    "fgl_wait_flag": (c_int, [c_void_p, c_int32, c_void_p]),
     "fgl_alloc": (c_int, [c_int, c_int64, POINTER(c_void_p)]),
     "fgl_free": (c_int, [c_void_p]),
     "fgl_ipc_get_handle": (c_int, [c_void_p, c_void_p]),
@@ -402,17 +405,26 @@ class DeviceBuffer:
     __del__ = close
 
 
-def cast_spinning_gather(scene: "Scene", poses, pattern, first_pose: int, range_ptrs, tri_ptrs, stream=None):
+def cast_spinning_gather(scene: "Scene", poses, pattern, first_pose: int, range_ptrs, tri_ptrs, flag_ptrs=None,
+                         stream=None):
     """Fused cast + all-gather: this rank's poses are cast and each result is stored into every
     buffer of range_ptrs / tri_ptrs (device pointers; index 0 = this rank's own output) at global
-    pose index first_pose + p."""
+    pose index first_pose + p. flag_ptrs (optional, same order): completion counters every rank's
+    cast increments once, after a system-scope fence (see wait_flag)."""
     poses = _dev(poses, torch.float32, scene.device).reshape(-1, 3, 4)
     s = spinning_struct(pattern)
     W = len(range_ptrs)
     rp = (c_void_p * W)(*range_ptrs)
     tp = (c_void_p * W)(*tri_ptrs)
-    _check(lib().fgl_cast_spinning_gather(scene._h, ctypes.byref(s), poses.data_ptr(), int(poses.shape[0]),
-                                          int(first_pose), rp, tp, W, _stream(stream)))
+    fp = None if flag_ptrs is None else (c_void_p * W)(*flag_ptrs)
+    _check(lib().fgl_cast_spinning_gather_signal(scene._h, ctypes.byref(s), poses.data_ptr() if poses.numel() else None,
+                                                 int(poses.shape[0]), int(first_pose), rp, tp, fp, W,
+                                                 _stream(stream)))
+
+
+def wait_flag(flag_ptr: int, target: int, stream=None):
+    """Make the stream wait (on the device) until the int32 counter at flag_ptr reaches target."""
+    _check(lib().fgl_wait_flag(flag_ptr, int(target), _stream(stream)))
 
 
 def kernel_launches() -> int:
