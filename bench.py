@@ -45,8 +45,11 @@ def _args():
     ap.add_argument("--morton-bits", type=int, default=0, help="b of Eq. 5 (0 = library default)")
     ap.add_argument("--morton-box", type=int, default=0, help="0 = cubic (R22, default), 1 = per-axis (Eq. 5)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
-    ap.add_argument("--no-gather", action="store_true", help="N > 1: skip the A12 all-gather (pure weak scaling)")
-    ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1: chunks overlapping cast and all-gather")
+    ap.add_argument("--gather", choices=["fused", "nccl", "none"], default="fused",
+                    help="N > 1, A12: fused = the cast kernel stores every result into all ranks' buffers over "
+                         "NVLink (CUDA IPC) with a device-side completion barrier; nccl = chunked all_gather on a "
+                         "side stream; none = pure cast scaling")
+    ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1, --gather nccl: chunks")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -265,8 +268,17 @@ def main():
     out = scene.cast(poses_d, pat)
     shape = tuple(out["range"].shape)
     gather = None
+    peer = None
     chunks = max(1, min(a.gather_chunks, P))
-    if world > 1 and not a.no_gather:
+    gather_mode = a.gather
+    if world > 1 and gather_mode == "fused" and not hasattr(pat, "elev_deg"):
+        gather_mode = "nccl"  # the fused kernel path covers spinning patterns
+    if world > 1 and gather_mode == "fused":
+        from paper_2509_17390_b200 import dist as fdist
+        cpu_group = dist.new_group(backend="gloo")
+        peer = fdist.PeerGather(P * world, pat, dev, cpu_group=cpu_group)
+        poses_all_d = torch.from_numpy(np.ascontiguousarray(cfg["poses"])).to(dev)
+    if world > 1 and gather_mode == "nccl":
         assert P % chunks == 0, "--poses must be a multiple of --gather-chunks"
         Pc = P // chunks
         # chunk-major gathered layout: g[c][r] = rank r's poses [c*Pc, (c+1)*Pc)
@@ -282,7 +294,10 @@ def main():
             scene.build()                        # A2-A7
         if cast_ev:
             cast_ev[0].record(stream)
-        if gather is None:
+        if peer is not None:
+            peer.cast(scene, poses_all_d)        # A8-A12 fused: results stored into every rank's buffer
+            peer.wait()                          # device-side barrier: all ranks' stores have landed
+        elif gather is None:
             scene.cast(poses_d, pat, out=out)    # A8-A11
         else:
             # A8-A11 chunk by chunk; A12 all-gather of chunk c (NCCL, side stream) overlaps the cast of c+1
@@ -344,6 +359,8 @@ def main():
     launches = fgl.kernel_launches() - launches0
     scene.check()  # validation result of the (asynchronous) uploads
     step_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    if peer is not None:
+        peer.sync()
     if graph is not None:
         # graph replays launch the same kernels as the eager step: count them from one eager step,
         # and time the cast part with events on eager casts of the same inputs
@@ -435,7 +452,8 @@ def main():
             "value": total_rays / (ms / 1000), "unit": "rays/s", "n_gpus": world, "steps": K, "warmup": a.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": _describe(cfg, P, world), "step": "upload+build+cast" + ("+allgather" if gather is not None else "")
+            "config": {"workload": _describe(cfg, P, world), "step": "upload+build+cast" + ("+allgather(nccl)" if gather is not None else "")
+                       + ("+allgather(fused P2P)" if peer is not None else "")
                        if a.mode == "full" else "cast only (prebuilt scene)",
                        "triangles": m.T, "rays_per_step": total_rays, "poses_per_step": P * world,
                        "l2": "flushed between steps (256 MiB memset, untimed)" if flush is not None else "not flushed",
