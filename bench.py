@@ -50,6 +50,8 @@ def _args():
                          "NVLink (CUDA IPC) with a device-side completion barrier; nccl = chunked all_gather on a "
                          "side stream; none = pure cast scaling")
     ap.add_argument("--gather-chunks", type=int, default=4, help="N > 1, --gather nccl: chunks")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="process group for barriers / timing reduction (gloo: functional N > 1 check on one GPU)")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -250,10 +252,15 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if a.gpus != world and world > 1:
         print(f"warning: --gpus {a.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    # --dist-backend gloo + more ranks than GPUs: a functional check of the N > 1 path on one GPU
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     P = a.poses or DEFAULT_POSES[a.config]
     cfg = _workload(a.config, P, world, rank)
     m, pat = cfg["mesh"], cfg["pattern"]
@@ -379,6 +386,7 @@ def main():
     cms = statistics.mean(cast_ms)
     if world > 1:
         t = torch.tensor([ms, cms], dtype=torch.float64, device=dev)
+        t = t.cpu() if a.dist_backend == "gloo" else t
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, cms = t.tolist()
     clocks = clk.summary()
@@ -433,6 +441,7 @@ def main():
         sc2.check()
         if world > 1:
             t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            t = t.cpu() if a.dist_backend == "gloo" else t
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = t.item()
         e2e = {"value": rays_rank * world / (ems / 1000), "unit": "rays/s",
