@@ -145,12 +145,34 @@ struct Hit {
     int32_t nodes, tris;
 };
 
+#ifndef FGL_FFMA2
+#define FGL_FFMA2 0
+#endif
+// packed FP32x2 (sm_100: FFMA2): one instruction evaluates the lo and hi planes of an axis
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void ffma2(float a0, float a1, float b, float c0, float c1, float &d0, float &d1) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a0, a1)), "l"(pk2(b, b)), "l"(pk2(c0, c1)));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(r));
+}
+
 // conservative slab test of one child box against [tmin, tmax]; returns the entry distance or +inf
 __device__ __forceinline__ float slab(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
                                       float tmin, float tmax) {
+#if FGL_FFMA2
+    float ax, bx, ay, by, az, bz;
+    ffma2(lx, hx, p.Ix, p.clx, p.chx, ax, bx);
+    ffma2(ly, hy, p.Iy, p.cly, p.chy, ay, by);
+    ffma2(lz, hz, p.Iz, p.clz, p.chz, az, bz);
+#else
     const float ax = fmaf(lx, p.Ix, p.clx), bx = fmaf(hx, p.Ix, p.chx);
     const float ay = fmaf(ly, p.Iy, p.cly), by = fmaf(hy, p.Iy, p.chy);
     const float az = fmaf(lz, p.Iz, p.clz), bz = fmaf(hz, p.Iz, p.chz);
+#endif
     const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
     const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
     return tn <= tf * kExpand ? tn : INFINITY;
