@@ -192,89 +192,7 @@ __device__ __forceinline__ int delta(const uint64_t *__restrict__ k, int64_t n, 
     return 64 + __clz((int)((uint32_t)i ^ (uint32_t)j));
 }
 
-// Karras 2012 (Eq. 6 read as the non-recursive LCP split, R7): one thread per internal node i
-__global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, int64_t n, int2 *__restrict__ child,
-                                                int2 *__restrict__ range, int32_t *__restrict__ parent) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t ki = __ldg(k + i);
-        const int d = (delta(k, n, i, ki, i + 1) - delta(k, n, i, ki, i - 1)) >= 0 ? 1 : -1;
-        const int dmin = delta(k, n, i, ki, i - d);
-        int64_t lmax = 2;
-        while (delta(k, n, i, ki, i + lmax * d) > dmin) lmax <<= 1;
-        int64_t l = 0;
-        for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
-            if (delta(k, n, i, ki, i + (l + t) * d) > dmin) l += t;
-        const int64_t j = i + l * d;
-        const int dnode = delta(k, n, i, ki, j);
-        int64_t s = 0, t = l;
-        do {
-            t = (t + 1) >> 1;
-            if (delta(k, n, i, ki, i + (s + t) * d) > dnode) s += t;
-        } while (t > 1);
-        const int64_t g = i + s * d + (d < 0 ? -1 : 0);
-        const int64_t f = i < j ? i : j, last = i < j ? j : i;
-        int32_t left = f == g ? ~(int32_t)g : (int32_t)g;
-        int32_t right = last == g + 1 ? ~(int32_t)(g + 1) : (int32_t)(g + 1);
-        child[i] = make_int2(left, right);
-        range[i] = make_int2((int32_t)f, (int32_t)last);
-        parent[left >= 0 ? left : (n - 1) + ~left] = (int32_t)i;
-        parent[right >= 0 ? right : (n - 1) + ~right] = (int32_t)i;
-        if (i == 0) parent[0] = -1;
-    }
-}
-
-// Leaf-order gather: tri48[j] = triangle perm[j] {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}, its exact
-// box leafbox[j], and the union of every 8 consecutive leaf boxes (agg[0], 8-lane reduction).
-__device__ __forceinline__ void warp_union(float4 &lo, float4 &hi) {
-    for (int o = 4; o; o >>= 1) {
-        lo.x = fminf(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
-        lo.y = fminf(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
-        lo.z = fminf(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
-        hi.x = fmaxf(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
-        hi.y = fmaxf(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
-        hi.z = fmaxf(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
-    }
-}
-
 constexpr float kInf = __builtin_huge_valf();
-
-__global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, int64_t V,
-                                                 const int32_t *__restrict__ tris,
-                                                 const uint32_t *__restrict__ perm, int64_t n,
-                                                 float4 *__restrict__ tri, float4 *__restrict__ leafbox,
-                                                 float4 *__restrict__ agg) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
-    if (j < n) {
-        const uint32_t k = perm[j];
-        const float3 a = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k), V)),
-                     b = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 1), V)),
-                     c = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 2), V));
-        tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
-        tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
-        tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
-        lo = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
-        hi = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
-        leafbox[2 * j] = lo;
-        leafbox[2 * j + 1] = hi;
-    }
-    warp_union(lo, hi);
-    if ((threadIdx.x & 7) == 0 && j < n) {
-        agg[2 * (j >> 3)] = lo;
-        agg[2 * (j >> 3) + 1] = hi;
-    }
-}
-
-// next aggregate level: union of every 8 consecutive boxes of the level below
-__global__ void __launch_bounds__(256) k_aggregate(const float4 *__restrict__ in, int64_t n_in,
-                                                   float4 *__restrict__ out) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
-    if (j < n_in) lo = in[2 * j], hi = in[2 * j + 1];
-    warp_union(lo, hi);
-    if ((threadIdx.x & 7) == 0 && j < n_in) out[2 * (j >> 3)] = lo, out[2 * (j >> 3) + 1] = hi;
-}
-
 constexpr int kMaxAgg = 10;  // 8^10 > 2^28 triangles
 // level 0 = leaf boxes [n]; levels 1..nlev-1 = unions of 8^k consecutive leaves, stored one after
 // the other in `agg` (level k has ceil(n / 8^k) entries)
@@ -323,32 +241,115 @@ __device__ __forceinline__ void range_box(const AggLevels &L, int64_t a, int64_t
     }
 }
 
-// Binary traversal nodes (node64) and the Eq. 7 node boxes, one thread per internal node, no
-// inter-thread dependencies: children boxes from range_box; subtrees of <= leaf_size triangles
-// become leaves.
-__global__ void __launch_bounds__(256) k_nodes_scan(int64_t n, int leaf_size, const int2 *__restrict__ child,
-                                                    const int2 *__restrict__ range, AggLevels L,
-                                                    float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
+// Karras 2012 (Eq. 6 read as the non-recursive LCP split, R7): one thread per internal node i
+__global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, int64_t n, int2 *__restrict__ child,
+                                                int2 *__restrict__ range, int32_t *__restrict__ parent, AggLevels L,
+                                                float4 *__restrict__ nodebox) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t ki = __ldg(k + i);
+        const int d = (delta(k, n, i, ki, i + 1) - delta(k, n, i, ki, i - 1)) >= 0 ? 1 : -1;
+        const int dmin = delta(k, n, i, ki, i - d);
+        int64_t lmax = 2;
+        while (delta(k, n, i, ki, i + lmax * d) > dmin) lmax <<= 1;
+        int64_t l = 0;
+        for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
+            if (delta(k, n, i, ki, i + (l + t) * d) > dmin) l += t;
+        const int64_t j = i + l * d;
+        const int dnode = delta(k, n, i, ki, j);
+        int64_t s = 0, t = l;
+        do {
+            t = (t + 1) >> 1;
+            if (delta(k, n, i, ki, i + (s + t) * d) > dnode) s += t;
+        } while (t > 1);
+        const int64_t g = i + s * d + (d < 0 ? -1 : 0);
+        const int64_t f = i < j ? i : j, last = i < j ? j : i;
+        int32_t left = f == g ? ~(int32_t)g : (int32_t)g;
+        int32_t right = last == g + 1 ? ~(int32_t)(g + 1) : (int32_t)(g + 1);
+        child[i] = make_int2(left, right);
+        range[i] = make_int2((int32_t)f, (int32_t)last);
+        parent[left >= 0 ? left : (n - 1) + ~left] = (int32_t)i;
+        parent[right >= 0 ? right : (n - 1) + ~right] = (int32_t)i;
+        if (i == 0) parent[0] = -1;
+        // Eq. 7 box of this node by its closed form (exact union of its leaf range)
+        float4 lo, hi;
+        range_box(L, f, last, lo, hi);
+        nodebox[2 * i] = lo;
+        nodebox[2 * i + 1] = hi;
+    }
+}
+
+// Leaf-order gather: tri48[j] = triangle perm[j] {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}, its exact
+// box leafbox[j], and the union of every 8 consecutive leaf boxes (agg[0], 8-lane reduction).
+__device__ __forceinline__ void warp_union(float4 &lo, float4 &hi) {
+    for (int o = 4; o; o >>= 1) {
+        lo.x = fminf(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
+        lo.y = fminf(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
+        lo.z = fminf(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
+        hi.x = fmaxf(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
+        hi.y = fmaxf(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
+        hi.z = fmaxf(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
+    }
+}
+
+
+__global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, int64_t V,
+                                                 const int32_t *__restrict__ tris,
+                                                 const uint32_t *__restrict__ perm, int64_t n,
+                                                 float4 *__restrict__ tri, float4 *__restrict__ leafbox,
+                                                 float4 *__restrict__ agg) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
+    if (j < n) {
+        const uint32_t k = perm[j];
+        const float3 a = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k), V)),
+                     b = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 1), V)),
+                     c = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 2), V));
+        tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
+        tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
+        tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
+        lo = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
+        hi = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
+        leafbox[2 * j] = lo;
+        leafbox[2 * j + 1] = hi;
+    }
+    warp_union(lo, hi);
+    if ((threadIdx.x & 7) == 0 && j < n) {
+        agg[2 * (j >> 3)] = lo;
+        agg[2 * (j >> 3) + 1] = hi;
+    }
+}
+
+// next aggregate level: union of every 8 consecutive boxes of the level below
+__global__ void __launch_bounds__(256) k_aggregate(const float4 *__restrict__ in, int64_t n_in,
+                                                   float4 *__restrict__ out) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
+    if (j < n_in) lo = in[2 * j], hi = in[2 * j + 1];
+    warp_union(lo, hi);
+    if ((threadIdx.x & 7) == 0 && j < n_in) out[2 * (j >> 3)] = lo, out[2 * (j >> 3) + 1] = hi;
+}
+
+// Binary traversal nodes (node64), one thread per internal node, from the children's Eq. 7 boxes
+// (leaf boxes / node boxes); subtrees of <= leaf_size triangles become leaves.
+__global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const int2 *__restrict__ child,
+                                               const int2 *__restrict__ range, const float4 *__restrict__ leafbox,
+                                               const float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n - 1) return;
     const int2 c = child[i], r = range[i];
     const int32_t g = c.x >= 0 ? c.x : ~c.x;  // split: left child covers [f, g], right [g + 1, l]
-    float4 l0, h0, l1, h1;
-    range_box(L, r.x, g, l0, h0);
-    range_box(L, g + 1, r.y, l1, h1);
-    nodebox[2 * i] = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.f);
-    nodebox[2 * i + 1] = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.f);
-    if (nodes) {
-        const int32_t n0 = g - r.x + 1, n1 = r.y - g;
-        const int32_t ref0 = (c.x < 0 || n0 <= leaf_size) ? make_leaf(r.x, n0) : c.x;
-        const int32_t ref1 = (c.y < 0 || n1 <= leaf_size) ? make_leaf(g + 1, n1) : c.y;
-        Node64 nd;
-        nd.a = make_float4(l0.x, h0.x, l0.y, h0.y);
-        nd.b = make_float4(l1.x, h1.x, l1.y, h1.y);
-        nd.c = make_float4(l0.z, h0.z, l1.z, h1.z);
-        nd.d = make_int4(ref0, ref1, 0, 0);
-        nodes[i] = nd;
-    }
+    const float4 *b0 = c.x >= 0 ? nodebox + 2 * (int64_t)c.x : leafbox + 2 * (int64_t)(~c.x);
+    const float4 *b1 = c.y >= 0 ? nodebox + 2 * (int64_t)c.y : leafbox + 2 * (int64_t)(~c.y);
+    const float4 l0 = b0[0], h0 = b0[1], l1 = b1[0], h1 = b1[1];
+    const int32_t n0 = g - r.x + 1, n1 = r.y - g;
+    const int32_t ref0 = (c.x < 0 || n0 <= leaf_size) ? make_leaf(r.x, n0) : c.x;
+    const int32_t ref1 = (c.y < 0 || n1 <= leaf_size) ? make_leaf(g + 1, n1) : c.y;
+    Node64 nd;
+    nd.a = make_float4(l0.x, h0.x, l0.y, h0.y);
+    nd.b = make_float4(l1.x, h1.x, l1.y, h1.y);
+    nd.c = make_float4(l0.z, h0.z, l1.z, h1.z);
+    nd.d = make_int4(ref0, ref1, 0, 0);
+    nodes[i] = nd;
 }
 
 // depth of every internal node (root = 0) by walking the parent links (L2-resident, ~log T steps)
@@ -506,11 +507,14 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
         }
         return;
     }
-    k_karras<<<grid_for(T - 1), 256, 0, s>>>(b.keys[slot], T, b.child, b.range, b.parent);
+    k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[slot], T, b.child, b.range, b.parent, L,
+                                                            b.nodebox);
     FGL_LAUNCHED("k_karras");
-    k_nodes_scan<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, leaf_size, b.child, b.range, L, b.nodebox,
-                                                                width == 2 ? b.nodes : nullptr);
-    FGL_LAUNCHED("k_nodes_scan");
+    if (width == 2) {
+        k_nodes<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.leafbox, b.nodebox,
+                                                               b.nodes);
+        FGL_LAUNCHED("k_nodes");
+    }
     if (width == 4) {
         k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
         FGL_LAUNCHED("k_depth");

@@ -23,9 +23,10 @@ constexpr int kWarps = kThreads / 32;
 #ifndef FGL_SORT_ITEMS
 #define FGL_SORT_ITEMS 16
 #endif
-constexpr int kItems = FGL_SORT_ITEMS;          // keys per thread
-constexpr int kTile = kThreads * kItems;        // keys per tile
-constexpr int kWarpSpan = kTile / kWarps;       // 512 contiguous keys per warp
+constexpr int kItems = FGL_SORT_ITEMS;          // keys per thread (large sorts: kItemsLarge)
+constexpr int kTile = kThreads * kItems;        // keys per tile (sizes the status array)
+constexpr int kItemsLarge = 8;                  // >= 4 M keys: smaller tiles, 64 registers, 2x occupancy
+constexpr int64_t kLargeSort = int64_t(1) << 22;
 constexpr uint64_t kAgg = 1ull << 30, kPrefix = 2ull << 30, kValMask = (1ull << 30) - 1;
 
 __global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t *__restrict__ keys, int64_t n, int npass,
@@ -44,6 +45,7 @@ __global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t *__restr
     }
 }
 
+template <int kIt>
 __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restrict__ kin,
                                                        const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
                                                        uint32_t *__restrict__ vout, int64_t n, int shift,
@@ -73,12 +75,13 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
     __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t lt = (1u << lane) - 1u;
-    const int64_t base = (int64_t)tile * kTile + (int64_t)w * kWarpSpan;
-    uint64_t key[kItems];
-    uint32_t val[kItems];
-    uint32_t rank[kItems];
+    constexpr int kT = kThreads * kIt, kSpan = kT / kWarps;
+    const int64_t base = (int64_t)tile * kT + (int64_t)w * kSpan;
+    uint64_t key[kIt];
+    uint32_t val[kIt];
+    uint32_t rank[kIt];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
+    for (int i = 0; i < kIt; ++i) {
         const int64_t idx = base + i * 32 + lane;
         const bool ok = idx < n;
         key[i] = ok ? kin[idx] : 0ull;
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
+    for (int i = 0; i < kIt; ++i) {
         const int64_t idx = base + i * 32 + lane;
         if (idx < n) {
             const uint32_t d = (uint32_t)((key[i] >> shift) & 0xFF);
@@ -153,7 +156,10 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
 }
 }  // namespace
 
-int sort_tile_blocks(int64_t n) { return (int)((n + kTile - 1) / kTile); }
+int sort_tile_blocks(int64_t n) {
+    const int64_t tile = n >= kLargeSort ? kThreads * kItemsLarge : kTile;
+    return (int)((n + tile - 1) / tile);
+}
 
 void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s) {
     int npass = (key_bits + 7) / 8;
@@ -179,8 +185,12 @@ void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_
     int cur = 0;
     for (int p = 0; p < npass; ++p) {
         if (++*epoch == 0) ++*epoch;  // epoch 0 marks never-written status words
-        k_onesweep<<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, 8 * p, ghist + 256 * p, status,
-                                             tile_ctr + p, *epoch);
+        if (n >= kLargeSort)
+            k_onesweep<kItemsLarge><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, 8 * p,
+                                                              ghist + 256 * p, status, tile_ctr + p, *epoch);
+        else
+            k_onesweep<kItems><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, 8 * p,
+                                                         ghist + 256 * p, status, tile_ctr + p, *epoch);
         FGL_LAUNCHED("k_onesweep");
         cur ^= 1;
     }

@@ -167,7 +167,7 @@ def test_build_rooms_full_size(fgl):
     assert st["triangles"] == m.T and st["build_ms"] > 0
 
 
-@pytest.mark.parametrize("n", [0, 1, 2, 3, 4095, 4096, 4097, 100_003, 1_000_000])
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4095, 4096, 4097, 100_003, 1_000_000, 5_000_011])
 @pytest.mark.parametrize("bits", [8, 30, 63, 64])
 def test_sort_pairs_matches_oracle(fgl, n, bits):
     rng = np.random.default_rng(n + bits)
