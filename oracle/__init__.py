@@ -60,6 +60,7 @@ def lib():
             "orc_stable_sort": (None, [P, P, c_int64, P, P]),
             "orc_radix_tree": (c_int, [P, c_int64, P, P]),
             "orc_refit": (None, [P, P, P, c_int64, P, P, P]),
+            "orc_nearest": (None, [P, c_int64, P, c_int64, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -270,3 +271,27 @@ def lbvh(verts, tris, bits: int = 21, cubic: bool = False):
     leaf, node = refit(verts, tris, perm, child)
     return dict(cent=cent, lo=lo, hi=hi, code=code, sorted_keys=sk, perm=perm, child=child, range=rng,
                 leaf_box=leaf, node_box=node)
+
+
+# --- point-cloud metrics (§V-A; reading R23) ------------------------------------------
+def nearest(points, queries):
+    """Exact nearest neighbour of every query in `points` (double distances, ties -> smaller index)."""
+    p = _c(points, np.float32).reshape(-1, 3)
+    q = _c(queries, np.float32).reshape(-1, 3)
+    d = np.empty(q.shape[0])
+    i = np.empty(q.shape[0], np.int32)
+    lib().orc_nearest(_p(p), p.shape[0], _p(q), q.shape[0], _p(d), _p(i))
+    return d, i
+
+
+def cloud_metrics(a, b, tau):
+    """Symmetric Chamfer distance (unsquared distances, mean of the two directed means), precision
+    (fraction of a within tau of b), recall (fraction of b within tau of a) and F-score (harmonic
+    mean; 0 when P + R = 0). "Within" is d <= tau (R23)."""
+    dab, _ = nearest(b, a)
+    dba, _ = nearest(a, b)
+    cd = 0.5 * (dab.mean() + dba.mean())
+    prec = float(np.mean(dab <= tau))
+    rec = float(np.mean(dba <= tau))
+    f = 2 * prec * rec / (prec + rec) if prec + rec > 0 else 0.0
+    return dict(chamfer=float(cd), precision=prec, recall=rec, fscore=f, d_ab=dab, d_ba=dba)

@@ -516,3 +516,28 @@ void orc_refit(const float *verts, const int32_t *tris, const uint32_t *perm, in
     free(order);
     free(stk);
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Point-cloud metrics of §V-A (SPEC evalkit S:527-545): for each query point the exact   */
+/* nearest neighbour in a reference cloud by the naive O(m n) scan, Euclidean distance in double, */
+/* ties to the smaller index. Chamfer / precision / recall / F-score are formed from these        */
+/* distances in oracle/__init__.py (reading R23).                                                 */
+/* ------------------------------------------------------------------------------------------ */
+void orc_nearest(const float *pts, int64_t n, const float *q, int64_t m, double *dist, int32_t *idx) {
+#pragma omp parallel for schedule(dynamic, 16) num_threads(orc_get_threads())
+    for (int64_t i = 0; i < m; ++i) {
+        double qx = q[3 * i], qy = q[3 * i + 1], qz = q[3 * i + 2];
+        double best = INFINITY;
+        int32_t bi = -1;
+        for (int64_t j = 0; j < n; ++j) {
+            double dx = (double)pts[3 * j] - qx, dy = (double)pts[3 * j + 1] - qy, dz = (double)pts[3 * j + 2] - qz;
+            double d2 = dx * dx + dy * dy + dz * dz;
+            if (d2 < best) {
+                best = d2;
+                bi = (int32_t)j;
+            }
+        }
+        dist[i] = sqrt(best);
+        idx[i] = bi;
+    }
+}

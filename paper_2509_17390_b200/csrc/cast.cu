@@ -534,6 +534,9 @@ struct RaysGen {
     }
 };
 
+#ifndef FGL_SPECULATE
+#define FGL_SPECULATE 1  // while-while: keep descending after a postponed leaf until all lanes hold one
+#endif
 #ifndef FGL_APPROX_PRE
 #define FGL_APPROX_PRE 0
 #endif
@@ -687,7 +690,11 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
                 leaf = cur;
                 cur = pop();
             }
+            #if FGL_SPECULATE
             if (!__any_sync(__activemask(), leaf == 0)) break;
+#else
+            if (leaf != 0) break;
+#endif
         }
         while (leaf < 0) {
             const int32_t v = ~leaf;
