@@ -179,6 +179,22 @@ FGL_API fgl_status fgl_cast_spinning_gather_signal(const fgl_scene *scene, const
                                                    int32_t *const *flags, int32_t npeer, void *cuda_stream);
 FGL_API fgl_status fgl_wait_flag(const int32_t *flag, int32_t target, void *cuda_stream);
 
+/* ---- point-cloud metrics (§V-A) --------------------------------
+ * A point scene indexes a cloud with the same LBVH (one degenerate triangle (i, i, i) per point;
+ * build it with fgl_scene_build, width 2). Same validation / FGL_ASYNC rules as upload_mesh. */
+FGL_API fgl_status fgl_scene_upload_points(fgl_scene *scene, const float *xyz, int64_t n, int ptr_kind,
+                                           void *cuda_stream);
+/* Exact nearest neighbour (Euclidean, float32 distances, ties to the smaller index) in a built
+ * point scene for m device query points [m][3]: dist [m] (NaN for a non-finite query), idx [m]. */
+FGL_API fgl_status fgl_nearest(const fgl_scene *scene, const float *queries, int64_t m, float *dist, int32_t *idx,
+                               void *cuda_stream);
+/* From directed nearest-neighbour distances d_ab [n_a] (a -> b) and d_ba [n_b] (device, NaN
+ * entries ignored): out (device double [6]) = {symmetric Chamfer distance (mean of the two directed
+ * means of unsquared distances), precision = frac(d_ab <= tau), recall = frac(d_ba <= tau),
+ * F-score = 2PR/(P+R) (0 if P+R = 0), finite n_a, finite n_b}. Reading R23. */
+FGL_API fgl_status fgl_cloud_metrics(const float *d_ab, int64_t n_a, const float *d_ba, int64_t n_b, float tau,
+                                     double *out, void *cuda_stream);
+
 /* ---- LBVH internals, for parity tests (host destination pointers; each may be NULL) ----- */
 typedef struct {
     float *scene_box;      /* [6]  lo.xyz, hi.xyz                                              */

@@ -26,6 +26,7 @@ struct fgl_scene {
     fgl::CastCounter *counters = nullptr;
     std::atomic<uint32_t> slot{0};
     bool built = false;
+    bool points = false;  // uploaded with fgl_scene_upload_points (degenerate triangles (i, i, i))
     int bits = 21, leaf_size = 4;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     size_t bytes = 0;
@@ -263,6 +264,7 @@ fgl_status fgl_scene_upload_mesh(fgl_scene *s, const float *verts, int64_t V, co
     }
     s->b.T = T;
     s->V = V, s->T = T;
+    s->points = false;
     cudaMemcpyKind kind = ptr_kind == FGL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     FGL_CUDA(cudaMemcpyAsync(s->verts, verts, sizeof(float) * 3 * V, kind, st));
     FGL_CUDA(cudaMemcpyAsync(s->tris, tris, sizeof(int32_t) * 3 * T, kind, st));
@@ -272,6 +274,71 @@ fgl_status fgl_scene_upload_mesh(fgl_scene *s, const float *verts, int64_t V, co
     FGL_CUDA(cudaStreamSynchronize(st));
     if (*s->hflag & 1u) throw Error(FGL_E_DATA, "triangle index out of range [0, V)");
     if (*s->hflag & 2u) throw Error(FGL_E_DATA, "non-finite vertex coordinate");
+    FGL_API_END
+}
+
+fgl_status fgl_scene_upload_points(fgl_scene *s, const float *xyz, int64_t n, int ptr_kind, void *stream) {
+    FGL_API_BEGIN
+    if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    const bool async = (ptr_kind & FGL_ASYNC) != 0;
+    ptr_kind &= ~FGL_ASYNC;
+    if (ptr_kind != FGL_HOST && ptr_kind != FGL_DEVICE) throw Error(FGL_E_USAGE, "ptr_kind must be FGL_HOST or FGL_DEVICE");
+    if (n <= 0) throw Error(FGL_E_DATA, "point cloud is empty");
+    if (!xyz) throw Error(FGL_E_USAGE, "xyz is NULL");
+    if (n > fgl::kMaxTris) throw Error(FGL_E_USAGE, "too many points (n must be < 2^28)");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    s->built = false;
+    if (n > s->cap_V) {
+        if (s->verts) cudaFree(s->verts), s->verts = nullptr;
+        FGL_CUDA(cudaMalloc((void **)&s->verts, sizeof(float) * 3 * n));
+        s->cap_V = n;
+    }
+    if (n > s->cap_T) {
+        if (s->tris) cudaFree(s->tris), s->tris = nullptr;
+        FGL_CUDA(cudaMalloc((void **)&s->tris, sizeof(int32_t) * 3 * n));
+        alloc_build(s, n);
+        s->cap_T = n;
+    }
+    s->b.T = n;
+    s->V = n, s->T = n;
+    s->points = true;
+    FGL_CUDA(cudaMemcpyAsync(s->verts, xyz, sizeof(float) * 3 * n,
+                             ptr_kind == FGL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    fgl::launch_iota3(s->tris, n, st);
+    fgl::launch_validate(s->verts, n, s->tris, n, s->vflag, st);
+    if (async) return FGL_OK;
+    FGL_CUDA(cudaMemcpyAsync(s->hflag, s->vflag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    FGL_CUDA(cudaStreamSynchronize(st));
+    if (*s->hflag & 2u) throw Error(FGL_E_DATA, "non-finite point coordinate");
+    FGL_API_END
+}
+
+fgl_status fgl_nearest(const fgl_scene *s, const float *queries, int64_t m, float *dist, int32_t *idx, void *stream) {
+    FGL_API_BEGIN
+    check_built(s);
+    if (!s->points) throw Error(FGL_E_USAGE, "fgl_nearest needs a point scene (fgl_scene_upload_points)");
+    if (m < 0) throw Error(FGL_E_USAGE, "m must be >= 0");
+    if (m == 0) return FGL_OK;
+    if (!queries || !dist || !idx) throw Error(FGL_E_USAGE, "NULL pointer argument");
+    if (s->b.width != 2) throw Error(FGL_E_USAGE, "fgl_nearest needs a width-2 build");
+    DeviceGuard g(s->dev);
+    fgl::launch_nearest(view(s), queries, m, dist, idx, (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_cloud_metrics(const float *d_ab, int64_t n_a, const float *d_ba, int64_t n_b, float tau, double *out,
+                             void *stream) {
+    FGL_API_BEGIN
+    if (n_a < 0 || n_b < 0) throw Error(FGL_E_USAGE, "negative count");
+    if (!(tau > 0.f)) throw Error(FGL_E_USAGE, "tau must be > 0");
+    if (!out || (n_a && !d_ab) || (n_b && !d_ba)) throw Error(FGL_E_USAGE, "NULL pointer argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    void *scratch = nullptr;
+    FGL_CUDA(cudaMallocAsync(&scratch, 6 * sizeof(double) + 16, st));
+    FGL_CUDA(cudaMemsetAsync(scratch, 0, 6 * sizeof(double) + 16, st));
+    fgl::launch_metrics(d_ab, n_a, d_ba, n_b, tau, (double *)scratch, (unsigned int *)((char *)scratch + 48), out, st);
+    cudaFreeAsync(scratch, st);
     FGL_API_END
 }
 

@@ -157,6 +157,11 @@ void launch_cast_bruteforce(const float *verts, int64_t V, const int32_t *tris, 
                             const float *dir,
                             int64_t R, float t_min, float t_max, float *range, int32_t *tri_id, cudaStream_t s);
 void launch_wait_flag(const int32_t *flag, int32_t target, cudaStream_t s);
+// points.cu
+void launch_iota3(int32_t *tris, int64_t n, cudaStream_t s);
+void launch_nearest(const SceneView &sv, const float *q, int64_t m, float *dist, int32_t *idx, cudaStream_t s);
+void launch_metrics(const float *dab, int64_t na, const float *dba, int64_t nb, float tau, double *acc,
+                    unsigned int *sync, double *out, cudaStream_t s);
 void launch_export_spinning(const SpinParams &p, const float *poses, int64_t P, float *orig, float *dir,
                             cudaStream_t s);
 void launch_export_rosette(const RosetteParams &p, const float *poses, int64_t P, float *orig, float *dir,

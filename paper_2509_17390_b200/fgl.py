@@ -80,6 +80,9 @@ _SIGS = {
     "fgl_cast_spinning_gather_signal": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_int64, c_void_p,
                                                 c_void_p, c_void_p, c_int32, c_void_p]),
     "fgl_wait_flag": (c_int, [c_void_p, c_int32, c_void_p]),
+    "fgl_scene_upload_points": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
+    "fgl_nearest": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "fgl_cloud_metrics": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_float, c_void_p, c_void_p]),
     "fgl_alloc": (c_int, [c_int, c_int64, POINTER(c_void_p)]),
     "fgl_free": (c_int, [c_void_p]),
     "fgl_ipc_get_handle": (c_int, [c_void_p, c_void_p]),
@@ -425,6 +428,48 @@ def cast_spinning_gather(scene: "Scene", poses, pattern, first_pose: int, range_
 def wait_flag(flag_ptr: int, target: int, stream=None):
     """Make the stream wait (on the device) until the int32 counter at flag_ptr reaches target."""
     _check(lib().fgl_wait_flag(flag_ptr, int(target), _stream(stream)))
+
+
+class PointCloud:
+    """A point cloud indexed by the LBVH (point scene) for exact nearest-neighbour queries."""
+
+    def __init__(self, xyz, device=None, stream=None):
+        self.scene = Scene(device=device, build=False, leaf_size=2, width=2)
+        self.device = self.scene.device
+        on_dev = isinstance(xyz, torch.Tensor) and xyz.is_cuda
+        if on_dev:
+            x = xyz.to(torch.float32).contiguous().reshape(-1, 3)
+            kind, ptr = DEVICE, x.data_ptr()
+        else:
+            x = np.ascontiguousarray(np.asarray(xyz.cpu().numpy() if isinstance(xyz, torch.Tensor) else xyz,
+                                                dtype=np.float32).reshape(-1, 3))
+            kind, ptr = HOST, x.ctypes.data
+        self.n = int(x.shape[0])
+        _check(lib().fgl_scene_upload_points(self.scene._h, ptr, self.n, kind, _stream(stream)))
+        self.scene.T = self.n
+        self.scene.build(stream=stream)
+
+    def nearest(self, queries, stream=None):
+        q = _dev(queries, torch.float32, self.device, (-1, 3))
+        m = int(q.shape[0])
+        d = torch.empty(m, dtype=torch.float32, device=self.device)
+        i = torch.empty(m, dtype=torch.int32, device=self.device)
+        _check(lib().fgl_nearest(self.scene._h, q.data_ptr(), m, d.data_ptr(), i.data_ptr(), _stream(stream)))
+        return d, i
+
+
+def cloud_metrics(a, b, tau: float, device=None, stream=None) -> dict:
+    """Symmetric Chamfer distance, precision, recall and F-score of clouds a, b (§V-A):
+    two exact nearest-neighbour passes over LBVH-indexed clouds + one reduction kernel."""
+    ca, cb = PointCloud(a, device, stream), PointCloud(b, device, stream)
+    d_ab, _ = cb.nearest(_dev(a, torch.float32, cb.device, (-1, 3)), stream)
+    d_ba, _ = ca.nearest(_dev(b, torch.float32, ca.device, (-1, 3)), stream)
+    out = torch.empty(6, dtype=torch.float64, device=ca.device)
+    _check(lib().fgl_cloud_metrics(d_ab.data_ptr(), int(d_ab.numel()), d_ba.data_ptr(), int(d_ba.numel()),
+                                   float(tau), out.data_ptr(), _stream(stream)))
+    o = out.cpu().tolist()
+    return dict(chamfer=o[0], precision=o[1], recall=o[2], fscore=o[3], n_a=int(o[4]), n_b=int(o[5]),
+                d_ab=d_ab, d_ba=d_ba)
 
 
 def kernel_launches() -> int:
