@@ -54,7 +54,8 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
     const float dy = fabsf(r.dy) < tiny ? copysignf(tiny, r.dy) : r.dy;
     const float dz = fabsf(r.dz) < tiny ? copysignf(tiny, r.dz) : r.dz;
 #if FGL_APPROX_PRE
-    // MUFU reciprocals (<= 2 ulp): covered by the slab slack, consistent per ray
+    // MUFU reciprocals (<= 2 ulp): covered by the slab slack, consistent per ray;
+    // the shear S is likewise only required to be consistent per ray (watertightness)
     p.Ix = __fdividef(1.f, dx), p.Iy = __fdividef(1.f, dy), p.Iz = __fdividef(1.f, dz);
 #else
     p.Ix = __frcp_rn(dx), p.Iy = __frcp_rn(dy), p.Iz = __frcp_rn(dz);
@@ -176,6 +177,18 @@ __device__ __forceinline__ float slab(const Pre &p, float lx, float hx, float ly
     const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
     const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
     return tn <= tf * kExpand ? tn : INFINITY;
+}
+
+// same test, hit flag and entry distance returned separately (no +inf materialisation)
+__device__ __forceinline__ bool slab_hit(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
+                                         float tmin, float tmax, float &tn_out) {
+    const float ax = fmaf(lx, p.Ix, p.clx), bx = fmaf(hx, p.Ix, p.chx);
+    const float ay = fmaf(ly, p.Iy, p.cly), by = fmaf(hy, p.Iy, p.chy);
+    const float az = fmaf(lz, p.Iz, p.clz), bz = fmaf(hz, p.Iz, p.chz);
+    const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
+    const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
+    tn_out = tn;
+    return tn <= tf * kExpand;
 }
 
 constexpr int32_t kDone = INT_MAX;  // "no more work" (never a node index: T - 1 < 2^28)
@@ -452,8 +465,13 @@ __device__ __forceinline__ void rotate_pose(const float *__restrict__ pose, floa
     float dx = r0.x * sx + r0.y * sy + r0.z * sz;
     float dy = r1.x * sx + r1.y * sy + r1.z * sz;
     float dz = r2.x * sx + r2.y * sy + r2.z * sz;
+#if FGL_APPROX_PRE
+    const float rn = rsqrtf(dx * dx + dy * dy + dz * dz);  // MUFU.RSQ (<= 2 ulp), same in cast and export
+    r.dx = dx * rn, r.dy = dy * rn, r.dz = dz * rn;
+#else
     const float n = sqrtf(dx * dx + dy * dy + dz * dz);
     r.dx = __fdiv_rn(dx, n), r.dy = __fdiv_rn(dy, n), r.dz = __fdiv_rn(dz, n);
+#endif
     r.ox = r0.w, r.oy = r1.w, r.oz = r2.w;
 }
 
@@ -538,7 +556,7 @@ struct RaysGen {
 #define FGL_SPECULATE 1  // while-while: keep descending after a postponed leaf until all lanes hold one
 #endif
 #ifndef FGL_APPROX_PRE
-#define FGL_APPROX_PRE 0
+#define FGL_APPROX_PRE 1
 #endif
 #ifndef FGL_BRANCHFREE_PUSH
 #define FGL_BRANCHFREE_PUSH 0
@@ -662,9 +680,9 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
             const int4 nd = __ldg(reinterpret_cast<const int4 *>(np + 3));
             if (kCount) ++h.nodes;
             const float lim = h.t;
-            const float t0 = slab(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim);
-            const float t1 = slab(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim);
-            const bool h0 = t0 != INFINITY, h1 = t1 != INFINITY;
+            float t0, t1;
+            const bool h0 = slab_hit(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim, t0);
+            const bool h1 = slab_hit(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim, t1);
 #if FGL_BRANCHFREE_PUSH
             {
                 const bool swap = t1 < t0;  // (only meaningful when both are hit)
