@@ -59,7 +59,8 @@ typedef struct {
                             [o, o+L] read as a cube (isotropic cells; reading R22);
                             1 = per-axis box, L_x, L_y, L_z separately                         */
     int32_t width;       /* traversal node width: 2 (binary "node64", default) or 4 ("node128")    */
-    int32_t reserved[4]; /* must be zero                                                     */
+    int32_t quantized;   /* width 4 only: 1 = 8-bit child boxes, outward-rounded ("node64q")      */
+    int32_t reserved[3]; /* must be zero                                                     */
 } fgl_build_opts;
 
 typedef struct {

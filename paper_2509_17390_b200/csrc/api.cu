@@ -120,7 +120,9 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.depth, nin);
 }
 
-fgl::SceneView view(const fgl_scene *s) { return fgl::SceneView{s->b.tri, s->b.nodes, s->b.nodes4, s->b.width}; }
+fgl::SceneView view(const fgl_scene *s) {
+    return fgl::SceneView{s->b.tri, s->b.nodes, s->b.nodes4, s->b.width, s->b.quantized};
+}
 
 fgl::CastCounter *next_counter(const fgl_scene *s) {
     auto *ms = const_cast<fgl_scene *>(s);
@@ -359,13 +361,15 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     FGL_API_BEGIN
     if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
     if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
-    int bits = 13, leaf = 2, cubic = 1, width = 2;
+    int bits = 13, leaf = 2, cubic = 1, width = 2, quant = 0;
     if (opts) {
+        if (opts->quantized < 0 || opts->quantized > 1) throw Error(FGL_E_USAGE, "quantized must be 0 or 1");
+        quant = opts->quantized;
         if (opts->width) width = opts->width;
         if (width != 2 && width != 4) throw Error(FGL_E_USAGE, "width must be 2 or 4");
         if (opts->morton_box < 0 || opts->morton_box > 1) throw Error(FGL_E_USAGE, "morton_box must be 0 or 1");
         cubic = opts->morton_box == 0;
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 3; ++i)
             if (opts->reserved[i]) throw Error(FGL_E_USAGE, "fgl_build_opts.reserved must be zero");
         if (opts->morton_bits) bits = opts->morton_bits;
         if (opts->leaf_size) leaf = opts->leaf_size;
@@ -379,7 +383,8 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     FGL_CUDA(cudaStreamIsCapturing(st, &cap));
     const bool timed = cap == cudaStreamCaptureStatusNone;  // build_ms is not recorded inside a graph
     if (timed) FGL_CUDA(cudaEventRecord(s->ev0, st));
-    fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, st);
+    if (quant && width != 4) throw Error(FGL_E_USAGE, "quantized nodes need width 4");
+    fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, quant, st);
     if (timed) FGL_CUDA(cudaEventRecord(s->ev1, st));
     s->built = true;
     FGL_API_END

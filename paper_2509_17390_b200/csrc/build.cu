@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(256) k_depth(int64_t n, const int32_t *__restr
 __global__ void __launch_bounds__(256) k_nodes4(int64_t n, int leaf_size, const int2 *__restrict__ child,
                                                 const int2 *__restrict__ range, const int32_t *__restrict__ depth,
                                                 const float4 *__restrict__ leafbox,
-                                                const float4 *__restrict__ nodebox, Node128 *__restrict__ nodes4) {
+                                                const float4 *__restrict__ nodebox, Node128 *__restrict__ nodes4,
+                                                int quantized) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
         const int2 ri = range[i];
         if (i != 0 && ((depth[i] & 1) || ri.y - ri.x + 1 <= leaf_size)) continue;
@@ -408,6 +409,42 @@ __global__ void __launch_bounds__(256) k_nodes4(int64_t n, int leaf_size, const 
             }
         }
         const int valid = k;
+        if (quantized) {
+            NodeQ q;
+            uint32_t bits = 0, qlo[3] = {0, 0, 0}, qhi[3] = {0, 0, 0};
+            float p[3];
+            for (int a = 0; a < 3; ++a) {
+                float plo = lo[a][0], phi = hi[a][0];
+                for (int c = 1; c < valid; ++c) plo = fminf(plo, lo[a][c]), phi = fmaxf(phi, hi[a][c]);
+                p[a] = plo;
+                // smallest e with 255 * 2^e >= the (round-up) extent
+                const float ext = __fsub_ru(phi, plo);
+                int e = -126;
+                if (ext > 0.f) {
+                    int x;
+                    const float m = frexpf(__fdiv_ru(ext, 255.f), &x);  // r = m 2^x, m in [0.5, 1)
+                    e = m == 0.5f ? x - 1 : x;
+                    e = e < -126 ? -126 : (e > 127 ? 127 : e);
+                }
+                bits |= (uint32_t)(e + 127) << (8 * a);
+                for (int c = 0; c < valid; ++c) {
+                    const float fl = floorf(ldexpf(__fsub_rd(lo[a][c], plo), -e));
+                    const float fh = ceilf(ldexpf(__fsub_ru(hi[a][c], plo), -e));
+                    const uint32_t bl = fl <= 0.f ? 0u : (fl >= 255.f ? 255u : (uint32_t)fl);
+                    const uint32_t bh = fh <= 0.f ? 0u : (fh >= 255.f ? 255u : (uint32_t)fh);
+                    qlo[a] |= bl << (8 * c);
+                    qhi[a] |= bh << (8 * c);
+                }
+            }
+            bits |= (uint32_t)((1u << valid) - 1u) << 24;
+            for (int c = valid; c < 4; ++c) ref[c] = kEmptyRef;
+            q.f0 = make_float4(p[0], p[1], p[2], __uint_as_float(bits));
+            q.q0 = make_int4((int)qlo[0], (int)qhi[0], (int)qlo[1], (int)qhi[1]);
+            q.q1 = make_int4((int)qlo[2], (int)qhi[2], ref[0], ref[1]);
+            q.q2 = make_int4(ref[2], ref[3], 0, 0);
+            reinterpret_cast<NodeQ *>(nodes4)[i] = q;
+            continue;
+        }
         for (; k < 4; ++k) {
             ref[k] = kEmptyRef;
             for (int a = 0; a < 3; ++a) lo[a][k] = hi[a][k] = kFarBox;
@@ -424,8 +461,30 @@ __global__ void __launch_bounds__(256) k_nodes4(int64_t n, int leaf_size, const 
 }
 
 // T == 1: a root whose first child is the single leaf and whose other children are empty
-__global__ void k_single4(const float4 *__restrict__ leafbox, Node128 *__restrict__ nodes4) {
+__global__ void k_single4(const float4 *__restrict__ leafbox, Node128 *__restrict__ nodes4, int quantized) {
     const float4 lo = leafbox[0], hi = leafbox[1];
+    if (quantized) {  // one child covering the whole box: q = (0, 255) on every axis
+        NodeQ q;
+        uint32_t bits = 1u << 24;
+        const float l[3] = {lo.x, lo.y, lo.z}, h[3] = {hi.x, hi.y, hi.z};
+        for (int a = 0; a < 3; ++a) {
+            const float ext = __fsub_ru(h[a], l[a]);
+            int e = -126;
+            if (ext > 0.f) {
+                int x;
+                const float m = frexpf(__fdiv_ru(ext, 255.f), &x);
+                e = m == 0.5f ? x - 1 : x;
+                e = e < -126 ? -126 : (e > 127 ? 127 : e);
+            }
+            bits |= (uint32_t)(e + 127) << (8 * a);
+        }
+        q.f0 = make_float4(lo.x, lo.y, lo.z, __uint_as_float(bits));
+        q.q0 = make_int4(0, 255, 0, 255);
+        q.q1 = make_int4(0, 255, make_leaf(0, 1), kEmptyRef);
+        q.q2 = make_int4(kEmptyRef, kEmptyRef, 0, 0);
+        reinterpret_cast<NodeQ *>(nodes4)[0] = q;
+        return;
+    }
     Node128 nd;
     const float F = kFarBox;
     nd.f[0] = make_float4(lo.x, F, F, F), nd.f[1] = make_float4(hi.x, F, F, F);
@@ -471,8 +530,9 @@ void launch_morton_points(const float *pts, int64_t n, const float *lo, const fl
 }
 
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  int cubic, int width, cudaStream_t s) {
+                  int cubic, int width, int quantized, cudaStream_t s) {
     b.width = width;
+    b.quantized = width == 4 ? quantized : 0;
     const int64_t T = b.T;
     const int key_bits = 3 * bits;
     k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
@@ -499,7 +559,7 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
     }
     if (T == 1) {
         if (width == 4) {
-            k_single4<<<1, 1, 0, s>>>(b.leafbox, b.nodes4);
+            k_single4<<<1, 1, 0, s>>>(b.leafbox, b.nodes4, b.quantized);
             FGL_LAUNCHED("k_single4");
         } else {
             k_single<<<1, 1, 0, s>>>(b.leafbox, b.nodes);
@@ -519,7 +579,7 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
         k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
         FGL_LAUNCHED("k_depth");
         k_nodes4<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.depth, b.leafbox, b.nodebox,
-                                                 b.nodes4);
+                                                 b.nodes4, b.quantized);
         FGL_LAUNCHED("k_nodes4");
     }
 }

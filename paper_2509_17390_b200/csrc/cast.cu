@@ -348,6 +348,100 @@ __device__ __forceinline__ Hit trace4(const SceneView &sv, const Ray &r, float t
     return h;
 }
 
+// 4-wide traversal over 8-bit quantised child boxes (node64q, 4 x LDG.128 per node). A child
+// plane x = p + q s is evaluated as t = q (s I) + (p I + c): s I is exact (s a power of two), and the
+// per-node offset p I + c is pushed outward by 2^-22 |p I| on top of the per-ray slack, so the test
+// stays conservative for the decoded (outward-rounded) box. Bytes become floats with the
+// 2^23-mantissa trick (PRMT + FADD).
+__device__ __forceinline__ float byte_f(uint32_t w, int k) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7440u | (uint32_t)k)) - 8388608.0f;
+}
+
+template <bool kCount>
+__device__ __forceinline__ Hit trace4q(const SceneView &sv, const Ray &r, float tmin, float tmax) {
+    const Pre p = precompute(r);
+    Hit h{tmax, INT_MAX, 0, 0};
+    int32_t st_ref[kStack];
+    float st_t[kStack];
+    int sp = 0;
+    int32_t cur = 0;
+    int32_t leaf = 0;
+    const NodeQ *nq = reinterpret_cast<const NodeQ *>(sv.nodes4);
+    const float sgx = p.Ix >= 0.f ? 1.f : -1.f, sgy = p.Iy >= 0.f ? 1.f : -1.f, sgz = p.Iz >= 0.f ? 1.f : -1.f;
+    auto pop = [&]() -> int32_t {
+        while (sp > 0) {
+            --sp;
+            if (st_t[sp] <= h.t * kExpand) return st_ref[sp];
+        }
+        return kDone;
+    };
+    while (true) {
+        while (cur >= 0 && cur != kDone) {
+            const float4 f0 = __ldg(&nq[cur].f0);
+            const int4 q0 = __ldg(&nq[cur].q0), q1 = __ldg(&nq[cur].q1), q2 = __ldg(&nq[cur].q2);
+            if (kCount) ++h.nodes;
+            const uint32_t bits = __float_as_uint(f0.w);
+            const float sx = __uint_as_float((bits & 0xFFu) << 23), sy = __uint_as_float(((bits >> 8) & 0xFFu) << 23);
+            const float sz = __uint_as_float(((bits >> 16) & 0xFFu) << 23);
+            const uint32_t mask = bits >> 24;
+            const float Ax = sx * p.Ix, Ay = sy * p.Iy, Az = sz * p.Iz;
+            const float px = f0.x * p.Ix, py = f0.y * p.Iy, pz = f0.z * p.Iz;
+            const float ex = fabsf(px) * 0x1p-22f * sgx, ey = fabsf(py) * 0x1p-22f * sgy, ez = fabsf(pz) * 0x1p-22f * sgz;
+            const float Blx = fmaf(f0.x, p.Ix, p.clx) - ex, Bhx = fmaf(f0.x, p.Ix, p.chx) + ex;
+            const float Bly = fmaf(f0.y, p.Iy, p.cly) - ey, Bhy = fmaf(f0.y, p.Iy, p.chy) + ey;
+            const float Blz = fmaf(f0.z, p.Iz, p.clz) - ez, Bhz = fmaf(f0.z, p.Iz, p.chz) + ez;
+            const float lim = h.t;
+            float t[4];
+            int32_t rf[4] = {q1.z, q1.w, q2.x, q2.y};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float ax = fmaf(byte_f((uint32_t)q0.x, k), Ax, Blx), bx = fmaf(byte_f((uint32_t)q0.y, k), Ax, Bhx);
+                const float ay = fmaf(byte_f((uint32_t)q0.z, k), Ay, Bly), by = fmaf(byte_f((uint32_t)q0.w, k), Ay, Bhy);
+                const float az = fmaf(byte_f((uint32_t)q1.x, k), Az, Blz), bz = fmaf(byte_f((uint32_t)q1.y, k), Az, Bhz);
+                const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
+                const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), lim));
+                t[k] = ((mask >> k) & 1u) && tn <= tf * kExpand ? tn : INFINITY;
+            }
+            cswap(t[0], rf[0], t[1], rf[1]);
+            cswap(t[2], rf[2], t[3], rf[3]);
+            cswap(t[0], rf[0], t[2], rf[2]);
+            cswap(t[1], rf[1], t[3], rf[3]);
+            cswap(t[1], rf[1], t[2], rf[2]);
+            if (t[3] != INFINITY) st_ref[sp] = rf[3], st_t[sp] = t[3], ++sp;
+            if (t[2] != INFINITY) st_ref[sp] = rf[2], st_t[sp] = t[2], ++sp;
+            if (t[1] != INFINITY) st_ref[sp] = rf[1], st_t[sp] = t[1], ++sp;
+            cur = t[0] != INFINITY ? rf[0] : pop();
+            if (cur < 0 && leaf == 0) {
+                leaf = cur;
+                cur = pop();
+            }
+            if (!__any_sync(__activemask(), leaf == 0)) break;
+        }
+        while (leaf < 0) {
+            const int32_t v = ~leaf;
+            const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
+            for (int32_t k = first; k < first + cnt; ++k) {
+                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+                const int32_t id = __float_as_int(a.w);
+                if (kCount) ++h.tris;
+                float tt;
+                if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, tt)) {
+                    h.t = tt;
+                    h.id = id;
+                }
+            }
+            leaf = 0;
+            if (cur < 0) {
+                leaf = cur;
+                cur = pop();
+            }
+        }
+        if (cur == kDone) break;
+    }
+    return h;
+}
+
 // Packet traversal for coherent pattern tiles (all 32 rays of a warp share the pose origin and
 // span ~1.5 degrees): the warp walks ONE node sequence — it descends into a child if any lane's ray
 // enters it within that lane's [t_min, t*] — so every node and triangle fetch is a broadcast and
@@ -564,7 +658,7 @@ struct RaysGen {
 #ifndef FGL_CAST_MINBLOCKS
 #define FGL_CAST_MINBLOCKS 8
 #endif
-enum TraversalMode { kRay2 = 0, kPacket2 = 1, kRay4 = 2 };
+enum TraversalMode { kRay2 = 0, kPacket2 = 1, kRay4 = 2, kRay4Q = 3 };
 
 template <class Gen, bool kCount, int kMode>
 __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
@@ -589,7 +683,9 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
             Hit h = trace_packet<kCount>(sv, r, tmin, tmax, sref);
             if (valid) write_out(out, idx, r, h);
         } else if (valid) {
-            Hit h = kMode == kRay4 ? trace4<kCount>(sv, r, tmin, tmax) : trace<kCount>(sv, r, tmin, tmax);
+            Hit h = kMode == kRay4Q ? trace4q<kCount>(sv, r, tmin, tmax)
+                    : kMode == kRay4 ? trace4<kCount>(sv, r, tmin, tmax)
+                                     : trace<kCount>(sv, r, tmin, tmax);
             write_out(out, idx, r, h);
         }
     }
@@ -769,7 +865,9 @@ void launch_one(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastO
 template <class Gen, bool kCount>
 void launch_mode(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
                  cudaStream_t s) {
-    if (sv.width == 4)
+    if (sv.width == 4 && sv.quantized)
+        launch_one<Gen, kCount, kRay4Q>(sv, gen, ntiles, o, ctr, s);
+    else if (sv.width == 4)
         launch_one<Gen, kCount, kRay4>(sv, gen, ntiles, o, ctr, s);
     else if (Gen::kCoherent && packet_mode())
         launch_one<Gen, kCount, kPacket2>(sv, gen, ntiles, o, ctr, s);

@@ -49,6 +49,14 @@ struct __align__(16) Node128 {
     int4 ref;
     int4 meta;
 };
+// 4-wide node with 8-bit child boxes ("node64q"): f0 = (origin p = union lo .xyz,
+// bits: e_x | e_y << 8 | e_z << 16 | valid-child mask << 24), q0 = (lo.x bytes, hi.x bytes, lo.y,
+// hi.y) (child k in byte k), q1 = (lo.z, hi.z, ref0, ref1), q2 = (ref2, ref3, 0, 0). Child planes
+// p + q 2^(e-127), quantised outward (floor of the round-down offset / ceil of the round-up one).
+struct __align__(16) NodeQ {
+    float4 f0;
+    int4 q0, q1, q2;
+};
 constexpr float kFarBox = 3.0e38f;  // empty child: a degenerate box no ray with t <= t_max reaches
 constexpr int32_t kEmptyRef = INT32_MIN;
 constexpr int kLeafShift = 3;
@@ -89,7 +97,8 @@ struct BuildBuffers {
     float4 *nodebox = nullptr;     // [2(T-1)]
     float4 *agg = nullptr;         // 8-ary box aggregates, level after level (unions of 8^k leaves)
     Node64 *nodes = nullptr;       // [max(T-1,1)]
-    Node128 *nodes4 = nullptr;     // [max(T-1,1)]
+    Node128 *nodes4 = nullptr;     // [max(T-1,1)] node128, or node64q (stride 64 B) when quantized
+    int quantized = 0;
     int32_t *depth = nullptr;      // [T-1]
     int width = 4;
     int sorted_slot = 0;           // which keys/vals buffer holds the sorted result
@@ -107,7 +116,7 @@ void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *g
 
 // build.cu
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  int cubic, int width, cudaStream_t s);
+                  int cubic, int width, int quantized, cudaStream_t s);
 void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
                      cudaStream_t s);
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
@@ -146,6 +155,7 @@ struct SceneView {
     const Node64 *nodes;
     const Node128 *nodes4;
     int width;
+    int quantized;
 };
 void launch_cast_spinning(const SceneView &sv, const SpinParams &p, const float *poses, int64_t P, const CastOut &o,
                           CastCounter *ctr, cudaStream_t s);

@@ -71,6 +71,50 @@ def _depth_oracle(child, n):
     return d
 
 
+def _check_nodes4q(g, o, m, T, leaf_size):
+    """8-bit quantised 4-wide nodes (node64q): decoded child boxes contain the exact union of their
+    triangles (outward rounding) and are at most one quantum (+ rounding) larger per side."""
+    raw = g["nodes4"].view(np.uint8).reshape(-1)
+    V = m.verts[m.tris[o["perm"]]]
+    cover = np.zeros(T, np.int32)
+    stack = [0]
+    while stack:
+        i = stack.pop()
+        rec = raw[64 * i:64 * (i + 1)]
+        f0 = rec[:16].view(np.float32)
+        bits = int(rec[12:16].view(np.uint32)[0])
+        q0 = rec[16:32].view(np.uint32)
+        q1 = rec[32:48].view(np.int32)
+        q2 = rec[48:64].view(np.int32)
+        mask = bits >> 24
+        scale = [2.0 ** (((bits >> (8 * a)) & 0xFF) - 127) for a in range(3)]
+        qwords = [int(q0[0]), int(q0[1]), int(q0[2]), int(q0[3]), int(q1[0]) & 0xFFFFFFFF, int(q1[1]) & 0xFFFFFFFF]
+        refs = [int(q1[2]), int(q1[3]), int(q2[0]), int(q2[1])]
+        for k in range(4):
+            if not (mask >> k) & 1:
+                assert refs[k] == -2 ** 31
+                continue
+            ref = refs[k]
+            if ref >= 0:
+                fr, l = o["range"][ref]
+                c = l - fr + 1
+                stack.append(ref)
+            else:
+                v = ~ref
+                fr, c = v >> 3, (v & 7) + 1
+                cover[fr:fr + c] += 1
+            sub = V[fr:fr + c].reshape(-1, 3).astype(np.float64)
+            for a in range(3):
+                qlo = (qwords[2 * a] >> (8 * k)) & 0xFF
+                qhi = (qwords[2 * a + 1] >> (8 * k)) & 0xFF
+                lo = float(f0[a]) + qlo * scale[a]
+                hi = float(f0[a]) + qhi * scale[a]
+                assert lo <= sub[:, a].min() and hi >= sub[:, a].max()       # conservative
+                assert sub[:, a].min() - lo <= scale[a] * 1.001 + 1e-30       # tight (one quantum)
+                assert hi - sub[:, a].max() <= scale[a] * 1.001 + 1e-30
+    assert np.all(cover == 1)
+
+
 def _check_nodes4(g, o, m, T, leaf_size):
     """4-wide nodes (DESIGN.md §5 node128): walk from the root; every child box is the exact union
     of its triangles; leaves cover each sorted position once; internal children are the even-depth
@@ -108,11 +152,14 @@ def _check_nodes4(g, o, m, T, leaf_size):
 
 
 @pytest.mark.parametrize("name", ["tiny1", "tiny2", "dups", "c1", "soup"])
-@pytest.mark.parametrize("leaf_size,cubic,width,bits", [(1, 0, 2, 21), (4, 0, 2, 16), (8, 0, 2, 10), (4, 1, 2, 21),
-                                                        (2, 1, 2, 13), (2, 1, 4, 16), (1, 1, 4, 21), (5, 0, 4, 7)])
-def test_build_matches_oracle(fgl, name, leaf_size, cubic, width, bits):
+@pytest.mark.parametrize("leaf_size,cubic,width,bits,quant", [(1, 0, 2, 21, 0), (4, 0, 2, 16, 0), (8, 0, 2, 10, 0),
+                                                              (4, 1, 2, 21, 0), (2, 1, 2, 13, 0), (2, 1, 4, 16, 0),
+                                                              (1, 1, 4, 21, 0), (5, 0, 4, 7, 0), (2, 1, 4, 13, 1),
+                                                              (4, 0, 4, 21, 1)])
+def test_build_matches_oracle(fgl, name, leaf_size, cubic, width, bits, quant):
     m = _meshes()[name]
-    s = fgl.Scene(m.verts, m.tris, leaf_size=leaf_size, morton_box=0 if cubic else 1, width=width, morton_bits=bits)
+    s = fgl.Scene(m.verts, m.tris, leaf_size=leaf_size, morton_box=0 if cubic else 1, width=width, morton_bits=bits,
+                  quantized=quant)
     g = s.export()
     o = oracle.lbvh(m.verts, m.tris, bits=bits, cubic=bool(cubic))
     T = m.T
@@ -130,6 +177,10 @@ def test_build_matches_oracle(fgl, name, leaf_size, cubic, width, bits):
     assert np.array_equal(tri[:, 0, 3].view(np.int32), o["perm"].astype(np.int32))
     # traversal nodes: every reachable child box is the exact union of its triangles, leaves cover
     # every sorted position exactly once
+    if width == 4 and quant:
+        if T >= 2:
+            _check_nodes4q(g, o, m, T, leaf_size)
+        return
     if width == 4:
         _check_nodes4(g, o, m, T, leaf_size)
         return

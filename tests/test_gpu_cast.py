@@ -349,3 +349,16 @@ def test_rosette_ragged_frames(fgl, n):
                                  d.cpu().numpy().astype(np.float64), ros.t_min, ros.t_max)
     _assert_parity(v, res["range"].reshape(-1).cpu().numpy(), res["tri_id"].reshape(-1).cpu().numpy(),
                    label=f"rosette n={n}")
+
+
+@pytest.mark.parametrize("width,quant", [(4, 0), (4, 1)])
+def test_wide_and_quantized_nodes_cast_parity(fgl, width, quant):
+    """The 4-wide and the 8-bit quantised 4-wide node layouts (options) give the same answers."""
+    for name, kw in (("C1", {}), ("C2", {"poses": 2})):
+        cfg = _cfg(name, **kw)
+        s = fgl.Scene(cfg["mesh"].verts, cfg["mesh"].tris, width=width, quantized=quant)
+        res = s.cast(cfg["poses"], cfg["pattern"])
+        base = _scene(fgl, cfg["mesh"]).cast(cfg["poses"], cfg["pattern"])
+        o, d = fgl.export_rays(cfg["pattern"], cfg["poses"])
+        _agree_up_to_rounding(cfg["mesh"], o.cpu().numpy(), d.cpu().numpy(), cfg["pattern"].t_min, cfg["pattern"].t_max,
+                              res["range"], res["tri_id"], base["range"], base["tri_id"])
