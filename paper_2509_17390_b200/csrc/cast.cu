@@ -711,6 +711,34 @@ inline bool packet_mode() {
 // so a warp holds angular neighbours from at most two adjacent tiles. The traversal itself is the
 // while-while loop of `trace` (same slab and leaf tests, same (t, id) rule), executed one outer
 // iteration at a time so that the refill check runs between leaf batches.
+// Tile dispenser: a CTA takes FGL_CHUNK consecutive tiles from the global counter at a time and
+// its warps share them, so the warps of a CTA (and of an SM) trace neighbouring rays and reuse each
+// other's nodes in L1. FGL_CHUNK = 1 is the plain per-warp global counter.
+#ifndef FGL_CHUNK
+#define FGL_CHUNK 1
+#endif
+struct ChunkState {
+    unsigned long long base;
+    unsigned int pos;
+};
+__device__ __forceinline__ unsigned long long next_tile(CastCounter *ctr, ChunkState &c) {
+    if (FGL_CHUNK == 1) return atomicAdd(&ctr->next, 1ull);
+    while (true) {
+        const unsigned int k = atomicAdd(&c.pos, 1u);
+        if (k < FGL_CHUNK) {
+            __threadfence_block();
+            return *(volatile unsigned long long *)&c.base + k;
+        }
+        if (k == FGL_CHUNK) {  // this warp refills the chunk
+            *(volatile unsigned long long *)&c.base = atomicAdd(&ctr->next, (unsigned long long)FGL_CHUNK);
+            __threadfence_block();
+            atomicExch(&c.pos, 0u);
+        } else {
+            while (*(volatile unsigned int *)&c.pos >= FGL_CHUNK) __nanosleep(32);
+        }
+    }
+}
+
 #ifndef FGL_REFILL
 #define FGL_REFILL 32
 #endif
@@ -718,6 +746,9 @@ template <class Gen, bool kCount>
 __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
     k_cast_dyn(const SceneView sv, const Gen gen, int64_t ntiles, const CastOut out, CastCounter *ctr) {
     constexpr unsigned kFull = 0xffffffffu;
+    __shared__ ChunkState s_chunk;
+    if (threadIdx.x == 0) s_chunk.base = 0ull, s_chunk.pos = FGL_CHUNK;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     uint64_t st[kStack];  // (entry t bits << 32) | node ref
@@ -742,7 +773,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
             int slot = wpos + rank;
             if (need > avail) {
                 unsigned long long nt = 0;
-                if (lane == 0) nt = atomicAdd(&ctr->next, 1ull);
+                if (lane == 0) nt = next_tile(ctr, s_chunk);
                 nt = __shfl_sync(kFull, nt, 0);
                 if (rank >= avail) tile = nt, slot = rank - avail;
                 wtile = nt;
