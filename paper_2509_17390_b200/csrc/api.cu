@@ -6,6 +6,8 @@
 #include <string>
 
 #include "../../include/fgl.h"
+#include <vector>
+
 #include "fgl_internal.cuh"
 
 using fgl::Error;
@@ -599,16 +601,22 @@ fgl_status fgl_scene_export(const fgl_scene *s, const fgl_export *out, void *str
         if (dst && bytes) FGL_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
     };
     cp(out->scene_box, b.box, 6 * sizeof(float));
-    cp(out->sorted_keys, b.keys[b.sorted_slot], T * sizeof(uint64_t));
-    cp(out->perm, b.vals[b.sorted_slot], T * sizeof(uint32_t));
-    if (out->codes) {
+    if (out->sorted_keys || out->perm || out->codes) {
+        // sorted (code, index) pairs; packed keys hold code << packed_shift | index
+        std::vector<uint64_t> k(T);
+        std::vector<uint32_t> p(T);
+        cp(k.data(), b.keys[b.sorted_slot], T * sizeof(uint64_t));
+        if (b.packed_shift) {
+            const uint64_t mask = (uint64_t(1) << b.packed_shift) - 1;
+            for (int64_t j = 0; j < T; ++j) p[j] = (uint32_t)(k[j] & mask), k[j] >>= b.packed_shift;
+        } else {
+            cp(p.data(), b.vals[b.sorted_slot], T * sizeof(uint32_t));
+        }
+        if (out->sorted_keys) std::memcpy(out->sorted_keys, k.data(), T * sizeof(uint64_t));
+        if (out->perm) std::memcpy(out->perm, p.data(), T * sizeof(uint32_t));
         // input-order codes: codes[perm[j]] = sorted_keys[j] (a permutation of the sorted array)
-        std::string tmpk(T * sizeof(uint64_t), '\0'), tmpp(T * sizeof(uint32_t), '\0');
-        cp(&tmpk[0], b.keys[b.sorted_slot], T * sizeof(uint64_t));
-        cp(&tmpp[0], b.vals[b.sorted_slot], T * sizeof(uint32_t));
-        const uint64_t *k = (const uint64_t *)tmpk.data();
-        const uint32_t *p = (const uint32_t *)tmpp.data();
-        for (int64_t j = 0; j < T; ++j) out->codes[p[j]] = k[j];
+        if (out->codes)
+            for (int64_t j = 0; j < T; ++j) out->codes[p[j]] = k[j];
     }
     cp(out->child, b.child, nin * sizeof(int2));
     cp(out->range, b.range, nin * sizeof(int2));

@@ -13,6 +13,10 @@
 
 #include "fgl_internal.cuh"
 
+#ifndef FGL_SORT_PACKED
+#define FGL_SORT_PACKED 1
+#endif
+
 namespace fgl {
 
 namespace {
@@ -147,10 +151,11 @@ __device__ __forceinline__ uint64_t morton_code(const MortonBox &m, float x, flo
     return spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
 }
 
+// keys[k] = code (vals[k] = k), or packed (vals == nullptr): keys[k] = code << pshift | k
 __global__ void __launch_bounds__(256) k_morton(const float4 *__restrict__ cent, int64_t T,
                                                 const float *__restrict__ box, int bits, int cubic,
-                                                uint64_t *__restrict__ keys,
-                                                uint32_t *__restrict__ vals, uint32_t *__restrict__ ghist) {
+                                                uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                                                int pshift, uint32_t *__restrict__ ghist) {
     __shared__ uint32_t h[8][256];
     __shared__ MortonBox mb;
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&h[0][0])[i] = 0;
@@ -161,8 +166,12 @@ __global__ void __launch_bounds__(256) k_morton(const float4 *__restrict__ cent,
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < T; k += (int64_t)gridDim.x * blockDim.x) {
         float4 c = cent[k];
         uint64_t code = morton_code(m, c.x, c.y, c.z);
-        keys[k] = code;
-        vals[k] = (uint32_t)k;
+        if (vals) {
+            keys[k] = code;
+            vals[k] = (uint32_t)k;
+        } else {
+            keys[k] = code << pshift | (uint64_t)k;
+        }
         for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(code >> (8 * p)) & 0xFF], 1u);
     }
     __syncthreads();
@@ -185,11 +194,12 @@ __global__ void k_morton_points(const float *__restrict__ pts, int64_t n, BoxArg
 
 // LCP of augmented keys code_i || i (sorted position fallback for equal codes; R7); -1 outside.
 // ki = k[i] is passed in (loaded once per thread).
-__device__ __forceinline__ int delta(const uint64_t *__restrict__ k, int64_t n, int64_t i, uint64_t ki, int64_t j) {
-    if (j < 0 || j >= n) return -1;
-    const uint64_t b = __ldg(k + j);
-    if (ki != b) return __clzll((long long)(ki ^ b));
-    return 64 + __clz((int)((uint32_t)i ^ (uint32_t)j));
+// With packed keys (code << ks | index), ks strips the index: the tree is the same either way.
+// 32-bit positions (T < 2^30); one unsigned compare covers both ends of [0, n).
+__device__ __forceinline__ int delta(const uint64_t *__restrict__ k, int n, int i, uint64_t ki, int j, int ks) {
+    if ((unsigned)j >= (unsigned)n) return -1;
+    const uint64_t x = ki ^ (__ldg(k + j) >> ks);
+    return x ? __clzll((long long)x) : 64 + __clz(i ^ j);
 }
 
 constexpr float kInf = __builtin_huge_valf();
@@ -202,7 +212,7 @@ struct AggLevels {
     int nlev;
 };
 
-__device__ __forceinline__ void acc(float4 &lo, float4 &hi, const float4 *p, int64_t i) {
+__device__ __forceinline__ void acc(float4 &lo, float4 &hi, const float4 *p, int i) {
     const float4 l = __ldg(p + 2 * i), h = __ldg(p + 2 * i + 1);
     lo.x = fminf(lo.x, l.x), lo.y = fminf(lo.y, l.y), lo.z = fminf(lo.z, l.z);
     hi.x = fmaxf(hi.x, h.x), hi.y = fmaxf(hi.y, h.y), hi.z = fmaxf(hi.z, h.z);
@@ -211,23 +221,22 @@ __device__ __forceinline__ void acc(float4 &lo, float4 &hi, const float4 *p, int
 // Eq. 7 by its closed form: the box of a node covering sorted leaves [a, b] is the union of their
 // boxes (exact: min/max do not round). Evaluated with the 8-ary aggregates: at most 7 + 7 reads per
 // level (independent loads, unrolled), <= 8 at the top level.
-__device__ __forceinline__ void range_box(const AggLevels &L, int64_t a, int64_t b, float4 &lo, float4 &hi) {
+__device__ __forceinline__ void range_box(const AggLevels &L, int a, int b, float4 &lo, float4 &hi) {
     lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
-    int64_t A = a, B = b + 1;  // half-open, in units of the current level
-    int64_t cnt = L.n, off = -1;
+    int A = a, B = b + 1;  // half-open, in units of the current level
+    int cnt = (int)L.n, off = -1;
     for (int lv = 0; lv < L.nlev && A < B; ++lv) {
         const float4 *p = lv == 0 ? L.leaf : L.agg + 2 * off;
         off = lv == 0 ? 0 : off + cnt;
-        cnt = (cnt + 7) / 8;
+        cnt = (cnt + 7) >> 3;
         if (lv + 1 < L.nlev) {
-            const int64_t rem = B - A;
-            const int nf = (int)(((8 - (A & 7)) & 7) < rem ? ((8 - (A & 7)) & 7) : rem);
+            const int rem = B - A;
+            const int nf = min((8 - (A & 7)) & 7, rem);
 #pragma unroll
             for (int k = 0; k < 7; ++k)
                 if (k < nf) acc(lo, hi, p, A + k);
             A += nf;
-            const int64_t rem2 = B - A;
-            const int nb = (int)((B & 7) < rem2 ? (B & 7) : rem2);
+            const int nb = min(B & 7, B - A);
 #pragma unroll
             for (int k = 0; k < 7; ++k)
                 if (k < nb) acc(lo, hi, p, B - 1 - k);
@@ -242,33 +251,35 @@ __device__ __forceinline__ void range_box(const AggLevels &L, int64_t a, int64_t
 }
 
 // Karras 2012 (Eq. 6 read as the non-recursive LCP split, R7): one thread per internal node i
-__global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, int64_t n, int2 *__restrict__ child,
-                                                int2 *__restrict__ range, int32_t *__restrict__ parent, AggLevels L,
+__global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, int n, int ks,
+                                                int2 *__restrict__ child, int2 *__restrict__ range,
+                                                int32_t *__restrict__ parent, AggLevels L,
                                                 float4 *__restrict__ nodebox) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t ki = __ldg(k + i);
-        const int d = (delta(k, n, i, ki, i + 1) - delta(k, n, i, ki, i - 1)) >= 0 ? 1 : -1;
-        const int dmin = delta(k, n, i, ki, i - d);
-        int64_t lmax = 2;
-        while (delta(k, n, i, ki, i + lmax * d) > dmin) lmax <<= 1;
-        int64_t l = 0;
-        for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
-            if (delta(k, n, i, ki, i + (l + t) * d) > dmin) l += t;
-        const int64_t j = i + l * d;
-        const int dnode = delta(k, n, i, ki, j);
-        int64_t s = 0, t = l;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;  // one thread per internal node
+    if (i < n - 1) {
+        const uint64_t ki = __ldg(k + i) >> ks;
+        const int d = (delta(k, n, i, ki, i + 1, ks) - delta(k, n, i, ki, i - 1, ks)) >= 0 ? 1 : -1;
+        const int dmin = delta(k, n, i, ki, i - d, ks);
+        int lmax = 2;
+        while (delta(k, n, i, ki, i + lmax * d, ks) > dmin) lmax <<= 1;
+        int l = 0;
+        for (int t = lmax >> 1; t >= 1; t >>= 1)
+            if (delta(k, n, i, ki, i + (l + t) * d, ks) > dmin) l += t;
+        const int j = i + l * d;
+        const int dnode = delta(k, n, i, ki, j, ks);
+        int s = 0, t = l;
         do {
             t = (t + 1) >> 1;
-            if (delta(k, n, i, ki, i + (s + t) * d) > dnode) s += t;
+            if (delta(k, n, i, ki, i + (s + t) * d, ks) > dnode) s += t;
         } while (t > 1);
-        const int64_t g = i + s * d + (d < 0 ? -1 : 0);
-        const int64_t f = i < j ? i : j, last = i < j ? j : i;
-        int32_t left = f == g ? ~(int32_t)g : (int32_t)g;
-        int32_t right = last == g + 1 ? ~(int32_t)(g + 1) : (int32_t)(g + 1);
+        const int g = i + s * d + (d < 0 ? -1 : 0);
+        const int f = i < j ? i : j, last = i < j ? j : i;
+        int32_t left = f == g ? ~g : g;
+        int32_t right = last == g + 1 ? ~(g + 1) : g + 1;
         child[i] = make_int2(left, right);
-        range[i] = make_int2((int32_t)f, (int32_t)last);
-        parent[left >= 0 ? left : (n - 1) + ~left] = (int32_t)i;
-        parent[right >= 0 ? right : (n - 1) + ~right] = (int32_t)i;
+        range[i] = make_int2(f, last);
+        parent[left >= 0 ? left : (n - 1) + ~left] = i;
+        parent[right >= 0 ? right : (n - 1) + ~right] = i;
         if (i == 0) parent[0] = -1;
         // Eq. 7 box of this node by its closed form (exact union of its leaf range)
         float4 lo, hi;
@@ -294,13 +305,14 @@ __device__ __forceinline__ void warp_union(float4 &lo, float4 &hi) {
 
 __global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts, int64_t V,
                                                  const int32_t *__restrict__ tris,
-                                                 const uint32_t *__restrict__ perm, int64_t n,
+                                                 const uint32_t *__restrict__ perm,
+                                                 const uint64_t *__restrict__ pkeys, uint64_t pmask, int64_t n,
                                                  float4 *__restrict__ tri, float4 *__restrict__ leafbox,
                                                  float4 *__restrict__ agg) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     float4 lo = make_float4(kInf, kInf, kInf, 0.f), hi = make_float4(-kInf, -kInf, -kInf, 0.f);
     if (j < n) {
-        const uint32_t k = perm[j];
+        const uint32_t k = perm ? perm[j] : (uint32_t)(pkeys[j] & pmask);
         const float3 a = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k), V)),
                      b = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 1), V)),
                      c = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 2), V));
@@ -538,14 +550,22 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
     k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
     FGL_LAUNCHED("k_prep");
     FGL_CUDA(cudaMemsetAsync(b.ghist, 0, sizeof(uint32_t) * 8 * 256, s));
-    k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, cubic, b.keys[0], b.vals[0], b.ghist);
+    // key-only sort when the triangle index fits below the code: (code << ib) | index sorts like the
+    // stable (code, index) pairs and moves 8 instead of 12 bytes per key and pass
+    int ib = 1;
+    while ((int64_t(1) << ib) < T) ++ib;
+    const int ps = (FGL_SORT_PACKED && key_bits + ib <= 64) ? ib : 0;
+    b.packed_shift = ps;
+    k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, cubic, b.keys[0], ps ? nullptr : b.vals[0],
+                                                       ps, b.ghist);
     FGL_LAUNCHED("k_morton");
     int slot = 0;
-    radix_sort_pairs(b.keys[0], b.vals[0], b.keys[1], b.vals[1], T, key_bits, b.sort_status, b.sort_tiles, b.ghist, true,
-                     &b.sort_epoch, &slot, s);
+    radix_sort_pairs(b.keys[0], ps ? nullptr : b.vals[0], b.keys[1], ps ? nullptr : b.vals[1], T, key_bits,
+                     b.sort_status, b.sort_tiles, b.ghist, true, &b.sort_epoch, &slot, s, ps);
     b.sorted_slot = slot;
-    // leaf-order records, leaf boxes and the 32-ary box aggregates used by the refit
-    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, b.vals[slot], T, b.tri, b.leafbox, b.agg);
+    // leaf-order records, leaf boxes and the 8-ary box aggregates used by the Eq. 7 boxes
+    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
+                                                          ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox, b.agg);
     FGL_LAUNCHED("k_reorder");
     AggLevels L;
     L.leaf = b.leafbox;
@@ -567,7 +587,7 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
         }
         return;
     }
-    k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[slot], T, b.child, b.range, b.parent, L,
+    k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[slot], (int)T, ps, b.child, b.range, b.parent, L,
                                                             b.nodebox);
     FGL_LAUNCHED("k_karras");
     if (width == 2) {

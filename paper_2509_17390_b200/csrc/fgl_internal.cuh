@@ -102,6 +102,7 @@ struct BuildBuffers {
     int32_t *depth = nullptr;      // [T-1]
     int width = 4;
     int sorted_slot = 0;           // which keys/vals buffer holds the sorted result
+    int packed_shift = 0;          // > 0: keys hold (code << packed_shift) | triangle index, no vals
 };
 
 constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
@@ -111,8 +112,10 @@ constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
 int sort_tile_blocks(int64_t n);
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
                       uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready, uint32_t *epoch,
-                      int *result_slot, cudaStream_t s);
-void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s);
+                      int *result_slot, cudaStream_t s, int shift0 = 0);  // vals0 == nullptr: key-only passes
+                                                                          // over bits [shift0, shift0 + key_bits)
+void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s,
+                      int shift0 = 0);
 
 // build.cu
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,

@@ -20,22 +20,27 @@ namespace {
 #endif
 constexpr int kThreads = FGL_SORT_THREADS;      // >= 256: one look-back thread per digit
 constexpr int kWarps = kThreads / 32;
-#ifndef FGL_SORT_ITEMS
-#define FGL_SORT_ITEMS 16
+#ifndef FGL_SORT_ITEMS_KV
+#define FGL_SORT_ITEMS_KV 8
 #endif
-constexpr int kItems = FGL_SORT_ITEMS;          // keys per thread (large sorts: kItemsLarge)
-constexpr int kTile = kThreads * kItems;        // keys per tile (sizes the status array)
-constexpr int kItemsLarge = 8;                  // >= 4 M keys: smaller tiles, 64 registers, 2x occupancy
-constexpr int64_t kLargeSort = int64_t(1) << 22;
+#ifndef FGL_SORT_ITEMS_K
+#define FGL_SORT_ITEMS_K 12
+#endif
+#ifndef FGL_SORT_BACKOFF
+#define FGL_SORT_BACKOFF 0
+#endif
+constexpr int kItemsKV = FGL_SORT_ITEMS_KV;     // keys per thread, key-value passes (34 KB shared)
+constexpr int kItemsK = FGL_SORT_ITEMS_K;       // keys per thread, key-only passes (33 KB shared)
+constexpr int kMinTile = kThreads * (kItemsKV < kItemsK ? kItemsKV : kItemsK);  // sizes the status array
 constexpr uint64_t kAgg = 1ull << 30, kPrefix = 2ull << 30, kValMask = (1ull << 30) - 1;
 
 __global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t *__restrict__ keys, int64_t n, int npass,
-                                                         uint32_t *__restrict__ ghist) {
+                                                         int shift0, uint32_t *__restrict__ ghist) {
     __shared__ uint32_t h[8][256];
     for (int i = threadIdx.x; i < 8 * 256; i += kThreads) (&h[0][0])[i] = 0;
     __syncthreads();
     for (int64_t i = blockIdx.x * (int64_t)kThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kThreads) {
-        uint64_t k = keys[i];
+        uint64_t k = keys[i] >> shift0;
         for (int p = 0; p < npass; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xFF], 1u);
     }
     __syncthreads();
@@ -45,22 +50,31 @@ __global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t *__restr
     }
 }
 
-template <int kIt>
-__global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restrict__ kin,
-                                                       const uint32_t *__restrict__ vin, uint64_t *__restrict__ kout,
-                                                       uint32_t *__restrict__ vout, int64_t n, int shift,
-                                                       const uint32_t *__restrict__ hist, uint64_t *status,
-                                                       uint32_t *tile_ctr, uint32_t epoch) {
+// One digit pass over one tile of kThreads * kIt keys (values optional: kVals = false sorts keys
+// that carry their payload in the low bits). Ranking is per warp (match_any + per-warp digit
+// counters, warps in key order); the ranked tile is staged in shared memory in digit order so the
+// global scatter writes runs of equal digits from consecutive threads (coalesced), after the
+// decoupled look-back has produced each digit's global offset.
+template <int kIt, bool kVals>
+__global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__restrict__ kin,
+                                                          const uint32_t *__restrict__ vin,
+                                                          uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
+                                                          int64_t n, int shift, const uint32_t *__restrict__ hist,
+                                                          uint64_t *status, uint32_t *tile_ctr, uint32_t epoch) {
+    static_assert(kThreads == 256, "one thread per digit");
+    constexpr int kT = kThreads * kIt, kSpan = kT / kWarps;
     __shared__ uint32_t wh[kWarps][256];
-    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_base[256];   // global start of each digit in this pass's output
+    __shared__ uint32_t s_tstart[256];  // start of each digit in the tile's staged (sorted) order
     __shared__ uint32_t s_wsum[kWarps];
     __shared__ uint32_t s_tile;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ uint64_t s_key[kT];
+    __shared__ uint32_t s_val[kVals ? kT : 1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, d = threadIdx.x;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
     for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&wh[0][0])[i] = 0;
-    // global base of each digit: exclusive scan of this pass's histogram
-    {
-        const uint32_t v = threadIdx.x < 256 ? hist[threadIdx.x] : 0u;
+    // block-wide exclusive scan over the 256 digits (one value per thread)
+    auto scan256 = [&](uint32_t v) -> uint32_t {
         uint32_t x = v;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -70,127 +84,139 @@ __global__ void __launch_bounds__(kThreads) k_onesweep(const uint64_t *__restric
         __syncthreads();
         uint32_t off = 0;
         for (int ww = 0; ww < w; ++ww) off += s_wsum[ww];
-        if (threadIdx.x < 256) s_base[threadIdx.x] = off + x - v;
-    }
-    __syncthreads();
+        __syncthreads();  // s_wsum may be reused by the next scan
+        return off + x - v;
+    };
+    s_base[d] = scan256(hist[d]);  // digit bases from the all-pass histogram
     const uint32_t tile = s_tile;
     const uint32_t lt = (1u << lane) - 1u;
-    constexpr int kT = kThreads * kIt, kSpan = kT / kWarps;
     const int64_t base = (int64_t)tile * kT + (int64_t)w * kSpan;
     uint64_t key[kIt];
-    uint32_t val[kIt];
+    uint32_t val[kVals ? kIt : 1];
     uint32_t rank[kIt];
 #pragma unroll
     for (int i = 0; i < kIt; ++i) {
         const int64_t idx = base + i * 32 + lane;
         const bool ok = idx < n;
         key[i] = ok ? kin[idx] : 0ull;
-        val[i] = ok ? vin[idx] : 0u;
-        const uint32_t d = ok ? (uint32_t)((key[i] >> shift) & 0xFF) : 256u + lane;  // invalid lanes match nobody
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t before = ok ? wh[w][d] : 0u;
+        if constexpr (kVals) val[i] = ok ? vin[idx] : 0u;
+        const uint32_t dg = ok ? (uint32_t)((key[i] >> shift) & 0xFF) : 256u + lane;  // invalid lanes match nobody
+        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t before = ok ? wh[w][dg] : 0u;
         __syncwarp();
-        if (ok && (peers & lt) == 0) wh[w][d] = before + __popc(peers);
+        if (ok && (peers & lt) == 0) wh[w][dg] = before + __popc(peers);
         __syncwarp();
         rank[i] = before + __popc(peers & lt);
     }
     __syncthreads();
-    // per digit (one thread each): tile count, exclusive prefix over warps, decoupled look-back
-    if (threadIdx.x < 256) {
-        const int d = threadIdx.x;
-        uint32_t cnt = 0;
+    // per digit: tile count (published at once), exclusive prefix over warps, tile start
+    uint32_t cnt = 0;
 #pragma unroll
-        for (int ww = 0; ww < kWarps; ++ww) {
-            const uint32_t c = wh[ww][d];
-            wh[ww][d] = cnt;
-            cnt += c;
-        }
-        const uint64_t ep = (uint64_t)epoch << 32;
-        // status words carry their own payload, so relaxed (L2-coherent) accesses suffice
-        cuda::atomic_ref<uint64_t, cuda::thread_scope_device> mine(status[(int64_t)tile * 256 + d]);
-        uint32_t excl = 0;
-        if (tile == 0) {
-            mine.store(ep | kPrefix | cnt, cuda::std::memory_order_relaxed);
-        } else {
-            mine.store(ep | kAgg | cnt, cuda::std::memory_order_relaxed);
-            // look back kWin predecessors per round (independent loads in flight), accumulating
-            // published tile counts until the nearest published inclusive prefix
-            constexpr int kWin = 8;
-            int64_t t = (int64_t)tile - 1;
-            bool done = false;
-            while (!done) {
-                uint64_t v[kWin];
-#pragma unroll
-                for (int k = 0; k < kWin; ++k) {
-                    v[k] = 0;
-                    if (t - k >= 0) {
-                        cuda::atomic_ref<uint64_t, cuda::thread_scope_device> prev(status[(t - k) * 256 + d]);
-                        v[k] = prev.load(cuda::std::memory_order_relaxed);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < kWin; ++k) {
-                    if (done || t < 0) break;
-                    if ((v[k] >> 32) != epoch || (v[k] & (kAgg | kPrefix)) == 0) break;  // not yet: re-poll from t
-                    excl += (uint32_t)(v[k] & kValMask);
-                    if (v[k] & kPrefix) done = true;
-                    --t;
-                }
-                if (t < 0) done = true;
-            }
-            mine.store(ep | kPrefix | (excl + cnt), cuda::std::memory_order_relaxed);
-        }
-        s_base[d] += excl;
+    for (int ww = 0; ww < kWarps; ++ww) {
+        const uint32_t c = wh[ww][d];
+        wh[ww][d] = cnt;
+        cnt += c;
     }
+    const uint64_t ep = (uint64_t)epoch << 32;
+    // status words carry their own payload, so relaxed (L2-coherent) accesses suffice
+    cuda::atomic_ref<uint64_t, cuda::thread_scope_device> mine(status[(int64_t)tile * 256 + d]);
+    mine.store(ep | (tile == 0 ? kPrefix : kAgg) | cnt, cuda::std::memory_order_relaxed);
+    const uint32_t tstart = scan256(cnt);
+    s_tstart[d] = tstart;
+    // decoupled look-back: kWin predecessors per round (independent loads in flight), accumulating
+    // published tile counts until the nearest published inclusive prefix
+    uint32_t excl = 0;
+    if (tile != 0) {
+        constexpr int kWin = 8;
+        int64_t t = (int64_t)tile - 1;
+        bool done = false;
+        while (!done) {
+            uint64_t v[kWin];
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                v[k] = 0;
+                if (t - k >= 0) {
+                    cuda::atomic_ref<uint64_t, cuda::thread_scope_device> prev(status[(t - k) * 256 + d]);
+                    v[k] = prev.load(cuda::std::memory_order_relaxed);
+                }
+            }
+            const int64_t t0 = t;
+#pragma unroll
+            for (int k = 0; k < kWin; ++k) {
+                if (done || t < 0) break;
+                if ((v[k] >> 32) != epoch || (v[k] & (kAgg | kPrefix)) == 0) break;  // not yet: re-poll from t
+                excl += (uint32_t)(v[k] & kValMask);
+                if (v[k] & kPrefix) done = true;
+                --t;
+            }
+            if (t < 0) done = true;
+#if FGL_SORT_BACKOFF
+            if (!done && t == t0) __nanosleep(FGL_SORT_BACKOFF);  // predecessor not yet published: yield issue slots
+#endif
+        }
+        mine.store(ep | kPrefix | (excl + cnt), cuda::std::memory_order_relaxed);
+    }
+    s_base[d] += excl - tstart;  // global position = s_base[digit] + staged position
     __syncthreads();
+    // stage the tile in digit order
 #pragma unroll
     for (int i = 0; i < kIt; ++i) {
-        const int64_t idx = base + i * 32 + lane;
-        if (idx < n) {
-            const uint32_t d = (uint32_t)((key[i] >> shift) & 0xFF);
-            const uint32_t pos = s_base[d] + wh[w][d] + rank[i];
-            kout[pos] = key[i];
-            vout[pos] = val[i];
+        if (base + i * 32 + lane < n) {
+            const uint32_t dg = (uint32_t)((key[i] >> shift) & 0xFF);
+            const uint32_t lp = s_tstart[dg] + wh[w][dg] + rank[i];
+            s_key[lp] = key[i];
+            if constexpr (kVals) s_val[lp] = val[i];
         }
+    }
+    __syncthreads();
+    // coalesced scatter: consecutive threads write consecutive keys of a digit run
+    const int64_t rem = n - (int64_t)tile * kT;
+    const int valid = rem < kT ? (int)rem : kT;
+    for (int p = threadIdx.x; p < valid; p += kThreads) {
+        const uint64_t kk = s_key[p];
+        const uint32_t pos = s_base[(kk >> shift) & 0xFF] + p;
+        kout[pos] = kk;
+        if constexpr (kVals) vout[pos] = s_val[p];
     }
 }
 }  // namespace
 
-int sort_tile_blocks(int64_t n) {
-    const int64_t tile = n >= kLargeSort ? kThreads * kItemsLarge : kTile;
-    return (int)((n + tile - 1) / tile);
-}
+int sort_tile_blocks(int64_t n) { return (int)((n + kMinTile - 1) / kMinTile); }
 
-void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s) {
+void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s, int shift0) {
     int npass = (key_bits + 7) / 8;
     FGL_CUDA(cudaMemsetAsync(ghist, 0, sizeof(uint32_t) * 8 * 256, s));
     if (n <= 0) return;
     int blocks = (int)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 4);
-    k_digit_hist<<<blocks, kThreads, 0, s>>>(keys, n, npass, ghist);
+    k_digit_hist<<<blocks, kThreads, 0, s>>>(keys, n, npass, shift0, ghist);
     FGL_LAUNCHED("k_digit_hist");
 }
 
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
                       uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready, uint32_t *epoch,
-                      int *result_slot, cudaStream_t s) {
+                      int *result_slot, cudaStream_t s, int shift0) {
     *result_slot = 0;
     if (n <= 1) return;
     if (n >= (int64_t)kValMask) throw Error(1, "radix sort: n must be < 2^30");
-    if (!ghist_ready) digit_histograms(keys0, n, key_bits, ghist, s);
+    if (!ghist_ready) digit_histograms(keys0, n, key_bits, ghist, s, shift0);
     const int npass = (key_bits + 7) / 8;
-    const int nblk = sort_tile_blocks(n);
+    const bool kv = vals0 != nullptr;
+    const int64_t tile = (int64_t)kThreads * (kv ? kItemsKV : kItemsK);
+    const unsigned nblk = (unsigned)((n + tile - 1) / tile);
     FGL_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t) * 8, s));
     uint64_t *k[2] = {keys0, keys1};
     uint32_t *v[2] = {vals0, vals1};
     int cur = 0;
     for (int p = 0; p < npass; ++p) {
         if (++*epoch == 0) ++*epoch;  // epoch 0 marks never-written status words
-        if (n >= kLargeSort)
-            k_onesweep<kItemsLarge><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, 8 * p,
-                                                              ghist + 256 * p, status, tile_ctr + p, *epoch);
+        if (kv)
+            k_onesweep<kItemsKV, true><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n,
+                                                                 shift0 + 8 * p, ghist + 256 * p, status,
+                                                                 tile_ctr + p, *epoch);
         else
-            k_onesweep<kItems><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n, 8 * p,
-                                                         ghist + 256 * p, status, tile_ctr + p, *epoch);
+            k_onesweep<kItemsK, false><<<nblk, kThreads, 0, s>>>(k[cur], nullptr, k[cur ^ 1], nullptr, n,
+                                                                 shift0 + 8 * p, ghist + 256 * p, status,
+                                                                 tile_ctr + p, *epoch);
         FGL_LAUNCHED("k_onesweep");
         cur ^= 1;
     }
