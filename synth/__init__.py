@@ -23,7 +23,7 @@ __all__ = [
     "scene_c1", "scene_rooms", "scene_terrain", "Terrain",
     "Spinning", "Rosette", "spinning_preset", "rosette_default",
     "pose", "poses_yaw_offsets", "trajectory_rooms", "poses_terrain", "random_poses",
-    "config",
+    "config", "Gaussians", "gaussians_random", "gaussians_on_mesh", "Grid", "grid_for", "gauss_config",
 ]
 
 
@@ -595,4 +595,124 @@ def config(name: str, **kw):
         ter = scene_terrain(3)
         return dict(name="C5", mesh=ter.mesh, terrain=ter, pattern=spinning_preset("HDL64"),
                     poses=poses_terrain(ter, kw.get("poses", 4096), 5))
+    raise KeyError(name)
+
+
+# ----------------------------------------------------------------------------------------------
+# 3DGS inputs for the voxelizer (§III-A, §IV-A)
+# ----------------------------------------------------------------------------------------------
+# A pretrained 3DGS asset is {(mu_i, q_i, s_i, sigma_i)}: centre, unit quaternion
+# (w, x, y, z), per-axis scale (> 0) and opacity in (0, 1). No trained assets exist offline, so
+# these are seeded stand-ins with the statistics of splats fitted to surfaces: flat discs aligned
+# with the surface (two tangent scales of a few cm, one thin normal scale), log-normal sizes,
+# opacities spread over (0.05, 1). How (q, s) become a covariance, a box or a density is each
+# side's own business; this module only draws the parameters.
+@dataclass
+class Gaussians:
+    mu: np.ndarray       # float32 [N][3]
+    quat: np.ndarray     # float32 [N][4] (w, x, y, z), unit up to float32 rounding
+    scale: np.ndarray    # float32 [N][3] > 0
+    opacity: np.ndarray  # float32 [N] in (0, 1)
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def N(self) -> int:
+        return int(self.mu.shape[0])
+
+
+def _gs(mu, q, s, o, **meta) -> Gaussians:
+    f = lambda a: np.ascontiguousarray(a, dtype=np.float32)
+    return Gaussians(f(mu), f(q), f(s), f(o), dict(meta))
+
+
+def _unit_quats(rng, n):
+    q = rng.normal(size=(n, 4))
+    return q / np.linalg.norm(q, axis=1, keepdims=True)
+
+
+def gaussians_random(N: int, seed: int = 11, extent: float = 4.0, scale_median: float = 0.08,
+                     scale_sigma: float = 0.5) -> Gaussians:
+    """N Gaussians with uniform centres in [0, extent]^3, uniformly random orientations,
+    log-normal per-axis scales and opacities uniform in (0.05, 1)."""
+    rng = np.random.default_rng(seed)
+    mu = rng.uniform(0.0, extent, size=(N, 3))
+    q = _unit_quats(rng, N)
+    s = scale_median * np.exp(scale_sigma * rng.normal(size=(N, 3)))
+    o = rng.uniform(0.05, 1.0, size=N)
+    return _gs(mu, q, s, o, kind="random", seed=seed)
+
+
+def _quat_z_to(n):
+    """Unit quaternions (w, x, y, z) of the shortest rotation taking +z to the unit normals n."""
+    w = 1.0 + n[:, 2]
+    q = np.stack([w, -n[:, 1], n[:, 0], np.zeros_like(w)], axis=1)
+    flip = w < 1e-6  # n = -z: rotate by pi about x
+    q[flip] = (0.0, 1.0, 0.0, 0.0)
+    return q / np.linalg.norm(q, axis=1, keepdims=True)
+
+
+def _quat_mul(a, b):
+    w1, x1, y1, z1 = a.T
+    w2, x2, y2, z2 = b.T
+    return np.stack([w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2, w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+                     w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2, w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2], axis=1)
+
+
+def gaussians_on_mesh(mesh: Mesh, N: int, seed: int = 12, tangent_median: float = 0.03,
+                      normal_scale: float = 0.004, sigma: float = 0.4) -> Gaussians:
+    """N surface splats on `mesh`: triangles drawn by area, uniform points on them, the thin axis
+    (local z) along the face normal with a random spin about it, log-normal tangent scales."""
+    rng = np.random.default_rng(seed)
+    v = mesh.verts.astype(np.float64)
+    a, b, c = v[mesh.tris[:, 0]], v[mesh.tris[:, 1]], v[mesh.tris[:, 2]]
+    cr = np.cross(b - a, c - a)
+    area = 0.5 * np.linalg.norm(cr, axis=1)
+    k = rng.choice(mesh.T, size=N, p=area / area.sum())
+    r1, r2 = rng.uniform(size=N), rng.uniform(size=N)
+    sq = np.sqrt(r1)
+    mu = (1 - sq)[:, None] * a[k] + (sq * (1 - r2))[:, None] * b[k] + (sq * r2)[:, None] * c[k]
+    n = cr[k] / np.linalg.norm(cr[k], axis=1, keepdims=True)
+    spin = rng.uniform(0.0, 2 * np.pi, size=N)
+    qs = np.stack([np.cos(spin / 2), 0 * spin, 0 * spin, np.sin(spin / 2)], axis=1)
+    q = _quat_mul(_quat_z_to(n), qs)
+    st = tangent_median * np.exp(sigma * rng.normal(size=(N, 2)))
+    sn = normal_scale * np.exp(0.25 * rng.normal(size=(N, 1)))
+    o = rng.uniform(0.05, 1.0, size=N)
+    return _gs(mu, q, np.concatenate([st, sn], axis=1), o, kind="surface", seed=seed, mesh_T=mesh.T)
+
+
+@dataclass
+class Grid:
+    """Voxel lattice: centre of voxel (i, j, k) = origin + (i + 1/2, j + 1/2, k + 1/2) h."""
+    origin: tuple
+    h: float
+    dims: tuple  # (nx, ny, nz)
+
+    @property
+    def nvox(self) -> int:
+        return int(self.dims[0]) * int(self.dims[1]) * int(self.dims[2])
+
+
+def grid_for(g: Gaussians, cells: int = 512, pad: int = 1) -> Grid:
+    """Grid over the centres' bounding box, `cells` voxels along its longest axis, padded by `pad`
+    free voxels on every side (SPEC voxelizer defaults: extent / 512, one voxel of padding)."""
+    lo = g.mu.min(axis=0).astype(np.float64)
+    hi = g.mu.max(axis=0).astype(np.float64)
+    h = float(np.float32((hi - lo).max() / cells))
+    dims = tuple(int(np.ceil((hi[a] - lo[a]) / h)) + 2 * pad for a in range(3))
+    origin = tuple(float(np.float32(lo[a] - pad * h)) for a in range(3))
+    return Grid(origin, h, dims)
+
+
+def gauss_config(name: str):
+    """G1: 2 000 random Gaussians in a 4 m cube, 64^3 grid (oracle-sized). G2: 1 M surface splats
+    on the C2 rooms mesh, 512 voxels along the longest axis (the paper's scale: "millions of
+    primitives", P:130)."""
+    name = name.upper()
+    if name == "G1":
+        g = gaussians_random(2000, 11)
+        return dict(name="G1", gauss=g, grid=grid_for(g, 62), kappa=3.0, theta=0.5, tile=8)
+    if name == "G2":
+        g = gaussians_on_mesh(scene_rooms(2), 1_000_000, 12)
+        return dict(name="G2", gauss=g, grid=grid_for(g, 512), kappa=3.0, theta=0.5, tile=8)
     raise KeyError(name)
