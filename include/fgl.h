@@ -196,6 +196,44 @@ FGL_API fgl_status fgl_nearest(const fgl_scene *scene, const float *queries, int
 FGL_API fgl_status fgl_cloud_metrics(const float *d_ab, int64_t n_a, const float *d_ba, int64_t n_b, float tau,
                                      double *out, void *cuda_stream);
 
+/* ---- Gaussian -> occupancy (§IV-A) --------------- */
+/* Uploads a 3DGS cloud G = {(mu_i, q_i, s_i, sigma_i)}: mu [n][3], q [n][4] as (w, x, y,
+ * z) (normalised on the device), s [n][3] > 0 (activated scales), opacity [n] in [0, 1]
+ * (activated), all float32 in `ptr_kind` memory (FGL_HOST / FGL_DEVICE, | FGL_ASYNC as for
+ * upload_mesh). kappa >= 1 is the Eq. 4 padding factor (3 = the 3-sigma box). The
+ * scene then indexes the Gaussians with the LBVH (fgl_scene_build: Morton codes of mu_i, Eqs.
+ * 5-7, width 2, cubic box); it cannot be cast against. FGL_E_DATA: n = 0, non-finite mu / q,
+ * q = 0, scale <= 0 or opacity outside [0, 1]. */
+FGL_API fgl_status fgl_scene_upload_gaussians(fgl_scene *scene, const float *mu, const float *quat,
+                                              const float *scale, const float *opacity, int64_t n, float kappa,
+                                              int ptr_kind, void *cuda_stream);
+
+/* Voxel lattice: voxel (i, j, k) has centre origin + (i + 1/2, j + 1/2, k + 1/2) spacing. */
+typedef struct {
+    float origin[3];
+    float spacing;        /* h > 0                                                               */
+    int32_t dims[3];      /* nx, ny, nz >= 1, nx * ny * nz <= 2^31                               */
+    int32_t tile;         /* B of Eq. 8; 0 = default (8); only 8 is accepted                     */
+    float theta;          /* Eq. 10 threshold                                                    */
+    int32_t reserved[3];  /* must be zero                                                        */
+} fgl_grid;
+
+/* Voxelizes a built Gaussian scene on the caller's stream (no host sync):
+ *   Eq. 8  candidates of each B^3 tile = Gaussians whose Eq. 4 box meets the box of the tile's
+ *          voxel centres (a BVH overlap query);
+ *   Eq. 9  D(v) = sum over candidates of exp(-m^2 / 2) f(sigma), f(sigma) = sigma (R24), with
+ *          m^2 = (v - mu)^T Sigma^-1 (v - mu) and contributions beyond m^2 > kappa^2 dropped (R25,
+ *          so the result does not depend on B), float32 arithmetic;
+ *   Eq. 10 occupancy V = D > theta; Eqs. 11-12 interior = V and its 6 neighbours (outside the grid
+ *          = empty, R27), surface = V and not interior.
+ * Device outputs: density float [nz][ny][nx] (nullable); occupancy, surface, interior as bit
+ * volumes uint32 [nz][ny][ceil(nx / 32)] (bit b of word w = voxel x = 32 w + b; surface and
+ * interior nullable); counts int64 [4] (nullable) = {occupied voxels, surface voxels, evaluated
+ * (voxel, candidate) pairs, traversal-stack overflow flag (0 unless the result is incomplete)}.
+ * FGL_E_USAGE: not a built Gaussian scene, NULL occupancy, bad grid; FGL_E_RESOURCE: > 2^31 voxels. */
+FGL_API fgl_status fgl_voxelize(const fgl_scene *scene, const fgl_grid *grid, float *density, uint32_t *occupancy,
+                                uint32_t *surface, uint32_t *interior, int64_t *counts, void *cuda_stream);
+
 /* ---- LBVH internals, for parity tests (host destination pointers; each may be NULL) ----- */
 typedef struct {
     float *scene_box;      /* [6]  lo.xyz, hi.xyz                                              */

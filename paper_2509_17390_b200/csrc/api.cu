@@ -29,6 +29,11 @@ struct fgl_scene {
     std::atomic<uint32_t> slot{0};
     bool built = false;
     bool points = false;  // uploaded with fgl_scene_upload_points (degenerate triangles (i, i, i))
+    bool gauss = false;   // uploaded with fgl_scene_upload_gaussians (mu in verts, records in b.tri)
+    float kappa = 3.0f;
+    float *g_quat = nullptr, *g_scale = nullptr, *g_opac = nullptr;  // [cap_V][4], [cap_V][3], [cap_V]
+    unsigned long long *vox_counts = nullptr;                         // scratch when the caller passes none
+    unsigned int *vox_overflow = nullptr;
     int bits = 21, leaf_size = 4;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     size_t bytes = 0;
@@ -142,6 +147,11 @@ void check_built(const fgl_scene *s) {
     if (!s->built) throw Error(FGL_E_USAGE, "scene is not built (call fgl_scene_build first)");
 }
 
+void check_cast(const fgl_scene *s) {  // casts need a triangle (or point) scene
+    check_built(s);
+    if (s->gauss) throw Error(FGL_E_USAGE, "cannot cast rays against a Gaussian scene (use fgl_voxelize)");
+}
+
 fgl::SpinParams spin_params(const fgl_spinning *p) {
     if (!p) throw Error(FGL_E_USAGE, "pattern is NULL");
     if (p->channels < 1 || p->channels > 512) throw Error(FGL_E_USAGE, "channels must be in [1, 512]");
@@ -231,6 +241,9 @@ void fgl_scene_destroy(fgl_scene *s) {
     free_build(s);
     if (s->verts) cudaFree(s->verts);
     if (s->tris) cudaFree(s->tris);
+    for (void *p : {(void *)s->g_quat, (void *)s->g_scale, (void *)s->g_opac, (void *)s->vox_counts,
+                    (void *)s->vox_overflow})
+        if (p) cudaFree(p);
     if (s->counters) cudaFree(s->counters);
     if (s->vflag) cudaFree(s->vflag);
     if (s->hflag) cudaFreeHost(s->hflag);
@@ -269,6 +282,7 @@ fgl_status fgl_scene_upload_mesh(fgl_scene *s, const float *verts, int64_t V, co
     s->b.T = T;
     s->V = V, s->T = T;
     s->points = false;
+    s->gauss = false;
     cudaMemcpyKind kind = ptr_kind == FGL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     FGL_CUDA(cudaMemcpyAsync(s->verts, verts, sizeof(float) * 3 * V, kind, st));
     FGL_CUDA(cudaMemcpyAsync(s->tris, tris, sizeof(int32_t) * 3 * T, kind, st));
@@ -307,6 +321,7 @@ fgl_status fgl_scene_upload_points(fgl_scene *s, const float *xyz, int64_t n, in
     s->b.T = n;
     s->V = n, s->T = n;
     s->points = true;
+    s->gauss = false;
     FGL_CUDA(cudaMemcpyAsync(s->verts, xyz, sizeof(float) * 3 * n,
                              ptr_kind == FGL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
     fgl::launch_iota3(s->tris, n, st);
@@ -318,9 +333,98 @@ fgl_status fgl_scene_upload_points(fgl_scene *s, const float *xyz, int64_t n, in
     FGL_API_END
 }
 
-fgl_status fgl_nearest(const fgl_scene *s, const float *queries, int64_t m, float *dist, int32_t *idx, void *stream) {
+fgl_status fgl_scene_upload_gaussians(fgl_scene *s, const float *mu, const float *quat, const float *scale,
+                                      const float *opacity, int64_t n, float kappa, int ptr_kind, void *stream) {
+    FGL_API_BEGIN
+    if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
+    const bool async = (ptr_kind & FGL_ASYNC) != 0;
+    ptr_kind &= ~FGL_ASYNC;
+    if (ptr_kind != FGL_HOST && ptr_kind != FGL_DEVICE) throw Error(FGL_E_USAGE, "ptr_kind must be FGL_HOST or FGL_DEVICE");
+    if (n <= 0) throw Error(FGL_E_DATA, "Gaussian cloud is empty");
+    if (!mu || !quat || !scale || !opacity) throw Error(FGL_E_USAGE, "NULL parameter array");
+    if (n > fgl::kMaxTris) throw Error(FGL_E_USAGE, "too many Gaussians (n must be < 2^28)");
+    if (!(kappa >= 1.0f) || !std::isfinite(kappa)) throw Error(FGL_E_USAGE, "kappa must be finite and >= 1 (Eq. 4)");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    s->built = false;
+    if (n > s->cap_V || !s->g_quat) {
+        for (float **p : {&s->verts, &s->g_quat, &s->g_scale, &s->g_opac})
+            if (*p) cudaFree(*p), *p = nullptr;
+        const int64_t cap = std::max(n, s->cap_V);
+        FGL_CUDA(cudaMalloc((void **)&s->verts, sizeof(float) * 3 * cap));
+        FGL_CUDA(cudaMalloc((void **)&s->g_quat, sizeof(float) * 4 * cap));
+        FGL_CUDA(cudaMalloc((void **)&s->g_scale, sizeof(float) * 3 * cap));
+        FGL_CUDA(cudaMalloc((void **)&s->g_opac, sizeof(float) * cap));
+        s->cap_V = cap;
+    }
+    if (n > s->cap_T) {
+        if (s->tris) cudaFree(s->tris), s->tris = nullptr;
+        FGL_CUDA(cudaMalloc((void **)&s->tris, sizeof(int32_t) * 3 * n));
+        alloc_build(s, n);
+        s->cap_T = n;
+    }
+    s->b.T = n;
+    s->V = n, s->T = n;
+    s->points = false;
+    s->gauss = true;
+    s->kappa = kappa;
+    const cudaMemcpyKind kind = ptr_kind == FGL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    FGL_CUDA(cudaMemcpyAsync(s->verts, mu, sizeof(float) * 3 * n, kind, st));
+    FGL_CUDA(cudaMemcpyAsync(s->g_quat, quat, sizeof(float) * 4 * n, kind, st));
+    FGL_CUDA(cudaMemcpyAsync(s->g_scale, scale, sizeof(float) * 3 * n, kind, st));
+    FGL_CUDA(cudaMemcpyAsync(s->g_opac, opacity, sizeof(float) * n, kind, st));
+    FGL_CUDA(cudaMemsetAsync(s->vflag, 0, sizeof(unsigned int), st));
+    fgl::launch_gauss_prep(s->verts, s->g_quat, s->g_scale, s->g_opac, n, s->b, s->vflag, st);
+    if (async) return FGL_OK;
+    FGL_CUDA(cudaMemcpyAsync(s->hflag, s->vflag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    FGL_CUDA(cudaStreamSynchronize(st));
+    if (*s->hflag & 2u)
+        throw Error(FGL_E_DATA, "invalid Gaussian (non-finite mu / q, q = 0, scale <= 0 or opacity outside [0, 1])");
+    FGL_API_END
+}
+
+fgl_status fgl_voxelize(const fgl_scene *s, const fgl_grid *grid, float *density, uint32_t *occupancy,
+                        uint32_t *surface, uint32_t *interior, int64_t *counts, void *stream) {
     FGL_API_BEGIN
     check_built(s);
+    if (!s->gauss) throw Error(FGL_E_USAGE, "fgl_voxelize needs a Gaussian scene (fgl_scene_upload_gaussians)");
+    if (!grid) throw Error(FGL_E_USAGE, "grid is NULL");
+    if (!occupancy) throw Error(FGL_E_USAGE, "occupancy output is NULL");
+    if (!(grid->spacing > 0.f) || !std::isfinite(grid->spacing)) throw Error(FGL_E_USAGE, "spacing must be finite and > 0");
+    for (int a = 0; a < 3; ++a) {
+        if (!std::isfinite(grid->origin[a])) throw Error(FGL_E_USAGE, "origin must be finite");
+        if (grid->dims[a] < 1) throw Error(FGL_E_USAGE, "dims must be >= 1");
+    }
+    if ((int64_t)grid->dims[0] * grid->dims[1] * grid->dims[2] > (int64_t(1) << 31))
+        throw Error(FGL_E_RESOURCE, "grid exceeds 2^31 voxels: use a coarser spacing");
+    if (!std::isfinite(grid->theta)) throw Error(FGL_E_USAGE, "theta must be finite");
+    if (grid->tile != 0 && grid->tile != 8) throw Error(FGL_E_USAGE, "tile must be 0 (default) or 8");
+    for (int i = 0; i < 3; ++i)
+        if (grid->reserved[i]) throw Error(FGL_E_USAGE, "fgl_grid.reserved must be zero");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    auto *ms = const_cast<fgl_scene *>(s);
+    if (!ms->vox_counts) {
+        FGL_CUDA(cudaMalloc((void **)&ms->vox_counts, sizeof(unsigned long long) * 4));
+        FGL_CUDA(cudaMalloc((void **)&ms->vox_overflow, sizeof(unsigned int)));
+        FGL_CUDA(cudaMemset(ms->vox_overflow, 0, sizeof(unsigned int)));
+    }
+    unsigned long long *cnt = counts ? reinterpret_cast<unsigned long long *>(counts) : nullptr;
+    if (cnt) FGL_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * 4, st));
+    fgl::VoxGrid vg;
+    for (int a = 0; a < 3; ++a) vg.origin[a] = grid->origin[a], vg.dims[a] = grid->dims[a];
+    vg.h = grid->spacing;
+    vg.theta = grid->theta;
+    fgl::launch_voxelize(s->b, vg, s->kappa, density, occupancy, surface, interior, cnt, ms->vox_overflow, st);
+    if (cnt) {  // [3] = traversal-stack overflows (sticky per scene; 0 in any sane configuration)
+        FGL_CUDA(cudaMemcpyAsync(cnt + 3, ms->vox_overflow, sizeof(unsigned int), cudaMemcpyDeviceToDevice, st));
+    }
+    FGL_API_END
+}
+
+fgl_status fgl_nearest(const fgl_scene *s, const float *queries, int64_t m, float *dist, int32_t *idx, void *stream) {
+    FGL_API_BEGIN
+    check_cast(s);
     if (!s->points) throw Error(FGL_E_USAGE, "fgl_nearest needs a point scene (fgl_scene_upload_points)");
     if (m < 0) throw Error(FGL_E_USAGE, "m must be >= 0");
     if (m == 0) return FGL_OK;
@@ -386,7 +490,13 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     const bool timed = cap == cudaStreamCaptureStatusNone;  // build_ms is not recorded inside a graph
     if (timed) FGL_CUDA(cudaEventRecord(s->ev0, st));
     if (quant && width != 4) throw Error(FGL_E_USAGE, "quantized nodes need width 4");
-    fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, quant, st);
+    if (s->gauss) {
+        if (width != 2 || quant) throw Error(FGL_E_USAGE, "a Gaussian scene builds width-2 nodes only");
+        if (!cubic) throw Error(FGL_E_USAGE, "a Gaussian scene uses the cubic Morton box");
+        fgl::launch_gauss_build(s->verts, s->g_quat, s->g_scale, s->g_opac, s->kappa, s->b, bits, leaf, st);
+    } else {
+        fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, quant, st);
+    }
     if (timed) FGL_CUDA(cudaEventRecord(s->ev1, st));
     s->built = true;
     FGL_API_END
@@ -417,7 +527,7 @@ fgl_status fgl_cast_spinning(const fgl_scene *s, const fgl_spinning *pattern, co
                              float *range, int32_t *tri_id, float *hit_xyz, int32_t *node_counts, int32_t *tri_counts,
                              void *stream) {
     FGL_API_BEGIN
-    check_built(s);
+    check_cast(s);
     fgl::SpinParams sp = spin_params(pattern);
     if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
     if (P == 0) return FGL_OK;
@@ -432,7 +542,7 @@ fgl_status fgl_cast_rosette(const fgl_scene *s, const fgl_rosette *pattern, cons
                             int64_t first_frame, float *range, int32_t *tri_id, float *hit_xyz, int32_t *node_counts,
                             int32_t *tri_counts, void *stream) {
     FGL_API_BEGIN
-    check_built(s);
+    check_cast(s);
     fgl::RosetteParams rp = rosette_params(pattern, first_frame);
     if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
     if (P == 0) return FGL_OK;
@@ -446,7 +556,7 @@ fgl_status fgl_cast_rosette(const fgl_scene *s, const fgl_rosette *pattern, cons
 fgl_status fgl_cast_rays(const fgl_scene *s, const float *orig, const float *dir, int64_t R, float t_min, float t_max,
                          float *range, int32_t *tri_id, void *stream) {
     FGL_API_BEGIN
-    check_built(s);
+    check_cast(s);
     check_interval(t_min, t_max);
     if (R < 0) throw Error(FGL_E_USAGE, "R must be >= 0");
     if (R == 0) return FGL_OK;
@@ -477,7 +587,7 @@ fgl_status fgl_cast_spinning_gather_signal(const fgl_scene *s, const fgl_spinnin
                                            int32_t *const *tri_bufs, int32_t *const *flags, int32_t npeer,
                                            void *stream) {
     FGL_API_BEGIN
-    check_built(s);
+    check_cast(s);
     fgl::SpinParams sp = spin_params(pattern);
     if (P < 0 || first_pose < 0) throw Error(FGL_E_USAGE, "P and first_pose must be >= 0");
     if (npeer < 1 || npeer > fgl::kMaxPeers) throw Error(FGL_E_USAGE, "npeer must be in [1, 8]");

@@ -541,14 +541,11 @@ void launch_morton_points(const float *pts, int64_t n, const float *lo, const fl
     FGL_LAUNCHED("k_morton_points");
 }
 
-void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  int cubic, int width, int quantized, cudaStream_t s) {
-    b.width = width;
-    b.quantized = width == 4 ? quantized : 0;
+// Eq. 5 codes of b.cent within b.box, then the stable sort (A3-A4). Sets b.packed_shift and
+// b.sorted_slot; the leaf order is then perm_at(b, j).
+void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s) {
     const int64_t T = b.T;
     const int key_bits = 3 * bits;
-    k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
-    FGL_LAUNCHED("k_prep");
     FGL_CUDA(cudaMemsetAsync(b.ghist, 0, sizeof(uint32_t) * 8 * 256, s));
     // key-only sort when the triangle index fits below the code: (code << ib) | index sorts like the
     // stable (code, index) pairs and moves 8 instead of 12 bytes per key and pass
@@ -563,10 +560,14 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
     radix_sort_pairs(b.keys[0], ps ? nullptr : b.vals[0], b.keys[1], ps ? nullptr : b.vals[1], T, key_bits,
                      b.sort_status, b.sort_tiles, b.ghist, true, &b.sort_epoch, &slot, s, ps);
     b.sorted_slot = slot;
-    // leaf-order records, leaf boxes and the 8-ary box aggregates used by the Eq. 7 boxes
-    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
-                                                          ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox, b.agg);
-    FGL_LAUNCHED("k_reorder");
+}
+
+// Karras tree (A5), Eq. 7 boxes (A6) and traversal nodes (A7) from the leaf boxes and the first
+// aggregate level written by the primitive-specific reorder kernel.
+void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s) {
+    const int64_t T = b.T;
+    b.width = width;
+    b.quantized = width == 4 ? quantized : 0;
     AggLevels L;
     L.leaf = b.leafbox;
     L.agg = b.agg;
@@ -587,8 +588,8 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
         }
         return;
     }
-    k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[slot], (int)T, ps, b.child, b.range, b.parent, L,
-                                                            b.nodebox);
+    k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[b.sorted_slot], (int)T, b.packed_shift, b.child,
+                                                            b.range, b.parent, L, b.nodebox);
     FGL_LAUNCHED("k_karras");
     if (width == 2) {
         k_nodes<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.leafbox, b.nodebox,
@@ -602,6 +603,20 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
                                                  b.nodes4, b.quantized);
         FGL_LAUNCHED("k_nodes4");
     }
+}
+
+void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
+                  int cubic, int width, int quantized, cudaStream_t s) {
+    const int64_t T = b.T;
+    k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
+    FGL_LAUNCHED("k_prep");
+    launch_morton_sort(b, bits, cubic, s);
+    const int ps = b.packed_shift, slot = b.sorted_slot;
+    // leaf-order records, leaf boxes and the 8-ary box aggregates used by the Eq. 7 boxes
+    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
+                                                          ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox, b.agg);
+    FGL_LAUNCHED("k_reorder");
+    launch_tree(b, leaf_size, width, quantized, s);
 }
 
 }  // namespace fgl

@@ -122,6 +122,8 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
                   int cubic, int width, int quantized, cudaStream_t s);
 void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
                      cudaStream_t s);
+void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s);
+void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s);
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
                           uint64_t *codes, cudaStream_t s);
 
@@ -170,6 +172,20 @@ void launch_cast_bruteforce(const float *verts, int64_t V, const int32_t *tris, 
                             const float *dir,
                             int64_t R, float t_min, float t_max, float *range, int32_t *tri_id, cudaStream_t s);
 void launch_wait_flag(const int32_t *flag, int32_t target, cudaStream_t s);
+// gauss.cu
+struct VoxGrid {
+    double origin[3];
+    double h;
+    int dims[3];
+    float theta;
+};
+void launch_gauss_prep(const float *mu, const float *quat, const float *scale, const float *opac, int64_t n,
+                       BuildBuffers &b, unsigned int *flag, cudaStream_t s);
+void launch_gauss_build(const float *mu, const float *quat, const float *scale, const float *opac, float kappa,
+                        BuildBuffers &b, int bits, int leaf_size, cudaStream_t s);
+void launch_voxelize(const BuildBuffers &b, const VoxGrid &g, float kappa, float *density, uint32_t *occ,
+                     uint32_t *surf, uint32_t *inter, unsigned long long *counts, unsigned int *overflow,
+                     cudaStream_t s);
 // points.cu
 void launch_iota3(int32_t *tris, int64_t n, cudaStream_t s);
 void launch_nearest(const SceneView &sv, const float *q, int64_t m, float *dist, int32_t *idx, cudaStream_t s);

@@ -50,6 +50,11 @@ class RosetteC(Structure):
                 ("half_fov_deg", c_float), ("t_min", c_float), ("t_max", c_float)]
 
 
+class GridC(Structure):
+    _fields_ = [("origin", c_float * 3), ("spacing", c_float), ("dims", c_int32 * 3), ("tile", c_int32),
+                ("theta", c_float), ("reserved", c_int32 * 3)]
+
+
 class ExportC(Structure):
     _fields_ = [(n, c_void_p) for n in ("scene_box", "codes", "sorted_keys", "perm", "child", "range", "leaf_box",
                                         "node_box", "tri48", "nodes", "nodes4", "depth")]
@@ -83,6 +88,9 @@ _SIGS = {
     "fgl_scene_upload_points": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "fgl_nearest": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "fgl_cloud_metrics": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_float, c_void_p, c_void_p]),
+    "fgl_scene_upload_gaussians": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_float, c_int,
+                                           c_void_p]),
+    "fgl_voxelize": (c_int, [c_void_p, POINTER(GridC), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fgl_alloc": (c_int, [c_int, c_int64, POINTER(c_void_p)]),
     "fgl_free": (c_int, [c_void_p]),
     "fgl_ipc_get_handle": (c_int, [c_void_p, c_void_p]),
@@ -471,6 +479,93 @@ def cloud_metrics(a, b, tau: float, device=None, stream=None) -> dict:
     o = out.cpu().tolist()
     return dict(chamfer=o[0], precision=o[1], recall=o[2], fscore=o[3], n_a=int(o[4]), n_b=int(o[5]),
                 d_ab=d_ab, d_ba=d_ba)
+
+
+class GaussianScene:
+    """A 3DGS cloud on one GPU with its LBVH over the Eq. 4 boxes (§IV-A), for
+    voxelize() (Eqs. 8-12). mu [N][3], quat [N][4] (w, x, y, z), scale [N][3], opacity [N]: host
+    arrays or CUDA tensors (float32)."""
+
+    def __init__(self, mu, quat, scale, opacity, kappa: float = 3.0, device=None, build: bool = True,
+                 leaf_size: int = 2, morton_bits: int = 0, stream=None, sync: bool = True):
+        self.scene = Scene(device=device, build=False, leaf_size=leaf_size, width=2, morton_bits=morton_bits)
+        self.device = self.scene.device
+        self.kappa = float(kappa)
+        self.upload(mu, quat, scale, opacity, stream, sync)
+        if build:
+            self.build(stream)
+
+    def upload(self, mu, quat, scale, opacity, stream=None, sync: bool = True):
+        arrs = [mu, quat, scale, opacity]
+        on_dev = all(isinstance(a, torch.Tensor) and a.is_cuda for a in arrs)
+        if on_dev:
+            keep = [a.to(torch.float32).contiguous() for a in arrs]
+            ptrs = [a.data_ptr() for a in keep]
+            kind = DEVICE
+        else:
+            keep = [np.ascontiguousarray(np.asarray(a.cpu().numpy() if isinstance(a, torch.Tensor) else a,
+                                                    dtype=np.float32)) for a in arrs]
+            ptrs = [a.ctypes.data for a in keep]
+            kind = HOST
+        n = int(keep[3].size)
+        for a, w in zip(keep[:3], (3, 4, 3)):
+            if int(np.prod(a.shape)) != n * w:
+                raise ValueError("mu / quat / scale must be [N][3] / [N][4] / [N][3] with N = len(opacity)")
+        _check(lib().fgl_scene_upload_gaussians(self.scene._h, *ptrs, n, self.kappa, kind | (0 if sync else ASYNC),
+                                                _stream(stream)))
+        self._keep = keep  # host arrays must outlive an async upload
+        self.N = self.scene.T = n
+        return self
+
+    def build(self, stream=None):
+        self.scene.build(stream=stream)
+        return self
+
+    def check(self, stream=None):
+        self.scene.check(stream)
+        return self
+
+    def stats(self) -> dict:
+        return self.scene.stats()
+
+    def voxelize(self, origin, spacing: float, dims, theta: float, density: bool = False, masks: bool = True,
+                 counts: bool = True, out=None, stream=None) -> dict:
+        """Occupancy (Eq. 10) and, with masks, surface / interior (Eqs. 11-12) bit volumes uint32
+        [nz][ny][ceil(nx / 32)]; density float32 [nz][ny][nx] on request; counts int64 [4] =
+        (occupied, surface, evaluated pairs, overflow)."""
+        nx, ny, nz = (int(d) for d in dims)
+        nw = (nx + 31) // 32
+        dev = self.device
+        out = {} if out is None else out
+        occ = out.get("occupancy")
+        if occ is None:
+            occ = torch.empty((nz, ny, nw), dtype=torch.int32, device=dev)
+        dens = out.get("density")
+        if density and dens is None:
+            dens = torch.empty((nz, ny, nx), dtype=torch.float32, device=dev)
+        surf = inter = None
+        if masks:
+            surf = out.get("surface")
+            if surf is None:
+                surf = torch.empty((nz, ny, nw), dtype=torch.int32, device=dev)
+            inter = out.get("interior")
+            if inter is None:
+                inter = torch.empty((nz, ny, nw), dtype=torch.int32, device=dev)
+        cnt = out.get("counts")
+        if counts and cnt is None:
+            cnt = torch.empty(4, dtype=torch.int64, device=dev)
+        g = GridC((c_float * 3)(*[float(o) for o in origin]), float(spacing), (c_int32 * 3)(nx, ny, nz), 0,
+                  float(theta), (c_int32 * 3)())
+        _check(lib().fgl_voxelize(self.scene._h, ctypes.byref(g), _ptr(dens if density else None), occ.data_ptr(),
+                                  _ptr(surf), _ptr(inter), _ptr(cnt if counts else None), _stream(stream)))
+        res = dict(occupancy=occ)
+        if density:
+            res["density"] = dens
+        if masks:
+            res["surface"], res["interior"] = surf, inter
+        if counts:
+            res["counts"] = cnt
+        return res
 
 
 def kernel_launches() -> int:
