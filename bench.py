@@ -36,7 +36,8 @@ def _args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["fgl", "reference"], default="fgl")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "G1", "G2"],
+                    help="C1-C5: LiDAR cast (the north star); G1/G2: Gaussian voxelizer (NEXT-2)")
     ap.add_argument("--poses", type=int, default=None, help="poses per GPU per step")
     ap.add_argument("--mode", choices=["full", "cast"], default="full",
                     help="full = upload+build+cast per step (default); cast = cast only on a prebuilt scene")
@@ -239,8 +240,222 @@ def run_reference(a):
 
 
 # ----------------------------------------------------------------------------------------------
+# NEXT-2: Gaussian -> occupancy (§IV-A Eqs. 4-12). One step = async upload of the 3DGS
+# parameters + LBVH build over the Eq. 4 boxes + tiled voxelization (Eqs. 8-10) + masks (11-12).
+VOX_METRIC = "voxels/sec (3DGS voxelization: Eq. 4 boxes + LBVH + Eqs. 8-12 per step)"
+# algorithmic FP32 ops per (voxel, candidate) pair: d = v - mu (3), d^T A d in Horner form (6 FMA +
+# 3 MUL), the kappa test (1), exp2 (1), the weighted accumulation (1 FMA) = 15
+OPS_PAIR = 15
+
+
+def _vox_oracle(cfg, seconds: float, seed: int = 0):
+    """The oracle's Eq. 9 (density_at) on a bounded seeded sample of grid voxels."""
+    from oracle import gauss as og
+    g, grid = cfg["gauss"], cfg["grid"]
+    nx, ny, nz = grid.dims
+    rng = np.random.default_rng(seed)
+
+    def pts(n):
+        idx = rng.integers(0, grid.nvox, n)
+        k, rem = np.divmod(idx, nx * ny)
+        j, i = np.divmod(rem, nx)
+        o = np.asarray(grid.origin)
+        return np.stack([o[0] + (i + 0.5) * grid.h, o[1] + (j + 0.5) * grid.h, o[2] + (k + 0.5) * grid.h], axis=1)
+
+    t0 = time.perf_counter()
+    og.density_at(g, pts(8), cfg["kappa"])
+    per = (time.perf_counter() - t0) / 8
+    n = int(max(8, seconds / max(per, 1e-9)))
+    return n, pts, per
+
+
+def run_voxel(a):
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg = synth.gauss_config(a.config)
+    g, grid, kappa, theta = cfg["gauss"], cfg["grid"], cfg["kappa"], cfg["theta"]
+    wl = (f"{cfg['name']}: {g.meta.get('kind')} 3DGS cloud N={g.N}, grid {grid.dims[0]}x{grid.dims[1]}x"
+          f"{grid.dims[2]} (h={grid.h:.4f} m), kappa={kappa}, theta={theta}, tile 8^3")
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import gauss as og
+        n, pts, _ = _vox_oracle(cfg, 1.5)
+        for _ in range(a.warmup):
+            og.density_at(g, pts(n), kappa)
+        times = []
+        for _ in range(a.steps):
+            p = pts(n)
+            t0 = time.perf_counter()
+            og.density_at(g, p, kappa)
+            times.append(time.perf_counter() - t0)
+        ms = 1000 * statistics.mean(times)
+        v = n / (ms / 1000)
+        print(json.dumps({"metric": VOX_METRIC, "value": v, "unit": "voxels/s", "n_gpus": 0, "steps": a.steps,
+                          "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                          "config": {"workload": wl, "sample_voxels_per_step": n},
+                          "cpu_baseline": {"value": v, "unit": "voxels/s", "cores": 1, "kind": "oracle",
+                                           "sample": f"{n} seeded voxels per step, Eq. 9 over all {g.N} Gaussians"},
+                          "e2e": {"value": v, "unit": "voxels/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_17390_b200 as fgl
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl" if a.dist_backend == "nccl" else "gloo", device_id=dev
+                                if a.dist_backend == "nccl" else None)
+    # replicas only: each rank voxelizes its own copy of the cloud (DESIGN.md §8: the grid is one
+    # problem per scene; independent scenes shard across ranks with no exchange)
+    arrs = [torch.from_numpy(x).to(dev) for x in (g.mu, g.quat, g.scale, g.opacity)]
+    gs = fgl.GaussianScene(*arrs, kappa=kappa, device=dev)
+    stream = torch.cuda.current_stream()
+    nx, ny, nz = grid.dims
+    nw = (nx + 31) // 32
+    out = dict(occupancy=torch.empty((nz, ny, nw), dtype=torch.int32, device=dev),
+               surface=torch.empty((nz, ny, nw), dtype=torch.int32, device=dev),
+               interior=torch.empty((nz, ny, nw), dtype=torch.int32, device=dev),
+               counts=torch.empty(4, dtype=torch.int64, device=dev))
+    vev = None
+
+    def step():
+        gs.upload(*arrs, sync=False)
+        gs.build()
+        if vev is not None:
+            vev[0].record(stream)
+        gs.voxelize(grid.origin, grid.h, grid.dims, theta, out=out)
+        if vev is not None:
+            vev[1].record(stream)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    graph = None
+    if not a.no_graph:
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            step()
+        stream.wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        for _ in range(a.warmup):
+            graph.replay()
+    flush = None if a.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    K = a.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(K):
+            if flush is not None:
+                flush.zero_()
+            ev[i][0].record(stream)
+            graph.replay() if graph is not None else step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    gs.check()
+    ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    l0 = fgl.kernel_launches()
+    step()
+    launches = (fgl.kernel_launches() - l0) * K
+    # voxelize alone (events on the launch stream) for the roofline
+    vms = []
+    for _ in range(max(5, K)):
+        if flush is not None:
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gs.voxelize(grid.origin, grid.h, grid.dims, theta, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        vms.append(e0.elapsed_time(e1))
+    vms = statistics.mean(vms)
+    if world > 1:
+        t = torch.tensor([ms, vms], dtype=torch.float64, device=dev)
+        t = t.cpu() if a.dist_backend == "gloo" else t
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, vms = t.tolist()
+    c = out["counts"].cpu().tolist()
+    pairs = c[2]
+    alu_peak = _alu_peak_tops()
+    achieved = OPS_PAIR * pairs / (vms / 1000) / 1e12
+    # e2e: host (pinned) parameters in, occupancy bits + counts out, through the public API
+    e2e = None
+    if not a.no_e2e:
+        host = [torch.from_numpy(x).pin_memory() for x in (g.mu, g.quat, g.scale, g.opacity)]
+        occ_h = torch.empty((nz, ny, nw), dtype=torch.int32).pin_memory()
+        gs2 = fgl.GaussianScene(*host, kappa=kappa, device=dev)
+        res = {}
+
+        def e2e_step():
+            gs2.upload(*host, sync=False)
+            gs2.build()
+            r = gs2.voxelize(grid.origin, grid.h, grid.dims, theta, masks=True, out=res)
+            res.update(r)
+            occ_h.copy_(r["occupancy"], non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        ee = []
+        for _ in range(max(3, K // 2)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ee.append(e0.elapsed_time(e1))
+        ems = statistics.mean(ee)
+        e2e = {"value": grid.nvox * world / (ems / 1000), "unit": "voxels/s",
+               "h2d_bytes_per_step": int(sum(x.numel() * 4 for x in host)),
+               "d2h_bytes_per_step": int(occ_h.numel() * 4), "ms_per_step": ems}
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        from oracle import gauss as og
+        n, pts, _ = _vox_oracle(cfg, a.cpu_seconds)
+        p = pts(n)
+        t0 = time.perf_counter()
+        og.density_at(g, p, kappa)
+        dt = time.perf_counter() - t0
+        cpu = {"value": n / dt, "unit": "voxels/s", "cores": 1, "kind": "oracle",
+               "sample": f"{n} seeded voxels of {cfg['name']}, Eq. 9 over all {g.N} Gaussians (numpy, {dt:.1f} s)"}
+    if rank == 0:
+        st = gs.stats()
+        print(json.dumps({
+            "metric": VOX_METRIC, "value": grid.nvox * world / (ms / 1000), "unit": "voxels/s", "n_gpus": world,
+            "steps": K, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl, "step": "upload+build+voxelize+masks", "voxels": grid.nvox,
+                       "gaussians": g.N, "parallelism": f"replicas x{world}",
+                       "l2": "flushed between steps (256 MiB memset, untimed)" if flush is not None else "not flushed",
+                       "launch": "one CUDA graph replay per step" if graph is not None else "eager launches"},
+            "gaussians_per_s": g.N * world / (ms / 1000), "build_ms": st["build_ms"], "voxelize_ms": vms,
+            "occupied": c[0], "surface": c[1], "pairs": pairs,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                         "frac": achieved / alu_peak, "traffic": None, "kernel": "k_voxelize",
+                         "note": f"{OPS_PAIR} algorithmic FP32 ops per (voxel, candidate) pair x {pairs} pairs / "
+                                 f"voxelize time (k_voxelize + k_masks, CUDA events); peak = 148 SM x 128 lanes x "
+                                 f"max SM clock"},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     a = _args()
+    if a.config.startswith("G"):
+        return run_voxel(a)
     if a.impl == "reference":
         return run_reference(a)
     import torch

@@ -507,9 +507,9 @@ class GaussianScene:
                                                     dtype=np.float32)) for a in arrs]
             ptrs = [a.ctypes.data for a in keep]
             kind = HOST
-        n = int(keep[3].size)
+        n = int(np.prod(tuple(keep[3].shape)))
         for a, w in zip(keep[:3], (3, 4, 3)):
-            if int(np.prod(a.shape)) != n * w:
+            if int(np.prod(tuple(a.shape))) != n * w:
                 raise ValueError("mu / quat / scale must be [N][3] / [N][4] / [N][3] with N = len(opacity)")
         _check(lib().fgl_scene_upload_gaussians(self.scene._h, *ptrs, n, self.kappa, kind | (0 if sync else ASYNC),
                                                 _stream(stream)))

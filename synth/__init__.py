@@ -706,13 +706,13 @@ def grid_for(g: Gaussians, cells: int = 512, pad: int = 1) -> Grid:
 
 def gauss_config(name: str):
     """G1: 2 000 random Gaussians in a 4 m cube, 64^3 grid (oracle-sized). G2: 1 M surface splats
-    on the C2 rooms mesh, 512 voxels along the longest axis (the paper's scale: "millions of
-    primitives", P:130)."""
+    (tangent scales ~3.5 cm, normal ~1.5 cm) on the C2 rooms mesh, 512 voxels along the longest
+    axis (~4.7 cm voxels; the paper's scale: "millions of primitives")."""
     name = name.upper()
     if name == "G1":
         g = gaussians_random(2000, 11)
         return dict(name="G1", gauss=g, grid=grid_for(g, 62), kappa=3.0, theta=0.5, tile=8)
     if name == "G2":
-        g = gaussians_on_mesh(scene_rooms(2), 1_000_000, 12)
+        g = gaussians_on_mesh(scene_rooms(2), 1_000_000, 12, tangent_median=0.035, normal_scale=0.015)
         return dict(name="G2", gauss=g, grid=grid_for(g, 512), kappa=3.0, theta=0.5, tile=8)
     raise KeyError(name)

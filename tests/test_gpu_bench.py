@@ -26,3 +26,15 @@ def test_bench_json_line():
     assert d["gpu_launches"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+def test_voxel_bench_json_line():
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "G1", "--steps", "3", "--warmup",
+                          "3", "--cpu-seconds", "1"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["unit"] == "voxels/s" and d["value"] > 1e8 and d["gpu_launches"] > 0
+    assert d["roofline"]["bound"] == "alu" and 0 < d["roofline"]["frac"] < 1.5
+    assert d["occupied"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
