@@ -168,12 +168,12 @@ def _alu_peak_tops():
     return 148 * 128 * mhz * 1e6 / 1e12
 
 
-def _ncu_traffic(config: str):
-    """dram read+write bytes per launch of the cast kernel from the committed ncu summary."""
+def _ncu_traffic(config: str, kernel: str = "k_cast"):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu summary."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             s = json.load(f)
-        return s[config]["k_cast"]["dram_bytes_per_launch"]
+        return s[config][kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -442,7 +442,8 @@ def run_voxel(a):
             "gaussians_per_s": g.N * world / (ms / 1000), "build_ms": st["build_ms"], "voxelize_ms": vms,
             "occupied": c[0], "surface": c[1], "pairs": pairs,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
-                         "frac": achieved / alu_peak, "traffic": None, "kernel": "k_voxelize",
+                         "frac": achieved / alu_peak, "traffic": _ncu_traffic(a.config, "k_voxelize"),
+                         "kernel": "k_voxelize",
                          "note": f"{OPS_PAIR} algorithmic FP32 ops per (voxel, candidate) pair x {pairs} pairs / "
                                  f"voxelize time (k_voxelize + k_masks, CUDA events); peak = 148 SM x 128 lanes x "
                                  f"max SM clock"},

@@ -18,6 +18,13 @@ namespace {
 
 constexpr float kLog2e = 1.4426950408889634f;
 
+// 2^x on the SFU without the library's denormal-result rescaling (x >= -kk > -126 here)
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float wmin(float v) {
     for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
@@ -84,7 +91,8 @@ __global__ void __launch_bounds__(256) k_gauss_prep(const float *__restrict__ mu
 
 // Leaf j = Gaussian k = perm(j): Eq. 4 box (outward: every rounding of R, |R| s and mu -+ r is
 // covered by a 2^-18 relative pad, so the float box contains the exact kappa ellipsoid) and the
-// record r0 = (mu, f(sigma) = sigma [R24]), r1 = (c00, c11, c22, id), r2 = (2 c01, 2 c02, 2 c12, 0)
+// record r0 = (mu, f(sigma) = sigma [R24]), r1 = (c00, c11, c22, id), r2 = (2 c01, 2 c02, 2 c12,
+// 1 / (4 c00))
 // with c = (log2 e / 2) Sigma^-1, Sigma^-1 = R diag(1/s^2) R^T, so exp(-m^2 / 2) =
 // exp2(-d^T c d). Also the first 8-ary aggregate level of the leaf boxes.
 __global__ void __launch_bounds__(256) k_gauss_reorder(const float *__restrict__ mu, const float *__restrict__ quat,
@@ -130,7 +138,7 @@ __global__ void __launch_bounds__(256) k_gauss_reorder(const float *__restrict__
             }
         rec[3 * j] = make_float4(m[0], m[1], m[2], opac[k]);
         rec[3 * j + 1] = make_float4(A[0][0], A[1][1], A[2][2], __int_as_float((int32_t)k));
-        rec[3 * j + 2] = make_float4(2.f * A[0][1], 2.f * A[0][2], 2.f * A[1][2], 0.f);
+        rec[3 * j + 2] = make_float4(2.f * A[0][1], 2.f * A[0][2], 2.f * A[1][2], 0.25f / A[0][0]);
     }
     for (int o = 4; o; o >>= 1) {
         lo.x = fminf(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
@@ -161,6 +169,7 @@ struct VoxArgs {
     int rowbytes;         // bytes per occupancy row (4 * ceil(nx / 32))
     float theta;
     float kk;             // (log2 e / 2) kappa^2: the R25 truncation in exp2 units
+    float kk_skip;        // kk with a 2^-10 margin: the row-minimum skip test never drops a term
 };
 
 __global__ void __launch_bounds__(kVoxThreads) k_voxelize(const Node64 *__restrict__ nodes,
@@ -263,11 +272,14 @@ __global__ void __launch_bounds__(kVoxThreads) k_voxelize(const Node64 *__restri
                 const float dy = vy - a.y, dz = vz - a.z;
                 const float P = fmaf(e.x, dy, e.y * dz);                   // 2 c01 dy + 2 c02 dz
                 const float Q = fmaf(dy, fmaf(b.y, dy, e.z * dz), b.z * dz * dz);  // c11 dy^2 + 2 c12 dy dz + c22 dz^2
+                // the row's quadratic c00 dx^2 + P dx + Q is >= Q - P^2 / (4 c00) for every x: when no
+                // lane of the warp can reach the kappa ellipsoid, skip the candidate (warp-uniform)
+                if (!__any_sync(0xffffffffu, fmaf(-P * P, e.w, Q) <= va.kk_skip)) continue;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const float dx = vx[q] - a.x;
                     const float arg = fmaf(dx, fmaf(b.x, dx, P), Q);
-                    if (arg <= va.kk) D[q] = fmaf(a.w, exp2f(-arg), D[q]);
+                    if (arg <= va.kk) D[q] = fmaf(a.w, ex2(-arg), D[q]);
                 }
             }
             pairs += (unsigned long long)nb;
@@ -373,6 +385,7 @@ void launch_voxelize(const BuildBuffers &b, const VoxGrid &g, float kappa, float
     va.rowbytes = 4 * nwx;
     va.theta = g.theta;
     va.kk = 0.5f * kLog2e * kappa * kappa;
+    va.kk_skip = va.kk * (1.0f + 0x1p-10f) + 0x1p-20f;
     FGL_CUDA(cudaMemsetAsync(occ, 0, sizeof(uint32_t) * (size_t)nwx * va.ny * va.nz, s));
     const int64_t ntiles = (int64_t)va.tx * va.ty * tz;
     k_voxelize<<<(unsigned)ntiles, kVoxThreads, 0, s>>>(b.nodes, b.tri, va, density, reinterpret_cast<uint8_t *>(occ),

@@ -9,7 +9,8 @@ M = ["gpu__time_duration.sum", "sm__inst_issued.avg.pct_of_peak_sustained_active
 SHORT = ["us", "issue%", "warps%", "dramR MB", "dramW MB", "winst M", "L1hit", "L2hit", "regs", "lsb", "bar", "membar", "lgthr"]
 out = subprocess.check_output(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], text=True, stderr=subprocess.DEVNULL)
 rows = list(csv.reader(io.StringIO(out)))
-h = rows[0]
+h, units = rows[0], rows[1]
+SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "KB": 1e-3, "MB": 1.0, "GB": 1e3}
 idx = [h.index(m) if m in h else None for m in M]
 print(f"{'kernel':24s}" + "".join(f"{s:>9s}" for s in SHORT))
 for r in rows[2:]:
@@ -17,8 +18,8 @@ for r in rows[2:]:
     vals = []
     for m, i in zip(M, idx):
         v = float(r[i].replace(",", "")) if i is not None and r[i] not in ("", "n/a") else float("nan")
-        if m.startswith("gpu__time"): v /= 1e3 if v > 1e5 else 1  # ns or us
-        if m.startswith("dram__bytes"): v /= 1e6
+        if m.startswith("gpu__time"): v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(units[i], 1.0)
+        if m.startswith("dram__bytes"): v *= SCALE.get(units[i], 1e-6)
         if m == "smsp__inst_executed.sum": v /= 1e6
         vals.append(v)
     print(f"{name:24s}" + "".join(f"{v:9.1f}" for v in vals))

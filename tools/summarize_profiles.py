@@ -39,7 +39,7 @@ def raw(rep):
 def main():
     summary = {}
     lines = []
-    for cfg in ("C2", "C3"):
+    for cfg in ("C2", "C3", "G2"):
         rep = os.path.join(OUT, f"{TAG}_k_cast_{cfg}.ncu-rep")
         if os.path.exists(rep):
             for d in raw(rep):
@@ -57,12 +57,18 @@ def main():
                                  capture_output=True, text=True).stdout
             with open(os.path.join(PROF, f"{TAG}_launches_{cfg}.txt"), "w") as f:
                 f.write(f"# one full step ({cfg}): per-launch device time (ncu, cold cache, serialised)\n" + txt)
-    rep = os.path.join(OUT, f"{TAG}_build_C2.ncu-rep")
-    if os.path.exists(rep):
+    for name in ("build_C2", "build_C3", "vox_G2"):
+        rep = os.path.join(OUT, f"{TAG}_{name}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
         for d in raw(rep):
-            lines.append(f"## C2 build {d['kernel']}")
+            lines.append(f"## {name} {d['kernel']}")
             lines += [f"  {k:70s} {v}" for k, v in d.items() if k not in ("kernel", "top_stalls")]
             lines.append(f"  top stalls: {d['top_stalls']}")
+            if name == "vox_G2" and "k_voxelize" in d["kernel"]:
+                rd = float(d["dram__bytes_read.sum"].split()[0]) * (1e6 if "Mbyte" in d["dram__bytes_read.sum"] else 1)
+                wr = float(d["dram__bytes_write.sum"].split()[0]) * (1e6 if "Mbyte" in d["dram__bytes_write.sum"] else 1)
+                summary["G2"] = {"k_voxelize": {"dram_bytes_per_launch": rd + wr, "source": os.path.basename(rep)}}
     with open(os.path.join(PROF, f"{TAG}_ncu_full.txt"), "w") as f:
         f.write("\n".join(lines) + "\n")
     old = {}
