@@ -234,6 +234,38 @@ typedef struct {
 FGL_API fgl_status fgl_voxelize(const fgl_scene *scene, const fgl_grid *grid, float *density, uint32_t *occupancy,
                                 uint32_t *surface, uint32_t *interior, int64_t *counts, void *cuda_stream);
 
+/* ---- occupancy -> mesh (§IV-B) ---------------------
+ * Volumes are device arrays on the current CUDA device, voxel (i, j, k) at linear index
+ * (k ny + j) nx + i with centre origin + (i + 1/2, j + 1/2, k + 1/2) spacing; bit volumes are
+ * uint32 [nz][ny][ceil(nx / 32)] (bit b of word w = voxel x = 32 w + b), as fgl_voxelize writes.
+ * Scratch is stream-ordered (cudaMallocAsync), so the calls are CUDA-graph capturable. */
+
+/* Eq. 13-14a: V' = G_sigma * V (separable, sigma in metres -> sigma / spacing[a] voxels, kernel
+ * truncated at ceil(3 sigma) voxels and normalised, zero outside the grid; float32), out = V' >= tau
+ * (bit volume). vprime (nullable): float [nz][ny][nx]. FGL_E_USAGE: sigma > 21 voxels, bad sizes. */
+FGL_API fgl_status fgl_denoise(const uint32_t *occupancy, const int32_t *dims, const float *spacing, float sigma,
+                               float tau, uint32_t *out, float *vprime, void *cuda_stream);
+
+/* Eqs. 15-17 narrow-band TSDF of a bit volume: s = +1 on free voxels 6-connected to the padded
+ * frame (flood fill), -1 elsewhere; kappa = shell index of the 6-neighbour expansion from
+ * S_0 = {x : a 6-neighbour differs in V} (the frame counts as free); phi = s min(kappa v_min, r)
+ * (float32; s r beyond the band), v_min = min(spacing). phi: float [nz][ny][nx]. The band
+ * r / v_min must be <= 254 shells. */
+FGL_API fgl_status fgl_tsdf(const uint32_t *occupancy, const int32_t *dims, const float *spacing, float r, float *phi,
+                            void *cuda_stream);
+
+/* Eq. 18 Marching Cubes of phi at iso on the voxel-centre lattice (corner inside iff phi < iso):
+ * face-consistent cube polygons (R34: inside corners cut off run by run per face, loops
+ * fanned from their lowest edge, or around a centre vertex when a fan diagonal would lie in a
+ * face), so the mesh is watertight wherever the surface stays inside the grid and consistently
+ * oriented (normals towards phi > iso). Vertices: one per crossing edge, numbered by global edge
+ * id 3 * voxel + axis, then the centre vertices; verts float [vcap][3], normals (nullable) the
+ * normalised interpolated central-difference gradient, tris int32 [tcap][3]; entries beyond a
+ * capacity are not written. counts (device int64 [2], nullable) = {vertices, triangles} needed. */
+FGL_API fgl_status fgl_marching_cubes(const float *phi, const int32_t *dims, const float *origin, const float *spacing,
+                                      float iso, float *verts, float *normals, int64_t vcap, int32_t *tris,
+                                      int64_t tcap, int64_t *counts, void *cuda_stream);
+
 /* ---- LBVH internals, for parity tests (host destination pointers; each may be NULL) ----- */
 typedef struct {
     float *scene_box;      /* [6]  lo.xyz, hi.xyz                                              */

@@ -422,6 +422,55 @@ fgl_status fgl_voxelize(const fgl_scene *s, const fgl_grid *grid, float *density
     FGL_API_END
 }
 
+namespace {
+void check_volume(const int32_t *dims, const float *spacing, int64_t max_voxels) {
+    if (!dims || !spacing) throw Error(FGL_E_USAGE, "dims / spacing is NULL");
+    int64_t n = 1;
+    for (int a = 0; a < 3; ++a) {
+        if (dims[a] < 1) throw Error(FGL_E_USAGE, "dims must be >= 1");
+        if (!(spacing[a] > 0.f) || !std::isfinite(spacing[a])) throw Error(FGL_E_USAGE, "spacing must be finite and > 0");
+        n *= dims[a];
+    }
+    if (n > max_voxels) throw Error(FGL_E_RESOURCE, "volume too large");
+}
+}  // namespace
+
+fgl_status fgl_denoise(const uint32_t *occupancy, const int32_t *dims, const float *spacing, float sigma, float tau,
+                       uint32_t *out, float *vprime, void *stream) {
+    FGL_API_BEGIN
+    check_volume(dims, spacing, (int64_t(1) << 31) - 1);
+    if (!occupancy || !out) throw Error(FGL_E_USAGE, "occupancy / out is NULL");
+    if (!(sigma > 0.f) || !std::isfinite(sigma)) throw Error(FGL_E_USAGE, "sigma must be finite and > 0");
+    if (!std::isfinite(tau)) throw Error(FGL_E_USAGE, "tau must be finite");
+    fgl::launch_denoise(occupancy, dims, spacing, sigma, tau, out, vprime, (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_tsdf(const uint32_t *occupancy, const int32_t *dims, const float *spacing, float r, float *phi,
+                    void *stream) {
+    FGL_API_BEGIN
+    check_volume(dims, spacing, (int64_t(1) << 31) - 1);
+    if (!occupancy || !phi) throw Error(FGL_E_USAGE, "occupancy / phi is NULL");
+    if (!(r > 0.f) || !std::isfinite(r)) throw Error(FGL_E_USAGE, "r must be finite and > 0");
+    fgl::launch_tsdf(occupancy, dims, spacing, r, phi, (cudaStream_t)stream);
+    FGL_API_END
+}
+
+fgl_status fgl_marching_cubes(const float *phi, const int32_t *dims, const float *origin, const float *spacing,
+                              float iso, float *verts, float *normals, int64_t vcap, int32_t *tris, int64_t tcap,
+                              int64_t *counts, void *stream) {
+    FGL_API_BEGIN
+    check_volume(dims, spacing, int64_t(1) << 30);
+    if (!phi || !origin) throw Error(FGL_E_USAGE, "phi / origin is NULL");
+    if (!std::isfinite(iso)) throw Error(FGL_E_USAGE, "iso must be finite");
+    if (vcap < 0 || tcap < 0) throw Error(FGL_E_USAGE, "capacities must be >= 0");
+    if ((vcap > 0 && !verts) || (tcap > 0 && !tris)) throw Error(FGL_E_USAGE, "verts / tris is NULL");
+    if (normals && vcap > 0 && !verts) throw Error(FGL_E_USAGE, "normals need verts");
+    fgl::launch_marching_cubes(phi, dims, origin, spacing, iso, verts, normals, vcap, tris, tcap, counts,
+                               (cudaStream_t)stream);
+    FGL_API_END
+}
+
 fgl_status fgl_nearest(const fgl_scene *s, const float *queries, int64_t m, float *dist, int32_t *idx, void *stream) {
     FGL_API_BEGIN
     check_cast(s);

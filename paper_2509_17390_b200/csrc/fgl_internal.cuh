@@ -186,6 +186,13 @@ void launch_gauss_build(const float *mu, const float *quat, const float *scale, 
 void launch_voxelize(const BuildBuffers &b, const VoxGrid &g, float kappa, float *density, uint32_t *occ,
                      uint32_t *surf, uint32_t *inter, unsigned long long *counts, unsigned int *overflow,
                      cudaStream_t s);
+// tsdf.cu
+void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, float sigma, float tau,
+                    uint32_t *out, float *vprime, cudaStream_t s);
+void launch_tsdf(const uint32_t *occ, const int *dims, const float *spacing, float r, float *phi, cudaStream_t s);
+void launch_marching_cubes(const float *phi, const int *dims, const float *origin, const float *spacing, float iso,
+                           float *verts, float *normals, int64_t vcap, int32_t *tris, int64_t tcap, int64_t *counts,
+                           cudaStream_t s);
 // points.cu
 void launch_iota3(int32_t *tris, int64_t n, cudaStream_t s);
 void launch_nearest(const SceneView &sv, const float *q, int64_t m, float *dist, int32_t *idx, cudaStream_t s);

@@ -91,6 +91,10 @@ _SIGS = {
     "fgl_scene_upload_gaussians": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_float, c_int,
                                            c_void_p]),
     "fgl_voxelize": (c_int, [c_void_p, POINTER(GridC), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "fgl_denoise": (c_int, [c_void_p, c_void_p, c_void_p, c_float, c_float, c_void_p, c_void_p, c_void_p]),
+    "fgl_tsdf": (c_int, [c_void_p, c_void_p, c_void_p, c_float, c_void_p, c_void_p]),
+    "fgl_marching_cubes": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_void_p, c_void_p, c_int64,
+                                   c_void_p, c_int64, c_void_p, c_void_p]),
     "fgl_alloc": (c_int, [c_int, c_int64, POINTER(c_void_p)]),
     "fgl_free": (c_int, [c_void_p]),
     "fgl_ipc_get_handle": (c_int, [c_void_p, c_void_p]),
@@ -566,6 +570,69 @@ class GaussianScene:
         if counts:
             res["counts"] = cnt
         return res
+
+
+# ---- occupancy -> mesh (§IV-B, NEXT-3) -----------------------------------------------------------
+def _vol_args(dims, spacing):
+    d = (c_int32 * 3)(*[int(x) for x in dims])
+    sp = (c_float * 3)(*([float(spacing)] * 3 if np.isscalar(spacing) else [float(x) for x in spacing]))
+    return d, sp
+
+
+def denoise(occupancy: torch.Tensor, dims, spacing, sigma: float, tau: float, vprime: bool = False, stream=None):
+    """Eqs. 13-14a on a device bit volume: returns the re-thresholded bit volume (and V' float32
+    [nz][ny][nx] when vprime)."""
+    d, sp = _vol_args(dims, spacing)
+    out = torch.empty_like(occupancy)
+    vp = torch.empty((int(dims[2]), int(dims[1]), int(dims[0])), dtype=torch.float32,
+                     device=occupancy.device) if vprime else None
+    _check(lib().fgl_denoise(occupancy.data_ptr(), d, sp, float(sigma), float(tau), out.data_ptr(), _ptr(vp),
+                             _stream(stream)))
+    return (out, vp) if vprime else out
+
+
+def tsdf(occupancy: torch.Tensor, dims, spacing, r: float, out=None, stream=None) -> torch.Tensor:
+    """Eqs. 15-17 narrow-band TSDF phi float32 [nz][ny][nx] of a device bit volume."""
+    d, sp = _vol_args(dims, spacing)
+    phi = out if out is not None else torch.empty((int(dims[2]), int(dims[1]), int(dims[0])), dtype=torch.float32,
+                                                  device=occupancy.device)
+    _check(lib().fgl_tsdf(occupancy.data_ptr(), d, sp, float(r), phi.data_ptr(), _stream(stream)))
+    return phi
+
+
+def marching_cubes(phi: torch.Tensor, origin, spacing, iso: float = 0.0, normals: bool = False, out=None,
+                   stream=None) -> dict:
+    """Eq. 18 on phi [nz][ny][nx] (device): dict(verts float32 [V][3], tris int32 [T][3][, normals]).
+    Sizes come from a counting pass (one host sync) unless `out` carries buffers large enough
+    (verts, tris[, normals], counts) — then the call is sync-free and the first counts entries are
+    valid."""
+    nz, ny, nx = phi.shape
+    d, sp = _vol_args((nx, ny, nz), spacing)
+    o = (c_float * 3)(*[float(x) for x in origin])
+    dev = phi.device
+    st = _stream(stream)
+    if out is None:
+        cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+        _check(lib().fgl_marching_cubes(phi.data_ptr(), d, o, sp, float(iso), None, None, 0, None, 0, cnt.data_ptr(),
+                                        st))
+        nv, nt = (int(x) for x in cnt.cpu())
+        out = dict(verts=torch.empty((max(nv, 1), 3), dtype=torch.float32, device=dev),
+                   tris=torch.empty((max(nt, 1), 3), dtype=torch.int32, device=dev), counts=cnt)
+        if normals:
+            out["normals"] = torch.empty((max(nv, 1), 3), dtype=torch.float32, device=dev)
+        sized = (nv, nt)
+    else:
+        sized = None
+    v, t, c = out["verts"], out["tris"], out["counts"]
+    nrm = out.get("normals") if normals else None
+    _check(lib().fgl_marching_cubes(phi.data_ptr(), d, o, sp, float(iso), v.data_ptr(), _ptr(nrm), int(v.shape[0]),
+                                    t.data_ptr(), int(t.shape[0]), c.data_ptr(), st))
+    if sized is None:
+        return out
+    res = dict(verts=v[:sized[0]], tris=t[:sized[1]], counts=c)
+    if normals:
+        res["normals"] = nrm[:sized[0]]
+    return res
 
 
 def kernel_launches() -> int:
