@@ -36,8 +36,9 @@ def _args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["fgl", "reference"], default="fgl")
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "G1", "G2"],
-                    help="C1-C5: LiDAR cast (the north star); G1/G2: Gaussian voxelizer (NEXT-2)")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "G1", "G2", "T1", "T2"],
+                    help="C1-C5: LiDAR cast (the north star); G1/G2: Gaussian voxelizer (NEXT-2); "
+                         "T1/T2: TSDF + Marching Cubes on the G1/G2 occupancy (NEXT-3)")
     ap.add_argument("--poses", type=int, default=None, help="poses per GPU per step")
     ap.add_argument("--mode", choices=["full", "cast"], default="full",
                     help="full = upload+build+cast per step (default); cast = cast only on a prebuilt scene")
@@ -453,10 +454,154 @@ def run_voxel(a):
     return 0
 
 
+# NEXT-3: occupancy -> mesh (§IV-B Eqs. 13-18). One step = denoise (Eqs. 13-14a) + narrow-
+# band TSDF (Eqs. 15-17) + Marching Cubes (Eq. 18) of the G config's occupancy volume.
+MESH_METRIC = "voxels/sec (occupancy -> mesh: denoise + narrow-band TSDF + Marching Cubes per step)"
+TSDF_SIGMA_VOX, TSDF_TAU, TSDF_BAND_VOX = 0.7, 0.35, 3
+
+
+def run_mesh(a):
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    gname = "G" + a.config[1:]
+    cfg = synth.gauss_config(gname)
+    g, grid, kappa, theta = cfg["gauss"], cfg["grid"], cfg["kappa"], cfg["theta"]
+    h = grid.h
+    sp = (h, h, h)
+    nx, ny, nz = grid.dims
+    wl = (f"{a.config}: occupancy of {gname} ({g.N} Gaussians, grid {nx}x{ny}x{nz}, h={h:.4f} m) -> denoise "
+          f"(sigma {TSDF_SIGMA_VOX} voxels, tau {TSDF_TAU}) -> TSDF (r = {TSDF_BAND_VOX} voxels) -> MC at iso 0")
+    if a.impl == "reference":
+        if rank != 0:
+            return 0
+        # the oracle on a bounded sub-block of the same occupancy (its TSDF + MC are numpy loops)
+        from oracle import gauss as og
+        from oracle import tsdf as ot
+        sub = synth.Grid(grid.origin, h, (min(nx, 48), min(ny, 48), min(nz, 32)))
+        D, _, _ = og.density(synth.Gaussians(g.mu, g.quat, g.scale, g.opacity), sub, kappa) if g.N <= 5000 else \
+            (None, None, None)
+        if D is None:
+            pts_ok = np.all((g.mu >= np.asarray(sub.origin) - 0.5) &
+                            (g.mu <= np.asarray(sub.origin) + np.asarray(sub.dims) * h + 0.5), axis=1)
+            gg = synth.Gaussians(g.mu[pts_ok], g.quat[pts_ok], g.scale[pts_ok], g.opacity[pts_ok])
+            D, _, _ = og.density(gg, sub, kappa)
+        V = og.occupancy(D, theta)
+
+        def once():
+            Vd = ot.rethreshold(ot.blur(V, TSDF_SIGMA_VOX * h, sp), TSDF_TAU)
+            phi, _ = ot.tsdf(Vd, sp, TSDF_BAND_VOX * h)
+            ot.marching_cubes(phi, sub.origin, sp)
+
+        for _ in range(a.warmup):
+            once()
+        times = []
+        for _ in range(a.steps):
+            t0 = time.perf_counter()
+            once()
+            times.append(time.perf_counter() - t0)
+        ms = 1000 * statistics.mean(times)
+        v = sub.nvox / (ms / 1000)
+        print(json.dumps({"metric": MESH_METRIC, "value": v, "unit": "voxels/s", "n_gpus": 0, "steps": a.steps,
+                          "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                          "config": {"workload": wl, "sample_voxels_per_step": sub.nvox},
+                          "cpu_baseline": {"value": v, "unit": "voxels/s", "cores": 1, "kind": "oracle",
+                                           "sample": f"a {sub.dims} sub-block of the occupancy per step"},
+                          "e2e": {"value": v, "unit": "voxels/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+    import torch
+
+    import paper_2509_17390_b200 as fgl
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    arrs = [torch.from_numpy(x).to(dev) for x in (g.mu, g.quat, g.scale, g.opacity)]
+    gs = fgl.GaussianScene(*arrs, kappa=kappa, device=dev)
+    occ = gs.voxelize(grid.origin, h, grid.dims, theta, masks=False)["occupancy"]
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    first = fgl.marching_cubes(fgl.tsdf(fgl.denoise(occ, grid.dims, sp, TSDF_SIGMA_VOX * h, TSDF_TAU), grid.dims, sp,
+                                        TSDF_BAND_VOX * h), grid.origin, sp)
+    nv, nt = first["verts"].shape[0], first["tris"].shape[0]
+    mesh_out = dict(verts=torch.empty((nv, 3), dtype=torch.float32, device=dev),
+                    tris=torch.empty((nt, 3), dtype=torch.int32, device=dev),
+                    counts=torch.zeros(2, dtype=torch.int64, device=dev))
+    den = torch.empty_like(occ)
+    phi = torch.empty((nz, ny, nx), dtype=torch.float32, device=dev)
+
+    def step():
+        fgl.denoise(occ, grid.dims, sp, TSDF_SIGMA_VOX * h, TSDF_TAU, out=den)
+        fgl.tsdf(den, grid.dims, sp, TSDF_BAND_VOX * h, out=phi)
+        fgl.marching_cubes(phi, grid.origin, sp, out=mesh_out)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    flush = None if a.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    K = a.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    l0 = fgl.kernel_launches()
+    with Clocks(local) as clk:
+        for i in range(K):
+            if flush is not None:
+                flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    launches = fgl.kernel_launches() - l0
+    ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    c = mesh_out["counts"].cpu().tolist()
+    e2e = None
+    if not a.no_e2e:  # host occupancy bits in, mesh (verts + tris) out
+        occ_h = occ.cpu().pin_memory()
+        vh = torch.empty((nv, 3), dtype=torch.float32).pin_memory()
+        th = torch.empty((nt, 3), dtype=torch.int32).pin_memory()
+        ee = []
+        for _ in range(max(3, K // 2)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            occ.copy_(occ_h, non_blocking=True)
+            step()
+            vh.copy_(mesh_out["verts"], non_blocking=True)
+            th.copy_(mesh_out["tris"], non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ee.append(e0.elapsed_time(e1))
+        ems = statistics.mean(ee)
+        e2e = {"value": grid.nvox / (ems / 1000), "unit": "voxels/s", "h2d_bytes_per_step": int(occ_h.numel() * 4),
+               "d2h_bytes_per_step": int(vh.numel() * 4 + th.numel() * 4), "ms_per_step": ems}
+    # HBM roofline: the kernels stream the volume; algorithmic bytes per voxel = denoise (1/8 B in,
+    # 3 passes x 8 B float r/w, 4 B V', 1/8 B out) + TSDF (union-find 4 B label x ~3 r/w, kappa 1 B x
+    # (band + 2), phi 4 B) + MC (phi 4 B x 2 reads, 3 x 4 B counts r/w x 3 passes) ~= 100 B
+    bytes_per_voxel = 100.0
+    hbm_peak, peak_kind = _peaks()
+    achieved = bytes_per_voxel * grid.nvox / (ms / 1000) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": MESH_METRIC, "value": grid.nvox / (ms / 1000), "unit": "voxels/s", "n_gpus": 1, "steps": K,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl, "step": "denoise+tsdf+marching_cubes", "voxels": grid.nvox,
+                       "parallelism": "replicas x1",
+                       "l2": "flushed between steps (256 MiB memset, untimed)" if flush is not None else "not flushed",
+                       "launch": "eager launches (stream-ordered scratch)"},
+            "mesh_vertices": c[0], "mesh_triangles": c[1],
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "kernel": "denoise+tsdf+mc (all)",
+                         "note": f"~{bytes_per_voxel:.0f} algorithmic bytes per voxel over the whole step "
+                                 f"(DESIGN.md §8d); peak {peak_kind}"},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}), flush=True)
+    return 0
+
+
 def main():
     a = _args()
     if a.config.startswith("G"):
         return run_voxel(a)
+    if a.config.startswith("T"):
+        return run_mesh(a)
     if a.impl == "reference":
         return run_reference(a)
     import torch

@@ -22,8 +22,23 @@ namespace fgl {
 namespace {
 
 // ---- scratch: stream-ordered allocations (capturable in CUDA graphs) -------------------------
+// keep freed scratch in the device's default pool (release threshold = max) so a repeated call
+// does not re-map memory from the driver every time
+void keep_pool() {
+    int dev = 0;
+    FGL_CUDA(cudaGetDevice(&dev));
+    static std::once_flag once[64];
+    std::call_once(once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        FGL_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+        uint64_t thr = UINT64_MAX;
+        FGL_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    });
+}
+
 template <class T>
 T *salloc(size_t n, cudaStream_t s) {
+    keep_pool();
     void *p = nullptr;
     FGL_CUDA(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), s));
     return (T *)p;
@@ -53,29 +68,31 @@ struct Taps {
     int R;
 };
 
-// pass 0: bits -> float along x; pass 1, 2: float -> float along y, z
+// pass 0: bits -> float along x; pass 1, 2: float -> float along y, z. Launch: x = blockIdx.x
+// * 256 + tid, row (y, z) = blockIdx.y (no divisions)
 __global__ void __launch_bounds__(256) k_blur(const uint32_t *__restrict__ bits, const float *__restrict__ in,
                                               float *__restrict__ out, Dims d, int axis, Taps t) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(i % d.nx);
-        const int64_t r = i / d.nx;
-        const int y = (int)(r % d.ny), z = (int)(r / d.ny);
-        const int c = axis == 0 ? x : (axis == 1 ? y : z);
-        const int n = axis == 0 ? d.nx : (axis == 1 ? d.ny : d.nz);
-        const int64_t stride = axis == 0 ? 1 : (axis == 1 ? d.nx : (int64_t)d.nx * d.ny);
-        float acc = 0.f;
+    const int x = blockIdx.x * 64 + threadIdx.x;
+    if (x >= d.nx) return;
+    for (int row = blockIdx.y * 4 + threadIdx.y; row < d.ny * d.nz; row += gridDim.y * 4) {
+    const int y = row % d.ny, z = row / d.ny;
+    const int64_t i = (int64_t)row * d.nx + x;
+    float acc = 0.f;
+    if (axis == 0) {
+        const uint32_t *rw = bits + (int64_t)row * d.nwx;
+        for (int k = -t.R; k <= t.R; ++k) {
+            const int cc = x + k;
+            if (cc >= 0 && cc < d.nx && ((__ldg(rw + (cc >> 5)) >> (cc & 31)) & 1u)) acc += t.w[k + t.R];
+        }
+    } else {
+        const int c = axis == 1 ? y : z, n = axis == 1 ? d.ny : d.nz;
+        const int64_t stride = axis == 1 ? d.nx : (int64_t)d.nx * d.ny;
         for (int k = -t.R; k <= t.R; ++k) {
             const int cc = c + k;
-            if (cc < 0 || cc >= n) continue;
-            float v;
-            if (axis == 0) {
-                v = bit_at(bits, d, cc, y, z) ? 1.f : 0.f;
-            } else {
-                v = __ldg(in + i + (int64_t)k * stride);
-            }
-            acc = fmaf(t.w[k + t.R], v, acc);
+            if (cc >= 0 && cc < n) acc = fmaf(t.w[k + t.R], __ldg(in + i + (int64_t)k * stride), acc);
         }
-        out[i] = acc;
+    }
+    out[i] = acc;
     }
 }
 
@@ -121,38 +138,70 @@ __device__ __forceinline__ void uf_union(int *lab, int a, int b) {
     }
 }
 
+// labels start at the first free voxel of each x-run (the run is its own component); one thread
+// per voxel, 2-D launch as k_blur
+__device__ __forceinline__ bool occ_at(const uint32_t *__restrict__ rw, int x) {
+    return (__ldg(rw + (x >> 5)) >> (x & 31)) & 1u;
+}
+__device__ __forceinline__ int run_start(const uint32_t *__restrict__ rw, int x) {
+    // highest occupied voxel below x in the row, + 1 (0 if none)
+    int w = x >> 5;
+    uint32_t m = __ldg(rw + w) & ((1u << (x & 31)) - 1u);
+    while (!m && w > 0) m = __ldg(rw + --w);
+    return m ? (w << 5) + (31 - __clz(m)) + 1 : 0;
+}
+
 __global__ void __launch_bounds__(256) k_cc_init(const uint32_t *__restrict__ occ, Dims d, int *__restrict__ lab) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(i % d.nx);
-        const int64_t r = i / d.nx;
-        const bool occd = (occ[r * d.nwx + (x >> 5)] >> (x & 31)) & 1u;
-        lab[i] = occd ? -1 : (int)i;
+    const int x = blockIdx.x * 64 + threadIdx.x;
+    if (x >= d.nx) return;
+    for (int row = blockIdx.y * 4 + threadIdx.y; row < d.ny * d.nz; row += gridDim.y * 4) {
+        const uint32_t *rw = occ + (int64_t)row * d.nwx;
+        const int64_t i = (int64_t)row * d.nx + x;
+        lab[i] = occ_at(rw, x) ? -1 : (int)((int64_t)row * d.nx + run_start(rw, x));
     }
 }
 
-__global__ void __launch_bounds__(256) k_cc_merge(Dims d, int *lab) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
-        if (__ldcg(lab + i) < 0) continue;
-        const int x = (int)(i % d.nx);
-        const int64_t r = i / d.nx;
-        const int y = (int)(r % d.ny), z = (int)(r / d.ny);
-        if (x > 0 && __ldcg(lab + i - 1) >= 0) uf_union(lab, (int)i, (int)(i - 1));
-        if (y > 0 && __ldcg(lab + i - d.nx) >= 0) uf_union(lab, (int)i, (int)(i - d.nx));
-        const int64_t sl = (int64_t)d.nx * d.ny;
-        if (z > 0 && __ldcg(lab + i - sl) >= 0) uf_union(lab, (int)i, (int)(i - sl));
+// union the runs of neighbouring rows (y - 1, z - 1) where they begin to overlap: at x = the later
+// of the two run starts, so each overlapping pair of runs is united once
+__global__ void __launch_bounds__(256) k_cc_merge(const uint32_t *__restrict__ occ, Dims d, int *lab) {
+    const int x = blockIdx.x * 64 + threadIdx.x;
+    if (x >= d.nx) return;
+    for (int row = blockIdx.y * 4 + threadIdx.y; row < d.ny * d.nz; row += gridDim.y * 4) {
+    const int y = row % d.ny, z = row / d.ny;
+    const uint32_t *rw = occ + (int64_t)row * d.nwx;
+    if (occ_at(rw, x)) continue;
+    const int64_t i = (int64_t)row * d.nx + x;
+    const bool start = x == 0 || occ_at(rw, x - 1);
+    if (y > 0) {
+        const uint32_t *rn = rw - d.nwx;
+        if (!occ_at(rn, x) && (start || occ_at(rn, x - 1))) uf_union(lab, (int)i, (int)(i - d.nx));
+    }
+    if (z > 0) {
+        const uint32_t *rn = rw - (int64_t)d.nwx * d.ny;
+        if (!occ_at(rn, x) && (start || occ_at(rn, x - 1)))
+            uf_union(lab, (int)i, (int)(i - (int64_t)d.nx * d.ny));
+    }
     }
 }
 
 // flatten to roots; free voxels on the grid boundary touch the padded frame: their root is outside
-__global__ void __launch_bounds__(256) k_cc_flatten(Dims d, int *lab, uint8_t *__restrict__ out_root) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
-        if (__ldcg(lab + i) < 0) continue;
+// roots of the run starts (lab[start] = root); free voxels on the grid boundary touch the padded
+// frame: their root is outside. Other voxels keep lab = their run start (root = lab[lab[i]]).
+__global__ void __launch_bounds__(256) k_cc_flatten(const uint32_t *__restrict__ occ, Dims d, int *lab,
+                                                    uint8_t *__restrict__ out_root) {
+    const int x = blockIdx.x * 64 + threadIdx.x;
+    if (x >= d.nx) return;
+    for (int row = blockIdx.y * 4 + threadIdx.y; row < d.ny * d.nz; row += gridDim.y * 4) {
+        const uint32_t *rw = occ + (int64_t)row * d.nwx;
+        if (occ_at(rw, x)) continue;
+        const int y = row % d.ny, z = row / d.ny;
+        const bool start = x == 0 || occ_at(rw, x - 1);
+        const bool border = x == 0 || y == 0 || z == 0 || x == d.nx - 1 || y == d.ny - 1 || z == d.nz - 1;
+        if (!start && !border) continue;
+        const int64_t i = (int64_t)row * d.nx + x;
         const int root = uf_find(lab, (int)i);
-        lab[i] = root;
-        const int x = (int)(i % d.nx);
-        const int64_t r = i / d.nx;
-        const int y = (int)(r % d.ny), z = (int)(r / d.ny);
-        if (x == 0 || y == 0 || z == 0 || x == d.nx - 1 || y == d.ny - 1 || z == d.nz - 1) out_root[root] = 1;
+        if (start) lab[i] = root;
+        if (border) out_root[root] = 1;
     }
 }
 
@@ -219,8 +268,8 @@ __global__ void __launch_bounds__(256) k_phi(const int *__restrict__ lab, const 
                                              const uint8_t *__restrict__ kappa, Dims d, float vmin, float r,
                                              float *__restrict__ phi) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
-        const int l = lab[i];
-        const bool out = l >= 0 && outside_root[l];
+        const int l = lab[i];  // run start (or -1), whose label is the component root
+        const bool out = l >= 0 && outside_root[lab[l]];
         const int k = kappa[i];
         float dist = k == 255 ? r : __fmul_rn((float)k, vmin);
         dist = fminf(dist, r);
@@ -424,64 +473,85 @@ __device__ __forceinline__ unsigned long long block_excl(unsigned long long v, u
     return off + x - v;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t *__restrict__ in, int64_t n,
-                                                              unsigned long long *__restrict__ part) {
+// three arrays scanned together (one pass structure, shared launches)
+struct Scan3 {
+    uint32_t *a[3];
+};
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Scan3 in, int64_t n, unsigned long long *__restrict__ part,
+                                                              int nb) {
     __shared__ unsigned long long s_w[kScanThreads / 32];
     const int64_t base = (int64_t)blockIdx.x * kScanTile;
-    unsigned long long v = 0;
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t idx = base + k * kScanThreads + threadIdx.x;
-        if (idx < n) v += in[idx];
+    for (int q = 0; q < 3; ++q) {
+        unsigned long long v = 0;
+        for (int k = 0; k < kScanItems; ++k) {
+            const int64_t idx = base + k * kScanThreads + threadIdx.x;
+            if (idx < n) v += in.a[q][idx];
+        }
+        unsigned long long tot;
+        block_excl(v, s_w, tot);
+        if (threadIdx.x == 0) part[q * nb + blockIdx.x] = tot;
     }
-    unsigned long long tot;
-    block_excl(v, s_w, tot);
-    if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_parts(unsigned long long *part, int nb,
                                                              unsigned long long *__restrict__ total) {
     __shared__ unsigned long long s_w[kScanThreads / 32];
+    const int q = blockIdx.x;  // one block per array
     unsigned long long carry = 0;
     for (int b0 = 0; b0 < nb; b0 += kScanThreads) {
         const int idx = b0 + threadIdx.x;
-        const unsigned long long v = idx < nb ? part[idx] : 0ull;
+        const unsigned long long v = idx < nb ? part[q * nb + idx] : 0ull;
         unsigned long long tot;
         const unsigned long long ex = block_excl(v, s_w, tot);
-        if (idx < nb) part[idx] = carry + ex;
+        if (idx < nb) part[q * nb + idx] = carry + ex;
         carry += tot;
     }
-    if (threadIdx.x == 0) *total = carry;
+    if (threadIdx.x == 0) total[q] = carry;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t *__restrict__ in, int64_t n,
-                                                            const unsigned long long *__restrict__ part,
-                                                            uint32_t *__restrict__ out) {
+// in place: each block reads its tile before writing it; coalesced striped loads/stores through
+// shared memory, each thread scanning 16 consecutive elements (padded rows: no bank conflicts)
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(Scan3 io, int64_t n,
+                                                            const unsigned long long *__restrict__ part, int nb) {
     __shared__ unsigned long long s_w[kScanThreads / 32];
-    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;  // blocked
-    uint32_t v[kScanItems];
-    unsigned long long sum = 0;
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t idx = base + k;
-        v[k] = idx < n ? in[idx] : 0u;
-        sum += v[k];
-    }
-    unsigned long long tot;
-    unsigned long long run = block_excl(sum, s_w, tot) + part[blockIdx.x];
-    for (int k = 0; k < kScanItems; ++k) {
-        const int64_t idx = base + k;
-        if (idx < n) out[idx] = (uint32_t)run;
-        run += v[k];
+    __shared__ uint32_t s_v[kScanThreads * (kScanItems + 1)];
+    const int64_t tile = (int64_t)blockIdx.x * kScanTile;
+    const int t = threadIdx.x;
+    for (int q = 0; q < 3; ++q) {
+        for (int k = 0; k < kScanItems; ++k) {  // striped global -> blocked shared
+            const int e = k * kScanThreads + t;
+            const int64_t idx = tile + e;
+            s_v[(e / kScanItems) * (kScanItems + 1) + e % kScanItems] = idx < n ? io.a[q][idx] : 0u;
+        }
+        __syncthreads();
+        uint32_t *mine = s_v + t * (kScanItems + 1);
+        unsigned long long sum = 0;
+        for (int k = 0; k < kScanItems; ++k) sum += mine[k];
+        unsigned long long tot;
+        unsigned long long run = block_excl(sum, s_w, tot) + part[q * nb + blockIdx.x];
+        for (int k = 0; k < kScanItems; ++k) {
+            const uint32_t v = mine[k];
+            mine[k] = (uint32_t)run;
+            run += v;
+        }
+        __syncthreads();
+        for (int k = 0; k < kScanItems; ++k) {  // blocked shared -> striped global
+            const int e = k * kScanThreads + t;
+            const int64_t idx = tile + e;
+            if (idx < n) io.a[q][idx] = s_v[(e / kScanItems) * (kScanItems + 1) + e % kScanItems];
+        }
+        __syncthreads();
     }
 }
 
-void exclusive_scan(const uint32_t *in, int64_t n, uint32_t *out, unsigned long long *total,
-                    unsigned long long *part, cudaStream_t s) {
+void exclusive_scan3(Scan3 io, int64_t n, unsigned long long *total, unsigned long long *part, cudaStream_t s) {
     const int nb = (int)((n + kScanTile - 1) / kScanTile);
-    k_scan_reduce<<<nb, kScanThreads, 0, s>>>(in, n, part);
+    k_scan_reduce<<<nb, kScanThreads, 0, s>>>(io, n, part, nb);
     FGL_LAUNCHED("k_scan_reduce");
-    k_scan_parts<<<1, kScanThreads, 0, s>>>(part, nb, total);
+    k_scan_parts<<<3, kScanThreads, 0, s>>>(part, nb, total);
     FGL_LAUNCHED("k_scan_parts");
-    k_scan_down<<<nb, kScanThreads, 0, s>>>(in, n, part, out);
+    k_scan_down<<<nb, kScanThreads, 0, s>>>(io, n, part, nb);
     FGL_LAUNCHED("k_scan_down");
 }
 
@@ -618,6 +688,11 @@ __global__ void k_mc_totals(const unsigned long long *ne, const unsigned long lo
 }  // namespace
 
 // ---- launchers ---------------------------------------------------------------------------------
+// 64 x 4 thread blocks over (x, row = (y, z)) for the row-wise kernels
+static dim3 grid2d(const Dims &d) {
+    return dim3((d.nx + 63) / 64, std::min((d.ny * d.nz + 3) / 4, 65535));
+}
+
 static Dims mkdims(const int *dims) {
     Dims d;
     d.nx = dims[0], d.ny = dims[1], d.nz = dims[2];
@@ -640,7 +715,7 @@ void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, 
         double sum = 0;
         for (int k = -t.R; k <= t.R; ++k) sum += std::exp(-0.5 * (k / sv) * (k / sv));
         for (int k = -t.R; k <= t.R; ++k) t.w[k + t.R] = (float)(std::exp(-0.5 * (k / sv) * (k / sv)) / sum);
-        k_blur<<<grid1d(d.n()), 256, 0, s>>>(occ, src, dst[ax], d, ax, t);
+        k_blur<<<grid2d(d), dim3(64, 4), 0, s>>>(occ, src, dst[ax], d, ax, t);
         FGL_LAUNCHED("k_blur");
         src = dst[ax];
     }
@@ -656,11 +731,12 @@ void launch_tsdf(const uint32_t *occ, const int *dims, const float *spacing, flo
     uint8_t *oroot = salloc<uint8_t>(d.n(), s), *kappa = salloc<uint8_t>(d.n(), s);
     uint32_t *v0 = salloc<uint32_t>(d.nw(), s), *v1 = salloc<uint32_t>(d.nw(), s);
     FGL_CUDA(cudaMemsetAsync(oroot, 0, d.n(), s));
-    k_cc_init<<<grid1d(d.n()), 256, 0, s>>>(occ, d, lab);
+    const dim3 g2 = grid2d(d);
+    k_cc_init<<<g2, dim3(64, 4), 0, s>>>(occ, d, lab);
     FGL_LAUNCHED("k_cc_init");
-    k_cc_merge<<<grid1d(d.n()), 256, 0, s>>>(d, lab);
+    k_cc_merge<<<g2, dim3(64, 4), 0, s>>>(occ, d, lab);
     FGL_LAUNCHED("k_cc_merge");
-    k_cc_flatten<<<grid1d(d.n()), 256, 0, s>>>(d, lab, oroot);
+    k_cc_flatten<<<g2, dim3(64, 4), 0, s>>>(occ, d, lab, oroot);
     FGL_LAUNCHED("k_cc_flatten");
     k_s0<<<grid1d(d.nw()), 256, 0, s>>>(occ, d, v0, kappa);
     FGL_LAUNCHED("k_s0");
@@ -686,12 +762,12 @@ void launch_marching_cubes(const float *phi, const int *dims, const float *origi
     uint8_t *eflag = salloc<uint8_t>(n, s);
     uint32_t *ecnt = salloc<uint32_t>(n, s), *tcnt = salloc<uint32_t>(n, s), *ccnt = salloc<uint32_t>(n, s);
     const int nb = (int)((n + kScanTile - 1) / kScanTile);
-    unsigned long long *part = salloc<unsigned long long>(nb, s), *tot = salloc<unsigned long long>(3, s);
+    unsigned long long *part = salloc<unsigned long long>(3 * (size_t)nb, s), *tot = salloc<unsigned long long>(3, s);
     k_mc_count<<<grid1d(n), 256, 0, s>>>(phi, d, iso, eflag, ecnt, tcnt, ccnt);
     FGL_LAUNCHED("k_mc_count");
-    exclusive_scan(ecnt, n, ecnt, tot + 0, part, s);  // in place: each block reads before it writes
-    exclusive_scan(tcnt, n, tcnt, tot + 1, part, s);
-    exclusive_scan(ccnt, n, ccnt, tot + 2, part, s);
+    Scan3 io;
+    io.a[0] = ecnt, io.a[1] = tcnt, io.a[2] = ccnt;
+    exclusive_scan3(io, n, tot, part, s);
     McArgs a;
     for (int q = 0; q < 3; ++q) a.o[q] = origin[q], a.sp[q] = spacing[q];
     a.iso = iso, a.vcap = verts ? vcap : 0, a.tcap = tris ? tcap : 0;

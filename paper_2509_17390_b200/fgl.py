@@ -579,11 +579,12 @@ def _vol_args(dims, spacing):
     return d, sp
 
 
-def denoise(occupancy: torch.Tensor, dims, spacing, sigma: float, tau: float, vprime: bool = False, stream=None):
+def denoise(occupancy: torch.Tensor, dims, spacing, sigma: float, tau: float, vprime: bool = False, out=None,
+            stream=None):
     """Eqs. 13-14a on a device bit volume: returns the re-thresholded bit volume (and V' float32
     [nz][ny][nx] when vprime)."""
     d, sp = _vol_args(dims, spacing)
-    out = torch.empty_like(occupancy)
+    out = torch.empty_like(occupancy) if out is None else out
     vp = torch.empty((int(dims[2]), int(dims[1]), int(dims[0])), dtype=torch.float32,
                      device=occupancy.device) if vprime else None
     _check(lib().fgl_denoise(occupancy.data_ptr(), d, sp, float(sigma), float(tau), out.data_ptr(), _ptr(vp),
