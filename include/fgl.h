@@ -53,7 +53,8 @@ enum { FGL_HOST = 0, FGL_DEVICE = 1, FGL_ASYNC = 4 /* or'ed into ptr_kind: see u
 typedef struct fgl_scene fgl_scene; /* opaque: device copies of the mesh, the BVH and scratch */
 
 typedef struct {
-    int32_t morton_bits; /* b of Eq. 5, 1..21; 0 = default 13 (39-bit keys, R7)     */
+    int32_t morton_bits; /* b of Eq. 5, 1..21; 0 = default: 10 below 2^22 primitives
+                            (30-bit keys, 4 sort passes), else 13 (39-bit keys), R7              */
     int32_t leaf_size;   /* max triangles per BVH leaf, 1..8; 0 = default (2)                 */
     int32_t morton_box;  /* 0 = cubic scene box (default): every axis uses L = max_a L_a, the box
                             [o, o+L] read as a cube (isotropic cells; reading R22);

@@ -210,12 +210,12 @@ def test_build_rooms_full_size(fgl):
     m = synth.scene_rooms(2)
     s = fgl.Scene(m.verts, m.tris)
     g = s.export()
-    o = oracle.lbvh(m.verts, m.tris, bits=13, cubic=True)  # library defaults: b = 13, cubic box (R7, R22)
+    o = oracle.lbvh(m.verts, m.tris, bits=10, cubic=True)  # library defaults below 2^22: b = 10, cubic box (R7, R22)
     for k_g, k_o in (("codes", "code"), ("sorted_keys", "sorted_keys"), ("perm", "perm"), ("child", "child"),
                      ("range", "range"), ("leaf_box", "leaf_box"), ("node_box", "node_box")):
         assert np.array_equal(g[k_g], o[k_o]), k_g
     st = s.stats()
-    assert st["triangles"] == m.T and st["build_ms"] > 0
+    assert st["triangles"] == m.T and st["build_ms"] > 0 and st["morton_bits"] == 10
 
 
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 4095, 4096, 4097, 100_003, 1_000_000, 5_000_011])
