@@ -40,7 +40,7 @@ def _args():
                     help="C1-C5: LiDAR cast (the north star); G1/G2: Gaussian voxelizer (NEXT-2); "
                          "T1/T2: TSDF + Marching Cubes on the G1/G2 occupancy (NEXT-3)")
     ap.add_argument("--poses", type=int, default=None, help="poses per GPU per step")
-    ap.add_argument("--mode", choices=["full", "cast"], default="full",
+    ap.add_argument("--mode", choices=["full", "cast", "refit"], default="full",
                     help="full = upload+build+cast per step (default); cast = cast only on a prebuilt scene")
     ap.add_argument("--leaf-size", type=int, default=0, help="0 = library default")
     ap.add_argument("--width", type=int, default=0, help="BVH node width 2 or 4 (0 = library default)")
@@ -661,6 +661,8 @@ def main():
         if a.mode == "full":
             scene.upload(verts_d, tris_d, sync=False)  # A1 (D2D copy + validation, checked after the run)
             scene.build()                        # A2-A7
+        elif a.mode == "refit":
+            scene.refit(verts_d, sync=False)     # NEXT-4: new positions, boxes + nodes refitted, tree kept
         if cast_ev:
             cast_ev[0].record(stream)
         if peer is not None:
@@ -825,7 +827,8 @@ def main():
             "data": "synthetic",
             "config": {"workload": _describe(cfg, P, world), "step": "upload+build+cast" + ("+allgather(nccl)" if gather is not None else "")
                        + ("+allgather(fused P2P)" if peer is not None else "")
-                       if a.mode == "full" else "cast only (prebuilt scene)",
+                       if a.mode == "full" else ("refit+cast (NEXT-4 dynamic mesh: tree kept)" if a.mode == "refit"
+                                                 else "cast only (prebuilt scene)"),
                        "triangles": m.T, "rays_per_step": total_rays, "poses_per_step": P * world,
                        "l2": "flushed between steps (256 MiB memset, untimed)" if flush is not None else "not flushed",
                        "launch": "one CUDA graph replay per step" if graph is not None else "eager launches",

@@ -115,6 +115,15 @@ FGL_API fgl_status fgl_scene_build(fgl_scene *scene, const fgl_build_opts *opts,
 /* Synchronises `cuda_stream` and returns FGL_E_DATA if the last upload failed validation. */
 FGL_API fgl_status fgl_scene_check(fgl_scene *scene, void *cuda_stream);
 
+/* Refit for a deforming mesh (dynamic scenes are the paper's future work,
+ * P:435): new vertex positions verts [V][3] (same V and triangles as the upload, FGL_HOST /
+ * FGL_DEVICE | FGL_ASYNC) replace the old ones; the leaf records, leaf boxes, Eq. 7 node boxes
+ * (exact unions over each node's stored leaf range) and nodes are recomputed while the Morton
+ * order and the tree topology of the last build are kept (casts stay exact; the tree degrades
+ * only in quality as the mesh moves away from the built pose). Recorded as build_ms.
+ * FGL_E_USAGE: not built, V differs, a Gaussian scene; FGL_E_DATA: non-finite vertex. */
+FGL_API fgl_status fgl_scene_refit(fgl_scene *scene, const float *verts, int64_t V, int ptr_kind, void *cuda_stream);
+
 /* Fills *out. Synchronises on the last build's end event (for build_ms and the scene box). */
 FGL_API fgl_status fgl_scene_stats(fgl_scene *scene, fgl_stats *out);
 

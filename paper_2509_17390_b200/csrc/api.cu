@@ -554,6 +554,33 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     FGL_API_END
 }
 
+fgl_status fgl_scene_refit(fgl_scene *s, const float *verts, int64_t V, int ptr_kind, void *stream) {
+    FGL_API_BEGIN
+    check_built(s);
+    if (s->gauss) throw Error(FGL_E_USAGE, "refit is for triangle / point scenes");
+    const bool async = (ptr_kind & FGL_ASYNC) != 0;
+    ptr_kind &= ~FGL_ASYNC;
+    if (ptr_kind != FGL_HOST && ptr_kind != FGL_DEVICE) throw Error(FGL_E_USAGE, "ptr_kind must be FGL_HOST or FGL_DEVICE");
+    if (!verts) throw Error(FGL_E_USAGE, "verts is NULL");
+    if (V != s->V) throw Error(FGL_E_USAGE, "refit needs the uploaded vertex count (same topology)");
+    DeviceGuard g(s->dev);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    FGL_CUDA(cudaStreamIsCapturing(st, &cap));
+    const bool timed = cap == cudaStreamCaptureStatusNone;
+    FGL_CUDA(cudaMemcpyAsync(s->verts, verts, sizeof(float) * 3 * V,
+                             ptr_kind == FGL_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st));
+    fgl::launch_validate(s->verts, V, s->tris, s->T, s->vflag, st);
+    if (timed) FGL_CUDA(cudaEventRecord(s->ev0, st));
+    fgl::launch_refit(s->verts, s->V, s->tris, s->b, s->leaf_size, st);
+    if (timed) FGL_CUDA(cudaEventRecord(s->ev1, st));
+    if (async) return FGL_OK;
+    FGL_CUDA(cudaMemcpyAsync(s->hflag, s->vflag, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+    FGL_CUDA(cudaStreamSynchronize(st));
+    if (*s->hflag & 2u) throw Error(FGL_E_DATA, "non-finite vertex coordinate");
+    FGL_API_END
+}
+
 fgl_status fgl_scene_stats(fgl_scene *s, fgl_stats *out) {
     FGL_API_BEGIN
     if (!s || !out) throw Error(FGL_E_USAGE, "NULL argument");

@@ -289,6 +289,19 @@ __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, 
     }
 }
 
+// Refit (dynamic meshes): Eq. 7 boxes of every internal node from its stored leaf
+// range over the new leaf boxes; the topology (Morton order, Karras tree) is kept.
+__global__ void __launch_bounds__(256) k_refit_boxes(int n, const int2 *__restrict__ range, AggLevels L,
+                                                     float4 *__restrict__ nodebox) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    const int2 r = range[i];
+    float4 lo, hi;
+    range_box(L, r.x, r.y, lo, hi);
+    nodebox[2 * i] = lo;
+    nodebox[2 * i + 1] = hi;
+}
+
 // Leaf-order gather: tri48[j] = triangle perm[j] {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}, its exact
 // box leafbox[j], and the union of every 8 consecutive leaf boxes (agg[0], 8-lane reduction).
 __device__ __forceinline__ void warp_union(float4 &lo, float4 &hi) {
@@ -564,10 +577,8 @@ void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s) {
 
 // Karras tree (A5), Eq. 7 boxes (A6) and traversal nodes (A7) from the leaf boxes and the first
 // aggregate level written by the primitive-specific reorder kernel.
-void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s) {
+static AggLevels launch_aggregates(BuildBuffers &b, cudaStream_t s) {
     const int64_t T = b.T;
-    b.width = width;
-    b.quantized = width == 4 ? quantized : 0;
     AggLevels L;
     L.leaf = b.leafbox;
     L.agg = b.agg;
@@ -578,31 +589,69 @@ void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaS
         FGL_LAUNCHED("k_aggregate");
         ++L.nlev;
     }
-    if (T == 1) {
-        if (width == 4) {
-            k_single4<<<1, 1, 0, s>>>(b.leafbox, b.nodes4, b.quantized);
-            FGL_LAUNCHED("k_single4");
-        } else {
-            k_single<<<1, 1, 0, s>>>(b.leafbox, b.nodes);
-            FGL_LAUNCHED("k_single");
-        }
-        return;
-    }
-    k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[b.sorted_slot], (int)T, b.packed_shift, b.child,
-                                                            b.range, b.parent, L, b.nodebox);
-    FGL_LAUNCHED("k_karras");
+    return L;
+}
+
+static void launch_nodes(BuildBuffers &b, int leaf_size, int width, bool depth_known, cudaStream_t s) {
+    const int64_t T = b.T;
     if (width == 2) {
         k_nodes<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.leafbox, b.nodebox,
                                                                b.nodes);
         FGL_LAUNCHED("k_nodes");
     }
     if (width == 4) {
-        k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
-        FGL_LAUNCHED("k_depth");
+        if (!depth_known) {
+            k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
+            FGL_LAUNCHED("k_depth");
+        }
         k_nodes4<<<grid_for(T - 1), 256, 0, s>>>(T, leaf_size, b.child, b.range, b.depth, b.leafbox, b.nodebox,
                                                  b.nodes4, b.quantized);
         FGL_LAUNCHED("k_nodes4");
     }
+}
+
+static void launch_single(BuildBuffers &b, int width, cudaStream_t s) {
+    if (width == 4) {
+        k_single4<<<1, 1, 0, s>>>(b.leafbox, b.nodes4, b.quantized);
+        FGL_LAUNCHED("k_single4");
+    } else {
+        k_single<<<1, 1, 0, s>>>(b.leafbox, b.nodes);
+        FGL_LAUNCHED("k_single");
+    }
+}
+
+void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s) {
+    const int64_t T = b.T;
+    b.width = width;
+    b.quantized = width == 4 ? quantized : 0;
+    AggLevels L = launch_aggregates(b, s);
+    if (T == 1) {
+        launch_single(b, width, s);
+        return;
+    }
+    k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[b.sorted_slot], (int)T, b.packed_shift, b.child,
+                                                            b.range, b.parent, L, b.nodebox);
+    FGL_LAUNCHED("k_karras");
+    launch_nodes(b, leaf_size, width, false, s);
+}
+
+// NEXT-4 refit: new vertex positions, same triangles and tree. Leaf records and boxes are regathered
+// in the stored leaf order, then aggregates, Eq. 7 node boxes from the stored ranges, and nodes.
+void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int leaf_size,
+                  cudaStream_t s) {
+    const int64_t T = b.T;
+    const int ps = b.packed_shift, slot = b.sorted_slot;
+    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
+                                                          ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox, b.agg);
+    FGL_LAUNCHED("k_reorder");
+    AggLevels L = launch_aggregates(b, s);
+    if (T == 1) {
+        launch_single(b, b.width, s);
+        return;
+    }
+    k_refit_boxes<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>((int)T, b.range, L, b.nodebox);
+    FGL_LAUNCHED("k_refit_boxes");
+    launch_nodes(b, leaf_size, b.width, true, s);
 }
 
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,

@@ -124,6 +124,7 @@ void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t
                      cudaStream_t s);
 void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s);
 void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s);
+void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int leaf_size, cudaStream_t s);
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
                           uint64_t *codes, cudaStream_t s);
 

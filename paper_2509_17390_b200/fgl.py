@@ -67,6 +67,7 @@ _SIGS = {
     "fgl_scene_upload_mesh": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_int64, c_int, c_void_p]),
     "fgl_scene_build": (c_int, [c_void_p, c_void_p, c_void_p]),
     "fgl_scene_stats": (c_int, [c_void_p, POINTER(Stats)]),
+    "fgl_scene_refit": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "fgl_scene_check": (c_int, [c_void_p, c_void_p]),
     "fgl_cast_spinning": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p]),
@@ -232,6 +233,20 @@ class Scene:
         o = BuildOpts(morton_bits or self.morton_bits, leaf_size or self.leaf_size, int(mb),
                       int(width or self.width), int(self.quantized), (c_int32 * 3)())
         _check(lib().fgl_scene_build(self._h, ctypes.byref(o), _stream(stream)))
+        return self
+
+    def refit(self, verts, stream=None, sync: bool = True):
+        """New positions for the same vertices (NEXT-4): boxes and nodes recomputed, tree kept."""
+        if isinstance(verts, torch.Tensor) and verts.is_cuda:
+            v = verts.to(torch.float32).contiguous()
+            kind, pv = DEVICE, v.data_ptr()
+        else:
+            v = np.ascontiguousarray(np.asarray(verts.cpu().numpy() if isinstance(verts, torch.Tensor) else verts,
+                                                dtype=np.float32))
+            kind, pv = HOST, v.ctypes.data
+        V = int(np.prod(tuple(v.shape))) // 3
+        _check(lib().fgl_scene_refit(self._h, pv, V, kind | (0 if sync else ASYNC), _stream(stream)))
+        self._refit_keep = v
         return self
 
     def check(self, stream=None):
