@@ -61,7 +61,10 @@ typedef struct {
                             1 = per-axis box, L_x, L_y, L_z separately                         */
     int32_t width;       /* traversal node width: 2 (binary "node64", default) or 4 ("node128")    */
     int32_t quantized;   /* width 4 only: 1 = 8-bit child boxes, outward-rounded ("node64q")      */
-    int32_t reserved[3]; /* must be zero                                                     */
+    int32_t restructure; /* width 2 only: 0 = plain LBVH (default); k = 1..8 passes of agglomerative
+                            treelet restructuring: SAH-guided re-clustering of
+                            7-leaf treelets bottom-up, 1-triangle leaves (leaf_size ignored)     */
+    int32_t reserved[2]; /* must be zero                                                     */
 } fgl_build_opts;
 
 typedef struct {

@@ -85,7 +85,8 @@ void dalloc(fgl_scene *s, T **p, size_t n) {
 void free_build(fgl_scene *s) {
     fgl::BuildBuffers &b = s->b;
     void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.sort_status, b.sort_tiles,
-                  b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth, b.agg};
+                  b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth, b.agg,
+                  b.cost, b.tsize};
     for (void *p : ps)
         if (p) cudaFree(p);
     b = fgl::BuildBuffers();
@@ -125,6 +126,8 @@ void alloc_build(fgl_scene *s, int64_t T) {
         dalloc(s, &b.agg, 2 * tot);
     }
     dalloc(s, &b.depth, nin);
+    dalloc(s, &b.cost, nin);
+    dalloc(s, &b.tsize, nin);
 }
 
 fgl::SceneView view(const fgl_scene *s) {
@@ -519,7 +522,7 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     // default b (R7): 10 bits per axis (30-bit keys, four sort passes) below 4 M primitives, where
     // the cubic cells are already finer than the primitives; 13 above (the 10 M-triangle terrain
     // loses 7% cast speed at b = 10)
-    int bits = s->T < (int64_t(1) << 22) ? 10 : 13, leaf = 2, cubic = 1, width = 2, quant = 0;
+    int bits = s->T < (int64_t(1) << 22) ? 10 : 13, leaf = 2, cubic = 1, width = 2, quant = 0, restructure = 0;
     if (opts) {
         if (opts->quantized < 0 || opts->quantized > 1) throw Error(FGL_E_USAGE, "quantized must be 0 or 1");
         quant = opts->quantized;
@@ -527,8 +530,10 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
         if (width != 2 && width != 4) throw Error(FGL_E_USAGE, "width must be 2 or 4");
         if (opts->morton_box < 0 || opts->morton_box > 1) throw Error(FGL_E_USAGE, "morton_box must be 0 or 1");
         cubic = opts->morton_box == 0;
-        for (int i = 0; i < 3; ++i)
+        for (int i = 0; i < 2; ++i)
             if (opts->reserved[i]) throw Error(FGL_E_USAGE, "fgl_build_opts.reserved must be zero");
+        if (opts->restructure < 0 || opts->restructure > 8) throw Error(FGL_E_USAGE, "restructure must be in [0, 8]");
+        restructure = opts->restructure;
         if (opts->morton_bits) bits = opts->morton_bits;
         if (opts->leaf_size) leaf = opts->leaf_size;
     }
@@ -547,7 +552,8 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
         if (!cubic) throw Error(FGL_E_USAGE, "a Gaussian scene uses the cubic Morton box");
         fgl::launch_gauss_build(s->verts, s->g_quat, s->g_scale, s->g_opac, s->kappa, s->b, bits, leaf, st);
     } else {
-        fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, quant, st);
+        if (restructure && width != 2) throw Error(FGL_E_USAGE, "restructure needs width 2");
+        fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, quant, st, restructure);
     }
     if (timed) FGL_CUDA(cudaEventRecord(s->ev1, st));
     s->built = true;

@@ -302,6 +302,168 @@ __global__ void __launch_bounds__(256) k_refit_boxes(int n, const int2 *__restri
     nodebox[2 * i + 1] = hi;
 }
 
+// ---- NEXT-4: agglomerative treelet restructuring (after Karras & Aila 2013, Domingues & Pedrini
+// 2015) -------------------------------------------------------------------------------------------
+// Bottom-up over the binary tree (one thread per leaf climbing; the second thread to reach a node
+// processes it, so a node is handled after both subtrees). At every node whose subtree holds >= 7
+// leaves, a treelet of up to 7 leaves is formed by repeatedly opening the treelet leaf with the
+// largest surface area; the treelet is re-clustered greedily (merge the pair whose union has the
+// smallest area) and the new topology is kept when it lowers the SAH cost
+// C(n) = C_i A(n) + C(left) + C(right), C(leaf) = C_t A(leaf). The node boxes stay exact unions.
+// Leaves are single triangles (a treelet may regroup any of them).
+constexpr float kCi = 1.2f, kCt = 1.0f;
+constexpr int kTreeletLeaves = 7;
+
+__device__ __forceinline__ float area(const float4 &lo, const float4 &hi) {
+    const float dx = hi.x - lo.x, dy = hi.y - lo.y, dz = hi.z - lo.z;
+    return 2.f * (dx * dy + dy * dz + dz * dx);
+}
+
+struct TRef {
+    int32_t ref;  // internal node index, or ~leaf
+    float4 lo, hi;
+    float cost;
+    int32_t size;
+};
+
+__device__ __forceinline__ void load_ref(TRef &t, int32_t ref, const float4 *nodebox, const float4 *leafbox,
+                                         const float *cost, const int32_t *size) {
+    t.ref = ref;
+    if (ref >= 0) {
+        t.lo = __ldcg(nodebox + 2 * (int64_t)ref), t.hi = __ldcg(nodebox + 2 * (int64_t)ref + 1);
+        t.cost = __ldcg(cost + ref), t.size = __ldcg(size + ref);
+    } else {
+        t.lo = __ldg(leafbox + 2 * (int64_t)~ref), t.hi = __ldg(leafbox + 2 * (int64_t)~ref + 1);
+        t.cost = kCt * area(t.lo, t.hi), t.size = 1;
+    }
+}
+
+__device__ __forceinline__ void unite(float4 &lo, float4 &hi, const float4 &l2, const float4 &h2) {
+    lo.x = fminf(lo.x, l2.x), lo.y = fminf(lo.y, l2.y), lo.z = fminf(lo.z, l2.z);
+    hi.x = fmaxf(hi.x, h2.x), hi.y = fmaxf(hi.y, h2.y), hi.z = fmaxf(hi.z, h2.z);
+}
+
+__device__ void treelet_node(int32_t n, int32_t T, int2 *child, int32_t *parent, float4 *nodebox,
+                             const float4 *leafbox, float *cost, int32_t *size, bool restructure) {
+    // node n's box, cost and size from its (final) children
+    const int2 c = __ldcg(child + n);
+    TRef a, b;
+    load_ref(a, c.x, nodebox, leafbox, cost, size);
+    load_ref(b, c.y, nodebox, leafbox, cost, size);
+    float4 lo = a.lo, hi = a.hi;
+    unite(lo, hi, b.lo, b.hi);
+    const float cn = kCi * area(lo, hi) + a.cost + b.cost;
+    const int32_t sz = a.size + b.size;
+    nodebox[2 * (int64_t)n] = lo, nodebox[2 * (int64_t)n + 1] = hi;
+    cost[n] = cn;
+    size[n] = sz;
+    if (!restructure || sz < kTreeletLeaves) return;
+    // form the treelet: open the largest-area internal treelet leaf until there are 7 leaves
+    TRef L[kTreeletLeaves];
+    int32_t I[kTreeletLeaves - 1];
+    int nl = 2, ni = 1;
+    L[0] = a, L[1] = b, I[0] = n;
+    while (nl < kTreeletLeaves) {
+        int best = -1;
+        float ba = -1.f;
+        for (int k = 0; k < nl; ++k)
+            if (L[k].ref >= 0) {
+                const float ar = area(L[k].lo, L[k].hi);
+                if (ar > ba) ba = ar, best = k;
+            }
+        if (best < 0) break;
+        const int32_t r = L[best].ref;
+        I[ni++] = r;
+        const int2 cc = __ldcg(child + r);
+        load_ref(L[best], cc.x, nodebox, leafbox, cost, size);
+        load_ref(L[nl++], cc.y, nodebox, leafbox, cost, size);
+    }
+    // old cost of the treelet's internal nodes = cost(n) - sum of leaf costs
+    float leafsum = 0.f;
+    for (int k = 0; k < nl; ++k) leafsum += L[k].cost;
+    const float old_internal = cn - leafsum;
+    // greedy agglomeration: merge the pair with the smallest union area; internal slots I[ni-1..0]
+    // (the last merge takes I[0] = n, so the treelet root keeps its index and parent)
+    TRef W[kTreeletLeaves];
+    for (int k = 0; k < nl; ++k) W[k] = L[k];
+    int nw = nl;
+    int2 newc[kTreeletLeaves - 1];
+    float new_internal = 0.f;
+    int slot = ni - 1;
+    float4 nlo[kTreeletLeaves - 1], nhi[kTreeletLeaves - 1];
+    float ncost[kTreeletLeaves - 1];
+    int32_t nsize[kTreeletLeaves - 1];
+    while (nw > 1) {
+        int bi = 0, bj = 1;
+        float bu = INFINITY;
+        for (int i = 0; i < nw; ++i)
+            for (int j = i + 1; j < nw; ++j) {
+                float4 ul = W[i].lo, uh = W[i].hi;
+                unite(ul, uh, W[j].lo, W[j].hi);
+                const float u = area(ul, uh);
+                if (u < bu) bu = u, bi = i, bj = j;
+            }
+        TRef m;
+        m.lo = W[bi].lo, m.hi = W[bi].hi;
+        unite(m.lo, m.hi, W[bj].lo, W[bj].hi);
+        const float ic = kCi * area(m.lo, m.hi);
+        new_internal += ic;
+        m.cost = ic + W[bi].cost + W[bj].cost;
+        m.size = W[bi].size + W[bj].size;
+        m.ref = I[slot];
+        newc[slot] = make_int2(W[bi].ref, W[bj].ref);
+        nlo[slot] = m.lo, nhi[slot] = m.hi, ncost[slot] = m.cost, nsize[slot] = m.size;
+        --slot;
+        W[bi] = m;
+        W[bj] = W[--nw];
+    }
+    if (!(new_internal < old_internal * (1.f - 1e-5f))) return;
+    for (int k = 0; k < ni; ++k) {
+        const int32_t idx = I[k];
+        child[idx] = newc[k];
+        nodebox[2 * (int64_t)idx] = nlo[k], nodebox[2 * (int64_t)idx + 1] = nhi[k];
+        cost[idx] = ncost[k];
+        size[idx] = nsize[k];
+        const int32_t r0 = newc[k].x, r1 = newc[k].y;
+        parent[r0 >= 0 ? r0 : (T - 1) + ~r0] = idx;
+        parent[r1 >= 0 ? r1 : (T - 1) + ~r1] = idx;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_treelet(int32_t T, int2 *child, int32_t *parent, float4 *nodebox,
+                                                 const float4 *__restrict__ leafbox, float *cost, int32_t *size,
+                                                 unsigned int *counter, int restructure) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= T) return;
+    int32_t n = __ldcg(parent + (T - 1) + j);
+    while (n >= 0) {
+        __threadfence();
+        if (atomicAdd(counter + n, 1u) == 0u) return;  // the sibling subtree is not done yet
+        __threadfence();
+        treelet_node(n, T, child, parent, nodebox, leafbox, cost, size, restructure != 0);
+        __threadfence();
+        n = __ldcg(parent + n);
+    }
+}
+
+// traversal nodes for single-triangle leaves from child refs and boxes (any topology)
+__global__ void __launch_bounds__(256) k_nodes_free(int64_t n, const int2 *__restrict__ child,
+                                                    const float4 *__restrict__ leafbox,
+                                                    const float4 *__restrict__ nodebox, Node64 *__restrict__ nodes) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n - 1) return;
+    const int2 c = child[i];
+    const float4 *b0 = c.x >= 0 ? nodebox + 2 * (int64_t)c.x : leafbox + 2 * (int64_t)(~c.x);
+    const float4 *b1 = c.y >= 0 ? nodebox + 2 * (int64_t)c.y : leafbox + 2 * (int64_t)(~c.y);
+    const float4 l0 = b0[0], h0 = b0[1], l1 = b1[0], h1 = b1[1];
+    Node64 nd;
+    nd.a = make_float4(l0.x, h0.x, l0.y, h0.y);
+    nd.b = make_float4(l1.x, h1.x, l1.y, h1.y);
+    nd.c = make_float4(l0.z, h0.z, l1.z, h1.z);
+    nd.d = make_int4(c.x >= 0 ? c.x : make_leaf(~c.x, 1), c.y >= 0 ? c.y : make_leaf(~c.y, 1), 0, 0);
+    nodes[i] = nd;
+}
+
 // Leaf-order gather: tri48[j] = triangle perm[j] {v0.xyz, id}, {v1.xyz, 0}, {v2.xyz, 0}, its exact
 // box leafbox[j], and the union of every 8 consecutive leaf boxes (agg[0], 8-lane reduction).
 __device__ __forceinline__ void warp_union(float4 &lo, float4 &hi) {
@@ -620,10 +782,11 @@ static void launch_single(BuildBuffers &b, int width, cudaStream_t s) {
     }
 }
 
-void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s) {
+void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s, int restructure) {
     const int64_t T = b.T;
     b.width = width;
     b.quantized = width == 4 ? quantized : 0;
+    b.restructured = 0;
     AggLevels L = launch_aggregates(b, s);
     if (T == 1) {
         launch_single(b, width, s);
@@ -632,6 +795,20 @@ void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaS
     k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[b.sorted_slot], (int)T, b.packed_shift, b.child,
                                                             b.range, b.parent, L, b.nodebox);
     FGL_LAUNCHED("k_karras");
+    if (restructure > 0 && width == 2) {
+        // costs / sizes bottom-up once, then `restructure` treelet passes; nodes over 1-triangle leaves
+        for (int pass = 0; pass <= restructure; ++pass) {
+            FGL_CUDA(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * (T - 1), s));
+            k_treelet<<<(unsigned)((T + 255) / 256), 256, 0, s>>>((int32_t)T, b.child, b.parent, b.nodebox, b.leafbox,
+                                                                  b.cost, b.tsize,
+                                                                  reinterpret_cast<unsigned int *>(b.flags), pass);
+            FGL_LAUNCHED("k_treelet");
+        }
+        k_nodes_free<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, b.child, b.leafbox, b.nodebox, b.nodes);
+        FGL_LAUNCHED("k_nodes_free");
+        b.restructured = 1;
+        return;
+    }
     launch_nodes(b, leaf_size, width, false, s);
 }
 
@@ -649,13 +826,23 @@ void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
         launch_single(b, b.width, s);
         return;
     }
+    if (b.restructured) {  // free topology: boxes bottom-up over the kept child links
+        FGL_CUDA(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * (T - 1), s));
+        k_treelet<<<(unsigned)((T + 255) / 256), 256, 0, s>>>((int32_t)T, b.child, b.parent, b.nodebox, b.leafbox,
+                                                              b.cost, b.tsize, reinterpret_cast<unsigned int *>(b.flags),
+                                                              0);
+        FGL_LAUNCHED("k_treelet");
+        k_nodes_free<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, b.child, b.leafbox, b.nodebox, b.nodes);
+        FGL_LAUNCHED("k_nodes_free");
+        return;
+    }
     k_refit_boxes<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>((int)T, b.range, L, b.nodebox);
     FGL_LAUNCHED("k_refit_boxes");
     launch_nodes(b, leaf_size, b.width, true, s);
 }
 
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  int cubic, int width, int quantized, cudaStream_t s) {
+                  int cubic, int width, int quantized, cudaStream_t s, int restructure) {
     const int64_t T = b.T;
     k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
     FGL_LAUNCHED("k_prep");
@@ -665,7 +852,7 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
     k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
                                                           ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox, b.agg);
     FGL_LAUNCHED("k_reorder");
-    launch_tree(b, leaf_size, width, quantized, s);
+    launch_tree(b, leaf_size, width, quantized, s, restructure);
 }
 
 }  // namespace fgl

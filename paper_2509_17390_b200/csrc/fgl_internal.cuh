@@ -103,6 +103,9 @@ struct BuildBuffers {
     int width = 4;
     int sorted_slot = 0;           // which keys/vals buffer holds the sorted result
     int packed_shift = 0;          // > 0: keys hold (code << packed_shift) | triangle index, no vals
+    float *cost = nullptr;         // [T-1] SAH cost of each internal node's subtree (restructuring)
+    int32_t *tsize = nullptr;      // [T-1] leaves under each internal node (restructuring)
+    int restructured = 0;          // 1: treelet-restructured tree (1-triangle leaves, free topology)
 };
 
 constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
@@ -119,11 +122,11 @@ void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *g
 
 // build.cu
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  int cubic, int width, int quantized, cudaStream_t s);
+                  int cubic, int width, int quantized, cudaStream_t s, int restructure = 0);
 void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
                      cudaStream_t s);
 void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s);
-void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s);
+void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s, int restructure = 0);
 void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int leaf_size, cudaStream_t s);
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
                           uint64_t *codes, cudaStream_t s);

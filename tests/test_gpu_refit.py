@@ -91,3 +91,60 @@ def test_refit_errors(fgl):
     u = fgl.Scene(build=False)
     with pytest.raises(fgl.FglError):
         u.refit(m.verts)
+
+
+# ---- NEXT-4 treelet restructuring --------------------------------------------------------------
+def _tree_checks(ex, T):
+    child, nb, lb = ex["child"], ex["node_box"].astype(np.float64), ex["leaf_box"].astype(np.float64)
+    seen = np.zeros(T, int)
+    stack, depth = [(0, 0)], 0
+    lo = np.zeros((T - 1, 3))
+    while stack:
+        n, d = stack.pop()
+        depth = max(depth, d)
+        for c in child[n]:
+            if c < 0:
+                seen[~c] += 1
+            else:
+                stack.append((c, d + 1))
+    assert np.all(seen == 1)  # every triangle exactly once
+    # every node box is the union of its two children's boxes (Eq. 7 on the new topology)
+    def box(c):
+        return lb[~c] if c < 0 else nb[c]
+    for n in range(T - 1):
+        a, b = box(child[n][0]), box(child[n][1])
+        assert np.array_equal(nb[n, :3], np.minimum(a[:3], b[:3])) and np.array_equal(nb[n, 3:], np.maximum(a[3:], b[3:]))
+    return depth
+
+
+@pytest.mark.parametrize("passes", [1, 3])
+def test_restructure_tree_valid_and_cast_parity(fgl, passes):
+    cfg = synth.config("C1")
+    m, pat, poses = cfg["mesh"], cfg["pattern"], cfg["poses"]
+    s = fgl.Scene(m.verts, m.tris, restructure=passes)
+    depth = _tree_checks(s.export(), m.T)
+    assert depth < 90
+    res = s.cast(poses, pat)
+    o, d = fgl.export_rays(pat, poses)
+    vd = oracle.cast_and_classify(m.verts, m.tris, o.cpu().numpy().astype(np.float64),
+                                  d.cpu().numpy().astype(np.float64), pat.t_min, pat.t_max, eps_rel=oracle.EPS_MODE_B)
+    j = oracle.judge(vd, res["range"].reshape(-1).cpu().numpy(), res["tri_id"].reshape(-1).cpu().numpy())
+    assert len(j["unamb_mismatch"]) == 0 and len(j["amb_outside"]) == 0
+
+
+def test_restructure_rooms_same_hits_fewer_nodes(fgl):
+    m = synth.scene_rooms(2)
+    plain = fgl.Scene(m.verts, m.tris)
+    rs = fgl.Scene(m.verts, m.tris, restructure=2)
+    assert _tree_checks(rs.export(), m.T) < 90
+    pat = synth.spinning_preset("HDL64")
+    poses = synth.poses_yaw_offsets((9.0, 7.5, 1.5), 2, 0.01)
+    a = plain.cast(poses, pat, counts=True)
+    b = rs.cast(poses, pat, counts=True)
+    assert (a["tri_id"] == b["tri_id"]).float().mean().item() > 0.9999
+    # a refit of the restructured tree keeps it exact
+    v2 = _deform(m.verts, 0.02)
+    rs.refit(v2)
+    fresh = fgl.Scene(v2, m.tris)
+    c1, c2 = rs.cast(poses, pat), fresh.cast(poses, pat)
+    assert (c1["tri_id"] == c2["tri_id"]).float().mean().item() > 0.9999
