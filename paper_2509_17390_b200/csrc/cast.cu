@@ -742,6 +742,9 @@ __device__ __forceinline__ unsigned long long next_tile(CastCounter *ctr, ChunkS
 #ifndef FGL_REFILL
 #define FGL_REFILL 32
 #endif
+#ifndef FGL_FULLVOTE
+#define FGL_FULLVOTE 1
+#endif
 template <class Gen, bool kCount>
 __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
     k_cast_dyn(const SceneView sv, const Gen gen, int64_t ntiles, const CastOut out, CastCounter *ctr) {
@@ -756,6 +759,8 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
     int32_t cur = kDone, leaf = 0;
     Pre p;
     Hit h{0.f, INT_MAX, 0, 0};
+    float tlim = 0.f;  // h.t * kExpand, the pop bound, updated with h.t
+    const Node64 *__restrict__ nodes = sv.nodes;
     Ray r;
     int64_t idx = 0;
     float tmin = 0.f;
@@ -787,22 +792,34 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
                 if (gen.ray((int64_t)tile, slot, r, idx, tmin, tmax)) {
                     p = precompute(r);
                     h = Hit{tmax, INT_MAX, 0, 0};
+                    tlim = tmax * kExpand;
                     sp = 0, cur = 0, leaf = 0;
                     active = true;
                 }
             }
         }
+#if !FGL_FULLVOTE
         if (!active) continue;
+#endif
         // ---- one outer iteration of the while-while traversal ----
         auto pop = [&]() -> int32_t {
             while (sp > 0) {
                 --sp;
-                if (__uint_as_float((uint32_t)(st[sp] >> 32)) <= h.t * kExpand) return (int32_t)(uint32_t)st[sp];
+                if (__uint_as_float((uint32_t)(st[sp] >> 32)) <= tlim) return (int32_t)(uint32_t)st[sp];
             }
             return kDone;
         };
+#if FGL_FULLVOTE
+        // every lane of the warp runs the loop (idle / finished lanes predicated off), so the
+        // speculation vote is a plain full-warp vote (no __activemask)
+        while (true) {
+            const bool go = active && cur >= 0 && cur != kDone;
+            if (go) {
+#else
         while (cur >= 0 && cur != kDone) {
-            const float4 *np = reinterpret_cast<const float4 *>(sv.nodes + cur);
+            {
+#endif
+            const float4 *np = reinterpret_cast<const float4 *>(nodes + cur);
             const float4 na = __ldg(np), nb = __ldg(np + 1), nc = __ldg(np + 2);
             const int4 nd = __ldg(reinterpret_cast<const int4 *>(np + 3));
             if (kCount) ++h.nodes;
@@ -835,12 +852,16 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
                 leaf = cur;
                 cur = pop();
             }
-            #if FGL_SPECULATE
+            }
+#if FGL_FULLVOTE
+            if (!__any_sync(kFull, go && leaf == 0)) break;
+#elif FGL_SPECULATE
             if (!__any_sync(__activemask(), leaf == 0)) break;
 #else
             if (leaf != 0) break;
 #endif
         }
+        if (!active) continue;
         while (leaf < 0) {
             const int32_t v = ~leaf;
             const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
@@ -853,6 +874,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
                 if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, t)) {
                     h.t = t;
                     h.id = id;
+                    tlim = t * kExpand;
                 }
             }
             leaf = 0;
