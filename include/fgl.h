@@ -259,6 +259,14 @@ FGL_API fgl_status fgl_voxelize(const fgl_scene *scene, const fgl_grid *grid, fl
 FGL_API fgl_status fgl_denoise(const uint32_t *occupancy, const int32_t *dims, const float *spacing, float sigma,
                                float tau, uint32_t *out, float *vprime, void *cuda_stream);
 
+/* Eq. 13-14b: as fgl_denoise, but the threshold is Quantile_q(V') over the whole grid, read as the
+ * inverted-CDF quantile: the value of 1-based rank max(1, ceil(q N)) in ascending order (R35),
+ * selected on the device by a 3-pass radix select of the float32 V' (so V~ = V' >= that value).
+ * threshold (nullable, device float [1]) receives the selected value. q in [0, 1]. */
+FGL_API fgl_status fgl_denoise_quantile(const uint32_t *occupancy, const int32_t *dims, const float *spacing,
+                                        float sigma, float q, uint32_t *out, float *vprime, float *threshold,
+                                        void *cuda_stream);
+
 /* Eqs. 15-17 narrow-band TSDF of a bit volume: s = +1 on free voxels 6-connected to the padded
  * frame (flood fill), -1 elsewhere; kappa = shell index of the 6-neighbour expansion from
  * S_0 = {x : a 6-neighbour differs in V} (the frame counts as free); phi = s min(kappa v_min, r)

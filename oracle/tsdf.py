@@ -1,7 +1,7 @@
 """ORACLE — TEST INFRASTRUCTURE ONLY (see oracle/__init__.py for the rules).
 
 Plain numpy statement of the mesh-reconstruction steps of PAPER.md §IV-B:
-binary denoising (Eq. 13) and fixed re-thresholding (Eq. 14a), the
+binary denoising (Eq. 13) and fixed / quantile re-thresholding (Eq. 14), the
 narrow-band TSDF — outside flood fill from the padded frame, boundary set S_0 (Eq. 15,
 P:206-208), layered shells kappa(x) and delta = kappa v_min (Eq. 16), phi =
 clip(s delta, -r, r) (Eq. 17) — and Marching Cubes on phi (Eq. 18).
@@ -60,6 +60,19 @@ def blur(V, sigma_m: float, spacing):
 def rethreshold(Vp, tau: float):
     """Eq. 14a: V~ = V' >= tau."""
     return np.asarray(Vp) >= tau
+
+
+def quantile(Vp, q: float):
+    """Quantile_q(V') of Eq. 14b read as the inverted-CDF quantile (R35): the value of 1-based rank
+    max(1, ceil(q N)) in ascending order."""
+    v = np.sort(np.asarray(Vp).reshape(-1))
+    k = min(max(1, int(math.ceil(q * v.size))), v.size)
+    return v[k - 1]
+
+
+def rethreshold_quantile(Vp, q: float):
+    """Eq. 14b: V~ = V' >= Quantile_q(V')."""
+    return np.asarray(Vp) >= quantile(Vp, q)
 
 
 # ---- Eqs. 15-17: narrow-band TSDF ------------------------------------------------------------

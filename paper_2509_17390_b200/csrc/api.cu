@@ -449,6 +449,17 @@ fgl_status fgl_denoise(const uint32_t *occupancy, const int32_t *dims, const flo
     FGL_API_END
 }
 
+fgl_status fgl_denoise_quantile(const uint32_t *occupancy, const int32_t *dims, const float *spacing, float sigma,
+                                float q, uint32_t *out, float *vprime, float *threshold, void *stream) {
+    FGL_API_BEGIN
+    check_volume(dims, spacing, (int64_t(1) << 31) - 1);
+    if (!occupancy || !out) throw Error(FGL_E_USAGE, "occupancy / out is NULL");
+    if (!(sigma > 0.f) || !std::isfinite(sigma)) throw Error(FGL_E_USAGE, "sigma must be finite and > 0");
+    if (!(q >= 0.f && q <= 1.f)) throw Error(FGL_E_USAGE, "q must be in [0, 1]");
+    fgl::launch_denoise(occupancy, dims, spacing, sigma, q, out, vprime, (cudaStream_t)stream, 1, threshold);
+    FGL_API_END
+}
+
 fgl_status fgl_tsdf(const uint32_t *occupancy, const int32_t *dims, const float *spacing, float r, float *phi,
                     void *stream) {
     FGL_API_BEGIN

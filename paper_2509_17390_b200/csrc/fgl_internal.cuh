@@ -192,7 +192,7 @@ void launch_voxelize(const BuildBuffers &b, const VoxGrid &g, float kappa, float
                      cudaStream_t s);
 // tsdf.cu
 void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, float sigma, float tau,
-                    uint32_t *out, float *vprime, cudaStream_t s);
+                    uint32_t *out, float *vprime, cudaStream_t s, int quantile = 0, float *thr_out = nullptr);
 void launch_tsdf(const uint32_t *occ, const int *dims, const float *spacing, float r, float *phi, cudaStream_t s);
 void launch_marching_cubes(const float *phi, const int *dims, const float *origin, const float *spacing, float iso,
                            float *verts, float *normals, int64_t vcap, int32_t *tris, int64_t tcap, int64_t *counts,

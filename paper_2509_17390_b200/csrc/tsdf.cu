@@ -68,31 +68,113 @@ struct Taps {
     int R;
 };
 
-// pass 0: bits -> float along x; pass 1, 2: float -> float along y, z. Launch: x = blockIdx.x
-// * 256 + tid, row (y, z) = blockIdx.y (no divisions)
+// pass 0: bits -> float along x; pass 1, 2: float -> float along y, z. 64 x 4 blocks over
+// (x, row = (y, z)); weights staged in shared memory; the tap window is clipped to the grid once
 __global__ void __launch_bounds__(256) k_blur(const uint32_t *__restrict__ bits, const float *__restrict__ in,
                                               float *__restrict__ out, Dims d, int axis, Taps t) {
+    __shared__ float w[kMaxTaps];
+    const int R = t.R;
+    for (int k = threadIdx.y * 64 + threadIdx.x; k < 2 * R + 1; k += 256) w[k] = t.w[k];
+    __syncthreads();
     const int x = blockIdx.x * 64 + threadIdx.x;
     if (x >= d.nx) return;
     for (int row = blockIdx.y * 4 + threadIdx.y; row < d.ny * d.nz; row += gridDim.y * 4) {
-    const int y = row % d.ny, z = row / d.ny;
-    const int64_t i = (int64_t)row * d.nx + x;
-    float acc = 0.f;
-    if (axis == 0) {
-        const uint32_t *rw = bits + (int64_t)row * d.nwx;
-        for (int k = -t.R; k <= t.R; ++k) {
-            const int cc = x + k;
-            if (cc >= 0 && cc < d.nx && ((__ldg(rw + (cc >> 5)) >> (cc & 31)) & 1u)) acc += t.w[k + t.R];
+        const int64_t i = (int64_t)row * d.nx + x;
+        float acc = 0.f;
+        if (axis == 0) {
+            const uint32_t *rw = bits + (int64_t)row * d.nwx;
+            const int lo = max(x - R, 0), hi = min(x + R, d.nx - 1);
+            for (int cc = lo; cc <= hi; ++cc)
+                if ((__ldg(rw + (cc >> 5)) >> (cc & 31)) & 1u) acc += w[cc - x + R];
+        } else {
+            const int y = row % d.ny, z = row / d.ny;
+            const int c = axis == 1 ? y : z, n = axis == 1 ? d.ny : d.nz;
+            const int64_t stride = axis == 1 ? d.nx : (int64_t)d.nx * d.ny;
+            const int lo = max(c - R, 0), hi = min(c + R, n - 1);
+            const float *pp = in + i + (int64_t)(lo - c) * stride;
+            for (int cc = lo; cc <= hi; ++cc, pp += stride) acc = fmaf(w[cc - c + R], __ldg(pp), acc);
         }
-    } else {
-        const int c = axis == 1 ? y : z, n = axis == 1 ? d.ny : d.nz;
-        const int64_t stride = axis == 1 ? d.nx : (int64_t)d.nx * d.ny;
-        for (int k = -t.R; k <= t.R; ++k) {
-            const int cc = c + k;
-            if (cc >= 0 && cc < n) acc = fmaf(t.w[k + t.R], __ldg(in + i + (int64_t)k * stride), acc);
-        }
+        out[i] = acc;
     }
-    out[i] = acc;
+}
+
+// ---- Eq. 14b: Quantile_q(V') by a three-pass radix select over the float bits (V' >= 0, so the
+// bit patterns order like the values): 11 + 11 + 10 bits, per-block shared histograms
+struct QSel {
+    uint32_t prefix;  // selected high bits so far
+    uint32_t rank;    // 0-based rank still to find inside the selected bucket
+};
+
+__global__ void __launch_bounds__(256) k_qhist(const float *__restrict__ vp, int64_t n, int shift, int bits,
+                                               const QSel *__restrict__ sel, uint32_t *__restrict__ ghist) {
+    __shared__ uint32_t h[2048];
+    const int nb = 1 << bits;
+    for (int k = threadIdx.x; k < nb; k += 256) h[k] = 0;
+    __syncthreads();
+    const uint32_t pre = sel->prefix;
+    const int hs = shift + bits;  // bits above this pass must equal the prefix
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = __float_as_uint(__ldg(vp + i));
+        if (hs >= 32 || (u >> hs) == pre) atomicAdd(&h[(u >> shift) & (nb - 1)], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nb; k += 256)
+        if (h[k]) atomicAdd(&ghist[k], h[k]);
+}
+
+// one block: find the bucket holding the rank, extend the prefix, clear the histogram
+__global__ void __launch_bounds__(256) k_qpick(uint32_t *ghist, int bits, QSel *sel) {
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_bucket, s_before;
+    const int nb = 1 << bits, per = nb / 256;  // 8 or 4 buckets per thread
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t c[8], sum = 0;
+    for (int k = 0; k < per; ++k) sum += (c[k] = ghist[threadIdx.x * per + k]);
+    uint32_t x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int k = 0; k < w; ++k) off += s_w[k];
+    uint32_t run = off + x - sum;  // exclusive prefix of this thread's buckets
+    const uint32_t r = sel->rank;
+    for (int k = 0; k < per; ++k) {
+        if (run <= r && r < run + c[k]) s_bucket = threadIdx.x * per + k, s_before = run;
+        run += c[k];
+    }
+    __syncthreads();
+    for (int k = 0; k < per; ++k) ghist[threadIdx.x * per + k] = 0u;
+    if (threadIdx.x == 0) {
+        sel->prefix = (sel->prefix << bits) | s_bucket;
+        sel->rank = r - s_before;
+    }
+}
+
+__global__ void k_qinit(QSel *sel, int64_t n, double q, float *thr_out) {
+    // inverted-CDF quantile: the value of 1-based rank max(1, ceil(q n)) in ascending order (R35)
+    int64_t k = (int64_t)ceil(q * (double)n);
+    if (k < 1) k = 1;
+    if (k > n) k = n;
+    sel->prefix = 0;
+    sel->rank = (uint32_t)(k - 1);
+    (void)thr_out;
+}
+
+__global__ void __launch_bounds__(256) k_threshold_q(const float *__restrict__ vp, Dims d, const QSel *sel,
+                                                     uint32_t *__restrict__ out, float *thr_out) {
+    const float tau = __uint_as_float(sel->prefix);
+    if (thr_out && blockIdx.x == 0 && threadIdx.x == 0) *thr_out = tau;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < d.nw(); w += (int64_t)gridDim.x * blockDim.x) {
+        const int wx = (int)(w % d.nwx);
+        const int64_t row = w / d.nwx;
+        const int x0 = wx * 32;
+        uint32_t b = 0;
+        for (int k = 0; k < 32 && x0 + k < d.nx; ++k)
+            if (vp[row * d.nx + x0 + k] >= tau) b |= 1u << k;
+        out[w] = b;
     }
 }
 
@@ -701,7 +783,7 @@ static Dims mkdims(const int *dims) {
 }
 
 void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, float sigma, float tau,
-                    uint32_t *out, float *vprime, cudaStream_t s) {
+                    uint32_t *out, float *vprime, cudaStream_t s, int quantile, float *thr_out) {
     const Dims d = mkdims(dims);
     float *a = salloc<float>(d.n(), s), *b = salloc<float>(d.n(), s);
     float *vp = vprime ? vprime : salloc<float>(d.n(), s);
@@ -719,8 +801,27 @@ void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, 
         FGL_LAUNCHED("k_blur");
         src = dst[ax];
     }
-    k_threshold<<<grid1d(d.nw()), 256, 0, s>>>(vp, d, tau, out);
-    FGL_LAUNCHED("k_threshold");
+    if (!quantile) {
+        k_threshold<<<grid1d(d.nw()), 256, 0, s>>>(vp, d, tau, out);
+        FGL_LAUNCHED("k_threshold");
+        if (thr_out) FGL_CUDA(cudaMemcpyAsync(thr_out, &tau, sizeof(float), cudaMemcpyHostToDevice, s));
+    } else {  // tau is the quantile level q (Eq. 14b)
+        QSel *sel = salloc<QSel>(1, s);
+        uint32_t *gh = salloc<uint32_t>(2048, s);
+        FGL_CUDA(cudaMemsetAsync(gh, 0, 2048 * sizeof(uint32_t), s));
+        k_qinit<<<1, 1, 0, s>>>(sel, d.n(), (double)tau, thr_out);
+        FGL_LAUNCHED("k_qinit");
+        const int pass_shift[3] = {21, 10, 0}, pass_bits[3] = {11, 11, 10};
+        for (int p = 0; p < 3; ++p) {
+            k_qhist<<<grid1d(d.n(), 256, 148 * 8), 256, 0, s>>>(vp, d.n(), pass_shift[p], pass_bits[p], sel, gh);
+            FGL_LAUNCHED("k_qhist");
+            k_qpick<<<1, 256, 0, s>>>(gh, pass_bits[p], sel);
+            FGL_LAUNCHED("k_qpick");
+        }
+        k_threshold_q<<<grid1d(d.nw()), 256, 0, s>>>(vp, d, sel, out, thr_out);
+        FGL_LAUNCHED("k_threshold_q");
+        sfree(sel, s), sfree(gh, s);
+    }
     sfree(a, s), sfree(b, s);
     if (!vprime) sfree(vp, s);
 }

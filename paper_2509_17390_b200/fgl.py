@@ -93,6 +93,8 @@ _SIGS = {
                                            c_void_p]),
     "fgl_voxelize": (c_int, [c_void_p, POINTER(GridC), c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "fgl_denoise": (c_int, [c_void_p, c_void_p, c_void_p, c_float, c_float, c_void_p, c_void_p, c_void_p]),
+    "fgl_denoise_quantile": (c_int, [c_void_p, c_void_p, c_void_p, c_float, c_float, c_void_p, c_void_p, c_void_p,
+                                     c_void_p]),
     "fgl_tsdf": (c_int, [c_void_p, c_void_p, c_void_p, c_float, c_void_p, c_void_p]),
     "fgl_marching_cubes": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_void_p, c_void_p, c_int64,
                                    c_void_p, c_int64, c_void_p, c_void_p]),
@@ -607,6 +609,19 @@ def denoise(occupancy: torch.Tensor, dims, spacing, sigma: float, tau: float, vp
     _check(lib().fgl_denoise(occupancy.data_ptr(), d, sp, float(sigma), float(tau), out.data_ptr(), _ptr(vp),
                              _stream(stream)))
     return (out, vp) if vprime else out
+
+
+def denoise_quantile(occupancy: torch.Tensor, dims, spacing, sigma: float, q: float, vprime: bool = False, out=None,
+                     stream=None):
+    """Eqs. 13-14b: blur, then threshold at Quantile_q(V'). Returns (bits, threshold[, V'])."""
+    d, sp = _vol_args(dims, spacing)
+    out = torch.empty_like(occupancy) if out is None else out
+    vp = torch.empty((int(dims[2]), int(dims[1]), int(dims[0])), dtype=torch.float32,
+                     device=occupancy.device) if vprime else None
+    thr = torch.empty(1, dtype=torch.float32, device=occupancy.device)
+    _check(lib().fgl_denoise_quantile(occupancy.data_ptr(), d, sp, float(sigma), float(q), out.data_ptr(), _ptr(vp),
+                                      thr.data_ptr(), _stream(stream)))
+    return (out, thr, vp) if vprime else (out, thr)
 
 
 def tsdf(occupancy: torch.Tensor, dims, spacing, r: float, out=None, stream=None) -> torch.Tensor:

@@ -152,3 +152,19 @@ def test_gaussians_to_mesh_to_cast():
     assert torch.all(res["tri_id"] >= 0)
     rng = res["range"].cpu().numpy()
     assert np.all((rng > 0.6) & (rng < 1.4))
+
+
+@pytest.mark.parametrize("q", [0.0, 0.3, 0.75, 0.98, 1.0])
+def test_denoise_quantile(q):
+    rng = np.random.default_rng(2)
+    V = rng.uniform(size=(17, 19, 41)) < 0.4
+    nz, ny, nx = V.shape
+    h = 0.05
+    out, thr, vp = fgl.denoise_quantile(_pack(V), (nx, ny, nz), (h, h, h), 0.9 * h, q, vprime=True)
+    vpn = vp.cpu().numpy()
+    # the selection is exact on the GPU's own float32 V' (same decision, same precision)
+    assert thr.item() == ot.quantile(vpn, q)
+    Vg = og.unpack_bits(out.cpu().numpy().view(np.uint32), (nx, ny, nz))
+    assert np.array_equal(Vg, ot.rethreshold_quantile(vpn, q))
+    ref = ot.blur(V, 0.9 * h, (h, h, h))
+    assert np.max(np.abs(vpn - ref)) < 1e-5

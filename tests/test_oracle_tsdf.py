@@ -199,3 +199,15 @@ def test_pipeline_on_occupancy_sphere():
     assert _check_closed_oriented(verts, tris) == 2
     vol = _volume(verts, tris)
     assert 0.6 < vol / (V.sum() * h ** 3) < 1.05  # the iso = 0 surface sits on the inner boundary layer
+
+
+def test_quantile_matches_numpy_inverted_cdf():
+    rng = np.random.default_rng(9)
+    for n in (1, 7, 1000):
+        v = rng.uniform(size=n).astype(np.float32)
+        v[: n // 3] = 0.0  # ties, as the blurred occupancy has
+        for q in (0.0, 0.1, 0.5, 0.9, 0.999, 1.0):
+            assert ot.quantile(v, q) == np.quantile(v, q, method="inverted_cdf")
+    v = np.arange(10, dtype=np.float32)
+    assert ot.quantile(v, 1.0) == 9 and ot.quantile(v, 0.0) == 0 and ot.quantile(v, 0.35) == 3
+    assert ot.rethreshold_quantile(v, 0.75).sum() == 3
