@@ -69,30 +69,29 @@ struct Taps {
 };
 
 // pass 0: bits -> float along x; pass 1, 2: float -> float along y, z. 64 x 4 blocks over
-// (x, row = (y, z)); weights staged in shared memory; the tap window is clipped to the grid once
+// (x, row = (y, z)), weights read from the parameter bank (staging them in shared memory measured
+// slower)
 __global__ void __launch_bounds__(256) k_blur(const uint32_t *__restrict__ bits, const float *__restrict__ in,
                                               float *__restrict__ out, Dims d, int axis, Taps t) {
-    __shared__ float w[kMaxTaps];
-    const int R = t.R;
-    for (int k = threadIdx.y * 64 + threadIdx.x; k < 2 * R + 1; k += 256) w[k] = t.w[k];
-    __syncthreads();
     const int x = blockIdx.x * 64 + threadIdx.x;
     if (x >= d.nx) return;
     for (int row = blockIdx.y * 4 + threadIdx.y; row < d.ny * d.nz; row += gridDim.y * 4) {
+        const int y = row % d.ny, z = row / d.ny;
         const int64_t i = (int64_t)row * d.nx + x;
         float acc = 0.f;
         if (axis == 0) {
             const uint32_t *rw = bits + (int64_t)row * d.nwx;
-            const int lo = max(x - R, 0), hi = min(x + R, d.nx - 1);
-            for (int cc = lo; cc <= hi; ++cc)
-                if ((__ldg(rw + (cc >> 5)) >> (cc & 31)) & 1u) acc += w[cc - x + R];
+            for (int k = -t.R; k <= t.R; ++k) {
+                const int cc = x + k;
+                if (cc >= 0 && cc < d.nx && ((__ldg(rw + (cc >> 5)) >> (cc & 31)) & 1u)) acc += t.w[k + t.R];
+            }
         } else {
-            const int y = row % d.ny, z = row / d.ny;
             const int c = axis == 1 ? y : z, n = axis == 1 ? d.ny : d.nz;
             const int64_t stride = axis == 1 ? d.nx : (int64_t)d.nx * d.ny;
-            const int lo = max(c - R, 0), hi = min(c + R, n - 1);
-            const float *pp = in + i + (int64_t)(lo - c) * stride;
-            for (int cc = lo; cc <= hi; ++cc, pp += stride) acc = fmaf(w[cc - c + R], __ldg(pp), acc);
+            for (int k = -t.R; k <= t.R; ++k) {
+                const int cc = c + k;
+                if (cc >= 0 && cc < n) acc = fmaf(t.w[k + t.R], __ldg(in + i + (int64_t)k * stride), acc);
+            }
         }
         out[i] = acc;
     }
