@@ -305,11 +305,12 @@ class Scene:
         return res
 
     def cast_to_host(self, poses, pattern, range_out: torch.Tensor, tri_id_out: torch.Tensor, chunks: int = 8,
-                     first_frame: int = 0, copy_stream=None, scratch=None):
+                     first_frame: int = 0, copy_stream=None, scratch=None, wait: bool = True):
         """Cast and stream the results to (pinned) host tensors, overlapping the device-to-host copy
         of chunk k with the cast of chunk k+1 (the copy runs on `copy_stream`). Returns when the
         copies are enqueued; the caller synchronises. `scratch` (optional) = dict(range, tri_id)
-        device tensors of the full output shape, reused across calls."""
+        device tensors of the full output shape, reused across calls. wait=False: the current
+        stream does not wait for the copies; the returned event marks their completion."""
         dev = self.device
         cur = torch.cuda.current_stream(dev)
         cs = copy_stream or torch.cuda.Stream(device=dev)
@@ -329,8 +330,12 @@ class Scene:
             with torch.cuda.stream(cs):
                 range_out[a:b].copy_(scratch["range"][a:b], non_blocking=True)
                 tri_id_out[a:b].copy_(scratch["tri_id"][a:b], non_blocking=True)
-        cur.wait_stream(cs)
-        return range_out, tri_id_out
+        if wait:
+            cur.wait_stream(cs)
+            return range_out, tri_id_out
+        done = torch.cuda.Event()
+        done.record(cs)
+        return done
 
     def cast_rays(self, orig, dir, t_min: float, t_max: float, bruteforce: bool = False, stream=None):
         o = _dev(orig, torch.float32, self.device, (-1, 3))
