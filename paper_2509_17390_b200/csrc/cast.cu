@@ -191,6 +191,37 @@ __device__ __forceinline__ bool slab_hit(const Pre &p, float lx, float hx, float
     return tn <= tf * kExpand;
 }
 
+// Octant-specialised form of slab_hit: when the sign of every I component is known at compile
+// time, the near plane of each axis is known (lo iff I >= 0), so the per-axis min/max that orders
+// each plane pair disappears: 6 FFMA + 4 FMNMX + 1 FMUL + 1 FSETP per box instead of 6 + 10 + 1 + 1.
+// The planes, their constants and the final test are those of slab_hit, so the result is the same
+// bit for bit (min/max of the same two values). OCT bit a = (I_a < 0).
+template <int OCT>
+__device__ __forceinline__ bool slab_oct(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
+                                         float tmin, float tmax, float &tn_out) {
+    constexpr bool sx = OCT & 1, sy = OCT & 2, sz = OCT & 4;
+    const float nx = fmaf(sx ? hx : lx, p.Ix, sx ? p.chx : p.clx), fx = fmaf(sx ? lx : hx, p.Ix, sx ? p.clx : p.chx);
+    const float ny = fmaf(sy ? hy : ly, p.Iy, sy ? p.chy : p.cly), fy = fmaf(sy ? ly : hy, p.Iy, sy ? p.cly : p.chy);
+    const float nz = fmaf(sz ? hz : lz, p.Iz, sz ? p.chz : p.clz), fz = fmaf(sz ? lz : hz, p.Iz, sz ? p.clz : p.chz);
+    const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, tmin));
+    const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
+    tn_out = tn;
+    return tn <= tf * kExpand;
+}
+
+__device__ __forceinline__ int ray_octant(const Pre &p) {
+    return (p.Ix < 0.f ? 1 : 0) | (p.Iy < 0.f ? 2 : 0) | (p.Iz < 0.f ? 4 : 0);
+}
+
+template <int OCT>
+__device__ __forceinline__ bool slab_sel(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
+                                         float tmin, float tmax, float &tn_out) {
+    if constexpr (OCT < 0)
+        return slab_hit(p, lx, hx, ly, hy, lz, hz, tmin, tmax, tn_out);
+    else
+        return slab_oct<OCT>(p, lx, hx, ly, hy, lz, hz, tmin, tmax, tn_out);
+}
+
 constexpr int32_t kDone = INT_MAX;  // "no more work" (never a node index: T - 1 < 2^28)
 
 // Traversal in the "while-while" form of Aila & Laine (HPG 2009): a lane that reaches a leaf
@@ -739,11 +770,59 @@ __device__ __forceinline__ unsigned long long next_tile(CastCounter *ctr, ChunkS
     }
 }
 
+// Pop the nearest stacked subtree that can still hold a hit (entry t <= t* (1 + 2^-20)).
+__device__ __forceinline__ int32_t pop_live(const uint64_t *st, int &sp, float tlim) {
+    while (sp > 0) {
+        --sp;
+        if (__uint_as_float((uint32_t)(st[sp] >> 32)) <= tlim) return (int32_t)(uint32_t)st[sp];
+    }
+    return kDone;
+}
+
+// The descent phase of one while-while iteration (Aila & Laine 2009): internal nodes are visited
+// near child first, the far hit child is pushed with its entry distance, and a lane reaching a leaf
+// postpones it and keeps descending until every active lane of the warp holds a leaf. OCT >= 0:
+// all active lanes travel in ray octant OCT (slab_oct); OCT = -1: mixed octants (slab_hit).
+template <int OCT, bool kCount>
+__device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const Pre &p, float tmin, bool active,
+                                        Hit &h, float tlim, uint64_t *st, int &sp, int32_t &cur,
+                                        int32_t &leaf) {
+    while (true) {
+        const bool go = active && cur >= 0 && cur != kDone;
+        if (go) {
+            const float4 *np = reinterpret_cast<const float4 *>(nodes + cur);
+            const float4 na = __ldg(np), nb = __ldg(np + 1), nc = __ldg(np + 2);
+            const int4 nd = __ldg(reinterpret_cast<const int4 *>(np + 3));
+            if (kCount) ++h.nodes;
+            const float lim = h.t;
+            float t0, t1;
+            const bool h0 = slab_sel<OCT>(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim, t0);
+            const bool h1 = slab_sel<OCT>(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim, t1);
+            if (h0 && h1) {
+                const bool swap = t1 < t0;
+                st[sp++] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
+                cur = swap ? nd.y : nd.x;
+            } else if (h0) {
+                cur = nd.x;
+            } else if (h1) {
+                cur = nd.y;
+            } else {
+                cur = pop_live(st, sp, tlim);
+            }
+            if (cur < 0 && leaf == 0) {
+                leaf = cur;
+                cur = pop_live(st, sp, tlim);
+            }
+        }
+        if (!__any_sync(0xffffffffu, go && leaf == 0)) break;
+    }
+}
+
+#ifndef FGL_OCTANT
+#define FGL_OCTANT 1  // octant-specialised descent when a warp's rays share an octant
+#endif
 #ifndef FGL_REFILL
 #define FGL_REFILL 32
-#endif
-#ifndef FGL_FULLVOTE
-#define FGL_FULLVOTE 1
 #endif
 template <class Gen, bool kCount>
 __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
@@ -758,6 +837,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
     int sp = 0;
     int32_t cur = kDone, leaf = 0;
     Pre p;
+    int oct = 0;  // ray octant (sign bits of the direction)
     Hit h{0.f, INT_MAX, 0, 0};
     float tlim = 0.f;  // h.t * kExpand, the pop bound, updated with h.t
     const Node64 *__restrict__ nodes = sv.nodes;
@@ -791,6 +871,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
                 float tmax;
                 if (gen.ray((int64_t)tile, slot, r, idx, tmin, tmax)) {
                     p = precompute(r);
+                    oct = ray_octant(p);
                     h = Hit{tmax, INT_MAX, 0, 0};
                     tlim = tmax * kExpand;
                     sp = 0, cur = 0, leaf = 0;
@@ -798,68 +879,28 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
                 }
             }
         }
-#if !FGL_FULLVOTE
-        if (!active) continue;
-#endif
         // ---- one outer iteration of the while-while traversal ----
-        auto pop = [&]() -> int32_t {
-            while (sp > 0) {
-                --sp;
-                if (__uint_as_float((uint32_t)(st[sp] >> 32)) <= tlim) return (int32_t)(uint32_t)st[sp];
-            }
-            return kDone;
-        };
-#if FGL_FULLVOTE
-        // every lane of the warp runs the loop (idle / finished lanes predicated off), so the
-        // speculation vote is a plain full-warp vote (no __activemask)
-        while (true) {
-            const bool go = active && cur >= 0 && cur != kDone;
-            if (go) {
-#else
-        while (cur >= 0 && cur != kDone) {
-            {
+        // Every lane of the warp runs the descent loop (idle / finished lanes predicated off), so the
+        // speculation vote is a plain full-warp vote. When all active lanes share a ray octant (the
+        // usual case: a tile spans ~1.5 degrees) the loop is the octant-specialised instance.
+        const unsigned act = __ballot_sync(kFull, active);
+        if (act) {
+#if FGL_OCTANT
+            const int o0 = __shfl_sync(kFull, oct, __ffs(act) - 1);
+            if (__all_sync(kFull, !active || oct == o0)) {
+                switch (o0) {
+                    case 0: descend<0, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 1: descend<1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 2: descend<2, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 3: descend<3, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 4: descend<4, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 5: descend<5, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 6: descend<6, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    default: descend<7, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                }
+            } else
 #endif
-            const float4 *np = reinterpret_cast<const float4 *>(nodes + cur);
-            const float4 na = __ldg(np), nb = __ldg(np + 1), nc = __ldg(np + 2);
-            const int4 nd = __ldg(reinterpret_cast<const int4 *>(np + 3));
-            if (kCount) ++h.nodes;
-            const float lim = h.t;
-            float t0, t1;
-            const bool h0 = slab_hit(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim, t0);
-            const bool h1 = slab_hit(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim, t1);
-#if FGL_BRANCHFREE_PUSH
-            {
-                const bool swap = t1 < t0;  // (only meaningful when both are hit)
-                st[sp] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
-                sp += (h0 && h1) ? 1 : 0;
-                const int32_t nr = (h0 && (!h1 || !swap)) ? nd.x : nd.y;
-                cur = (h0 || h1) ? nr : pop();
-            }
-#else
-            if (h0 && h1) {
-                const bool swap = t1 < t0;
-                st[sp++] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
-                cur = swap ? nd.y : nd.x;
-            } else if (h0) {
-                cur = nd.x;
-            } else if (h1) {
-                cur = nd.y;
-            } else {
-                cur = pop();
-            }
-#endif
-            if (cur < 0 && leaf == 0) {
-                leaf = cur;
-                cur = pop();
-            }
-            }
-#if FGL_FULLVOTE
-            if (!__any_sync(kFull, go && leaf == 0)) break;
-#elif FGL_SPECULATE
-            if (!__any_sync(__activemask(), leaf == 0)) break;
-#else
-            if (leaf != 0) break;
-#endif
+                descend<-1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf);
         }
         if (!active) continue;
         while (leaf < 0) {
@@ -880,7 +921,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
             leaf = 0;
             if (cur < 0) {
                 leaf = cur;
-                cur = pop();
+                cur = pop_live(st, sp, tlim);
             }
         }
         if (cur == kDone) {
