@@ -21,6 +21,13 @@ namespace fgl {
 
 namespace {
 
+#ifndef FGL_APPROX_PRE
+#define FGL_APPROX_PRE 1  // MUFU reciprocals for the per-ray slab / shear constants
+#endif
+#ifndef FGL_APPROX_NORM
+#define FGL_APPROX_NORM 0  // MUFU rsqrt for the direction normalisation (off: exact sqrt + division)
+#endif
+
 constexpr int kCastThreads = 128;
 constexpr int kStack = 96;                   // > max depth of a Karras tree over 63-bit keys + index
 constexpr float kExpand = 1.0f + 0x1p-20f;   // conservative slab test: tfar * (1 + 2 gamma_3) (Ize 2013)
@@ -46,6 +53,13 @@ struct Pre {
     float m0x, m0y, m0z, m1x, m1y, m1z, m2x, m2y, m2z;
 };
 
+// 1/x by MUFU.RCP (rcp.approx.ftz.f32, <= 1 ulp); |x| >= 2^-80 here, so no denormal is flushed
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ Pre precompute(const Ray &r) {
     Pre p;
     p.ox = r.ox, p.oy = r.oy, p.oz = r.oz;
@@ -56,7 +70,7 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
 #if FGL_APPROX_PRE
     // MUFU reciprocals (<= 2 ulp): covered by the slab slack, consistent per ray;
     // the shear S is likewise only required to be consistent per ray (watertightness)
-    p.Ix = __fdividef(1.f, dx), p.Iy = __fdividef(1.f, dy), p.Iz = __fdividef(1.f, dz);
+    p.Ix = rcp_approx(dx), p.Iy = rcp_approx(dy), p.Iz = rcp_approx(dz);
 #else
     p.Ix = __frcp_rn(dx), p.Iy = __frcp_rn(dy), p.Iz = __frcp_rn(dz);
 #endif
@@ -79,7 +93,7 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
     const float dkx = kx == 0 ? r.dx : (kx == 1 ? r.dy : r.dz);
     const float dky = ky == 0 ? r.dx : (ky == 1 ? r.dy : r.dz);
 #if FGL_APPROX_PRE
-    const float Sz = __fdividef(1.f, dkz), Sx = dkx * Sz, Sy = dky * Sz;
+    const float Sz = rcp_approx(dkz), Sx = dkx * Sz, Sy = dky * Sz;
 #else
     const float Sx = __fdiv_rn(dkx, dkz), Sy = __fdiv_rn(dky, dkz), Sz = __frcp_rn(dkz);
 #endif
@@ -616,7 +630,7 @@ __device__ __forceinline__ void rotate_pose(const float *__restrict__ pose, floa
     float dx = r0.x * sx + r0.y * sy + r0.z * sz;
     float dy = r1.x * sx + r1.y * sy + r1.z * sz;
     float dz = r2.x * sx + r2.y * sy + r2.z * sz;
-#if FGL_APPROX_PRE
+#if FGL_APPROX_NORM
     const float rn = rsqrtf(dx * dx + dy * dy + dz * dz);  // MUFU.RSQ (<= 2 ulp), same in cast and export
     r.dx = dx * rn, r.dy = dy * rn, r.dz = dz * rn;
 #else
@@ -626,13 +640,41 @@ __device__ __forceinline__ void rotate_pose(const float *__restrict__ pose, floa
     r.ox = r0.w, r.oy = r1.w, r.oz = r2.w;
 }
 
-// spinning beam (c, a): d_s = (cos e cos th, cos e sin th, sin e), th = 2 pi a / A + az0 (R11, R12)
-__device__ __forceinline__ void spin_ray(const SpinParams &sp, const float *__restrict__ poses, int64_t p, int c, int a,
-                                         Ray &r) {
-    float se, ce, sa, ca;
-    sincospif(__fdiv_rn(sp.elev_deg[c], 180.f), &se, &ce);
-    sincospif(__fadd_rn(__fdiv_rn(2.f * (float)a, (float)sp.columns), __fdiv_rn(sp.az0_deg, 180.f)), &sa, &ca);
-    rotate_pose(poses + 12 * p, ce * ca, ce * sa, se, r);
+// spinning beam (c, a): d_s = (cos e cos th, cos e sin th, sin e), th = 2 pi a / A + az0 (R11, R12).
+// (sin, cos) of the elevation of channel c and of the azimuth of column a; k_spin_table evaluates
+// them once per call into a [C + A] table, so the per-ray generator only rotates and normalises.
+__device__ __forceinline__ float2 spin_elev_sc(const SpinParams &sp, int c) {
+    float s, co;
+    sincospif(__fdiv_rn(sp.elev_deg[c], 180.f), &s, &co);
+    return make_float2(s, co);
+}
+__device__ __forceinline__ float2 spin_az_sc(const SpinParams &sp, int a) {
+    float s, co;
+    sincospif(__fadd_rn(__fdiv_rn(2.f * (float)a, (float)sp.columns), __fdiv_rn(sp.az0_deg, 180.f)), &s, &co);
+    return make_float2(s, co);
+}
+__device__ __forceinline__ void spin_ray_tab(const float2 *__restrict__ tab, int C, const float *__restrict__ poses,
+                                             int64_t p, int c, int a, Ray &r) {
+    const float2 e = __ldg(tab + c), z = __ldg(tab + C + a);
+    rotate_pose(poses + 12 * p, e.y * z.y, e.y * z.x, e.x, r);
+}
+
+// 32-bit division by a launch-invariant divisor (Granlund & Montgomery 1994): for n < 2^31 and
+// d >= 2, s = ceil(log2 d), m = ceil(2^(31+s) / d) < 2^32, n / d = umulhi(n, m) >> (s - 1).
+struct FastDiv {
+    uint32_t d, m, sh;  // sh = s - 1; d = 1 is m = 0 (quotient n)
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0u, 0u};
+    if (d <= 1) return f;
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    f.m = (uint32_t)(((1ull << (31 + s)) + d - 1) / d);
+    f.sh = s - 1;
+    return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+    return f.m ? __umulhi(n, f.m) >> f.sh : n;
 }
 
 // rosette sample n of pose p (R20): exact 32-bit phases, two counter-rotating prisms
@@ -657,17 +699,19 @@ struct SpinGen {
     static constexpr bool kCoherent = true;
     SpinParams sp;
     const float *poses;
-    int tc, ta, nct, nat;  // tile shape and tiles per pose
+    const float2 *tab;     // k_spin_table: [C] elevation (sin, cos), then [A] azimuth (sin, cos)
+    int tc, ta, lta;       // tile shape (tc x ta = 32, ta = 2^lta)
+    FastDiv per, nat;      // tiles per pose, column tiles per channel tile
     __device__ __forceinline__ bool ray(int64_t tile, int lane, Ray &r, int64_t &idx, float &tmin, float &tmax) const {
-        const int64_t per = (int64_t)nct * nat;
-        const int64_t p = tile / per;
-        const int64_t rem = tile - p * per;
-        const int cb = (int)(rem / nat), ab = (int)(rem - (int64_t)cb * nat);
-        const int c = cb * tc + lane / ta, a = ab * ta + lane % ta;
+        const uint32_t t = (uint32_t)tile;  // < 2^31 (checked at launch)
+        const uint32_t p = fdiv(t, per);
+        const uint32_t rem = t - p * per.d;
+        const uint32_t cb = fdiv(rem, nat), ab = rem - cb * nat.d;
+        const int c = (int)cb * tc + (lane >> lta), a = (int)ab * ta + (lane & (ta - 1));
         tmin = sp.t_min, tmax = sp.t_max;
         if (c >= sp.channels || a >= sp.columns) return false;
-        spin_ray(sp, poses, p, c, a, r);
-        idx = (p * sp.channels + c) * (int64_t)sp.columns + a;
+        spin_ray_tab(tab, sp.channels, poses, p, c, a, r);
+        idx = ((int64_t)p * sp.channels + c) * (int64_t)sp.columns + a;
         return true;
     }
 };
@@ -705,9 +749,6 @@ struct RaysGen {
 
 #ifndef FGL_SPECULATE
 #define FGL_SPECULATE 1  // while-while: keep descending after a postponed leaf until all lanes hold one
-#endif
-#ifndef FGL_APPROX_PRE
-#define FGL_APPROX_PRE 1
 #endif
 #ifndef FGL_BRANCHFREE_PUSH
 #define FGL_BRANCHFREE_PUSH 0
@@ -1087,17 +1128,33 @@ __global__ void __launch_bounds__(kBfThreads) k_bruteforce(const float *__restri
     }
 }
 
-__global__ void k_export_spin(const SpinParams sp, const float *__restrict__ poses, int64_t n, float *orig,
-                              float *dir) {
+__global__ void k_spin_table(const SpinParams sp, float2 *tab) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < sp.channels) tab[i] = spin_elev_sc(sp, i);
+    else if (i < sp.channels + sp.columns) tab[i] = spin_az_sc(sp, i - sp.channels);
+}
+
+__global__ void k_export_spin(const SpinParams sp, const float2 *__restrict__ tab, const float *__restrict__ poses,
+                              int64_t n, float *orig, float *dir) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t per = (int64_t)sp.channels * sp.columns;
         const int64_t p = g / per;
         const int c = (int)((g - p * per) / sp.columns), a = (int)(g % sp.columns);
         Ray r;
-        spin_ray(sp, poses, p, c, a, r);
+        spin_ray_tab(tab, sp.channels, poses, p, c, a, r);
         orig[3 * g] = r.ox, orig[3 * g + 1] = r.oy, orig[3 * g + 2] = r.oz;
         dir[3 * g] = r.dx, dir[3 * g + 1] = r.dy, dir[3 * g + 2] = r.dz;
     }
+}
+
+// stream-ordered [C + A] sin/cos table for one spinning call (freed on the stream after use)
+float2 *spin_table(const SpinParams &p, cudaStream_t s) {
+    const int n = p.channels + p.columns;
+    float2 *tab = nullptr;
+    FGL_CUDA(cudaMallocAsync((void **)&tab, sizeof(float2) * (size_t)n, s));
+    k_spin_table<<<(n + 127) / 128, 128, 0, s>>>(p, tab);
+    FGL_LAUNCHED("k_spin_table");
+    return tab;
 }
 
 __global__ void k_export_rosette(const RosetteParams rp, const float *__restrict__ poses, int64_t n, float *orig,
@@ -1127,9 +1184,17 @@ void launch_cast_spinning(const SceneView &sv, const SpinParams &p, const float 
 #endif
     g.tc = p.channels >= FGL_TILE_C ? FGL_TILE_C : (p.channels >= 4 ? 4 : (p.channels >= 2 ? 2 : 1));
     g.ta = 32 / g.tc;
-    g.nct = (p.channels + g.tc - 1) / g.tc;
-    g.nat = (p.columns + g.ta - 1) / g.ta;
-    launch_persistent(sv, g, P * (int64_t)g.nct * g.nat, o, ctr, s);
+    g.lta = __builtin_ctz(g.ta);
+    const int64_t nct = (p.channels + g.tc - 1) / g.tc, nat = (p.columns + g.ta - 1) / g.ta;
+    const int64_t ntiles = P * nct * nat;
+    if (ntiles >= (int64_t(1) << 31)) throw Error(1, "spinning cast: more than 2^31 ray tiles in one call");
+    g.per = make_fastdiv((uint32_t)(nct * nat));
+    g.nat = make_fastdiv((uint32_t)nat);
+    if (ntiles <= 0 && !o.nsignal) return;
+    float2 *tab = spin_table(p, s);
+    g.tab = tab;
+    launch_persistent(sv, g, ntiles, o, ctr, s);
+    FGL_CUDA(cudaFreeAsync(tab, s));
 }
 
 void launch_cast_rosette(const SceneView &sv, const RosetteParams &p, const float *poses, int64_t P,
@@ -1172,8 +1237,10 @@ void launch_export_spinning(const SpinParams &p, const float *poses, int64_t P, 
                             cudaStream_t s) {
     const int64_t n = P * p.channels * (int64_t)p.columns;
     if (n <= 0) return;
-    k_export_spin<<<grid_for(n), 256, 0, s>>>(p, poses, n, orig, dir);
+    float2 *tab = spin_table(p, s);
+    k_export_spin<<<grid_for(n), 256, 0, s>>>(p, tab, poses, n, orig, dir);
     FGL_LAUNCHED("k_export_spin");
+    FGL_CUDA(cudaFreeAsync(tab, s));
 }
 
 void launch_export_rosette(const RosetteParams &p, const float *poses, int64_t P, float *orig, float *dir,
