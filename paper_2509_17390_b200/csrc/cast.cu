@@ -21,6 +21,9 @@ namespace fgl {
 
 namespace {
 
+#ifndef FGL_SHEAR_MATRIX
+#define FGL_SHEAR_MATRIX 0  // watertight shear as a 3x3 matrix (9 registers; else axis selects, 4)
+#endif
 #ifndef FGL_APPROX_PRE
 #define FGL_APPROX_PRE 1  // MUFU reciprocals for the per-ray slab / shear constants
 #endif
@@ -50,7 +53,12 @@ struct Pre {
     float ox, oy, oz;
     float Ix, Iy, Iz;
     float clx, chx, cly, chy, clz, chz;
+#if FGL_SHEAR_MATRIX
     float m0x, m0y, m0z, m1x, m1y, m1z, m2x, m2y, m2z;
+#else
+    float Sx, Sy, Sz;
+    int perm;  // 2 kz + (d_kz < 0): kz = argmax |d_a|, kx = kz + 1, ky = kx + 1 (mod 3), swapped if d_kz < 0
+#endif
 };
 
 // 1/x by MUFU.RCP (rcp.approx.ftz.f32, <= 1 ulp); |x| >= 2^-80 here, so no denormal is flushed
@@ -97,6 +105,7 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
 #else
     const float Sx = __fdiv_rn(dkx, dkz), Sy = __fdiv_rn(dky, dkz), Sz = __frcp_rn(dkz);
 #endif
+#if FGL_SHEAR_MATRIX
     p.m0x = kx == 0 ? 1.f : (kz == 0 ? -Sx : 0.f);
     p.m0y = kx == 1 ? 1.f : (kz == 1 ? -Sx : 0.f);
     p.m0z = kx == 2 ? 1.f : (kz == 2 ? -Sx : 0.f);
@@ -106,6 +115,10 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
     p.m2x = kz == 0 ? Sz : 0.f;
     p.m2y = kz == 1 ? Sz : 0.f;
     p.m2z = kz == 2 ? Sz : 0.f;
+#else
+    p.Sx = Sx, p.Sy = Sy, p.Sz = Sz;
+    p.perm = 2 * kz + (dkz < 0.f ? 1 : 0);
+#endif
     return p;
 }
 
@@ -113,23 +126,44 @@ struct V3 {
     float x, y, z;
 };
 
-// sheared coordinates of a vertex relative to the ray origin
+// Sheared coordinates of a vertex relative to the ray origin: (A_kx - Sx A_kz, A_ky - Sy A_kz, Sz A_kz)
+// with A = v - o. PERM >= 0: the warp-uniform axis permutation, fixed at compile time; PERM = -1:
+// the ray's own permutation by selects. Both evaluate the same two roundings per coordinate, so a
+// vertex shared by two triangles gets the same sheared coordinates in either form (watertightness).
+template <int PERM>
 __device__ __forceinline__ V3 shear(const Pre &p, float4 v) {
     const float X = v.x - p.ox, Y = v.y - p.oy, Z = v.z - p.oz;
-    V3 s;
-    s.x = fmaf(p.m0z, Z, fmaf(p.m0y, Y, p.m0x * X));
-    s.y = fmaf(p.m1z, Z, fmaf(p.m1y, Y, p.m1x * X));
-    s.z = fmaf(p.m2z, Z, fmaf(p.m2y, Y, p.m2x * X));
-    return s;
+#if FGL_SHEAR_MATRIX
+    // the permutation folded into a 3x3 matrix (entries 1, -S or 0: the products by 0 and 1 are exact)
+    return V3{fmaf(p.m0z, Z, fmaf(p.m0y, Y, p.m0x * X)), fmaf(p.m1z, Z, fmaf(p.m1y, Y, p.m1x * X)),
+              fmaf(p.m2z, Z, fmaf(p.m2y, Y, p.m2x * X))};
+#else
+    float Ax, Ay, Az;
+    if constexpr (PERM >= 0) {
+        constexpr int kz = PERM >> 1, k1 = kz == 2 ? 0 : kz + 1, k2 = k1 == 2 ? 0 : k1 + 1;
+        constexpr int kx = (PERM & 1) ? k2 : k1, ky = (PERM & 1) ? k1 : k2;
+        Ax = kx == 0 ? X : (kx == 1 ? Y : Z);
+        Ay = ky == 0 ? X : (ky == 1 ? Y : Z);
+        Az = kz == 0 ? X : (kz == 1 ? Y : Z);
+    } else {
+        const int kz = p.perm >> 1, k1 = kz == 2 ? 0 : kz + 1, k2 = k1 == 2 ? 0 : k1 + 1;
+        const int kx = (p.perm & 1) ? k2 : k1, ky = (p.perm & 1) ? k1 : k2;
+        Ax = kx == 0 ? X : (kx == 1 ? Y : Z);
+        Ay = ky == 0 ? X : (ky == 1 ? Y : Z);
+        Az = kz == 0 ? X : (kz == 1 ? Y : Z);
+    }
+    return V3{fmaf(-p.Sx, Az, Ax), fmaf(-p.Sy, Az, Ay), p.Sz * Az};
+#endif
 }
 
 // Watertight ray/triangle test (two-sided, inclusive edges). Edge functions are evaluated without
 // FMA contraction so that the two triangles of a shared edge see exactly opposite values; an
 // exactly-zero edge function is re-evaluated in double (float products are exact there).
 // Returns true and t when t is in [tmin, best_t] and (t, id) beats (best_t, best_id).
+template <int PERM = -1>
 __device__ __forceinline__ bool hit_tri(const Pre &p, float4 a, float4 b, float4 c, float tmin, float best_t,
                                         int32_t best_id, int32_t id, float &t_out) {
-    const V3 A = shear(p, a), B = shear(p, b), C = shear(p, c);
+    const V3 A = shear<PERM>(p, a), B = shear<PERM>(p, b), C = shear<PERM>(p, c);
     float U = __fsub_rn(__fmul_rn(C.x, B.y), __fmul_rn(C.y, B.x));
     float V = __fsub_rn(__fmul_rn(A.x, C.y), __fmul_rn(A.y, C.x));
     float W = __fsub_rn(__fmul_rn(B.x, A.y), __fmul_rn(B.y, A.x));
@@ -160,34 +194,12 @@ struct Hit {
     int32_t nodes, tris;
 };
 
-#ifndef FGL_FFMA2
-#define FGL_FFMA2 0
-#endif
-// packed FP32x2 (sm_100: FFMA2): one instruction evaluates the lo and hi planes of an axis
-__device__ __forceinline__ unsigned long long pk2(float a, float b) {
-    unsigned long long r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void ffma2(float a0, float a1, float b, float c0, float c1, float &d0, float &d1) {
-    unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a0, a1)), "l"(pk2(b, b)), "l"(pk2(c0, c1)));
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(r));
-}
-
 // conservative slab test of one child box against [tmin, tmax]; returns the entry distance or +inf
 __device__ __forceinline__ float slab(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
                                       float tmin, float tmax) {
-#if FGL_FFMA2
-    float ax, bx, ay, by, az, bz;
-    ffma2(lx, hx, p.Ix, p.clx, p.chx, ax, bx);
-    ffma2(ly, hy, p.Iy, p.cly, p.chy, ay, by);
-    ffma2(lz, hz, p.Iz, p.clz, p.chz, az, bz);
-#else
     const float ax = fmaf(lx, p.Ix, p.clx), bx = fmaf(hx, p.Ix, p.chx);
     const float ay = fmaf(ly, p.Iy, p.cly), by = fmaf(hy, p.Iy, p.chy);
     const float az = fmaf(lz, p.Iz, p.clz), bz = fmaf(hz, p.Iz, p.chz);
-#endif
     const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
     const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
     return tn <= tf * kExpand ? tn : INFINITY;
@@ -714,6 +726,22 @@ struct SpinGen {
         idx = ((int64_t)p * sp.channels + c) * (int64_t)sp.columns + a;
         return true;
     }
+    // the same ray / output slot without the index (k_cast_dyn recomputes the index at the write)
+    __device__ __forceinline__ bool ray_at(int64_t tile, int lane, Ray &r) const {
+        int64_t idx;
+        float a, b;
+        return ray(tile, lane, r, idx, a, b);
+    }
+    __device__ __forceinline__ int64_t index(int64_t tile, int lane) const {
+        const uint32_t t = (uint32_t)tile;
+        const uint32_t p = fdiv(t, per);
+        const uint32_t rem = t - p * per.d;
+        const uint32_t cb = fdiv(rem, nat), ab = rem - cb * nat.d;
+        const int c = (int)cb * tc + (lane >> lta), a = (int)ab * ta + (lane & (ta - 1));
+        return ((int64_t)p * sp.channels + c) * (int64_t)sp.columns + a;
+    }
+    __device__ __forceinline__ float interval_min() const { return sp.t_min; }
+    __device__ __forceinline__ float interval_max() const { return sp.t_max; }
 };
 
 struct RosetteGen {
@@ -730,6 +758,17 @@ struct RosetteGen {
         idx = p * rp.n + k;
         return true;
     }
+    __device__ __forceinline__ bool ray_at(int64_t tile, int lane, Ray &r) const {
+        int64_t idx;
+        float a, b;
+        return ray(tile, lane, r, idx, a, b);
+    }
+    __device__ __forceinline__ int64_t index(int64_t tile, int lane) const {
+        const int64_t p = tile / ntile;
+        return p * rp.n + (int)(tile - p * ntile) * 32 + lane;
+    }
+    __device__ __forceinline__ float interval_min() const { return rp.t_min; }
+    __device__ __forceinline__ float interval_max() const { return rp.t_max; }
 };
 
 struct RaysGen {
@@ -745,6 +784,14 @@ struct RaysGen {
         r.dx = dir[3 * idx], r.dy = dir[3 * idx + 1], r.dz = dir[3 * idx + 2];
         return true;
     }
+    __device__ __forceinline__ bool ray_at(int64_t tile, int lane, Ray &r) const {
+        int64_t idx;
+        float a, b;
+        return ray(tile, lane, r, idx, a, b);
+    }
+    __device__ __forceinline__ int64_t index(int64_t tile, int lane) const { return tile * 32 + lane; }
+    __device__ __forceinline__ float interval_min() const { return t_min; }
+    __device__ __forceinline__ float interval_max() const { return t_max; }
 };
 
 #ifndef FGL_SPECULATE
@@ -755,6 +802,9 @@ struct RaysGen {
 #endif
 #ifndef FGL_CAST_MINBLOCKS
 #define FGL_CAST_MINBLOCKS 8
+#endif
+#ifndef FGL_DYN_MINBLOCKS
+#define FGL_DYN_MINBLOCKS 10  // k_cast_dyn: 10 CTAs x 4 warps per SM (48 registers; measured best)
 #endif
 enum TraversalMode { kRay2 = 0, kPacket2 = 1, kRay4 = 2, kRay4Q = 3 };
 
@@ -800,41 +850,6 @@ inline bool packet_mode() {
         v = (e && strcmp(e, "packet") == 0) ? 1 : 0;
     }
     return v == 1;
-}
-
-// Per-ray BVH2 traversal with dynamic ray fetch (Aila & Laine 2009, "persistent threads" with
-// replacement of terminated rays): a lane whose ray is done idles only until at least kRefill
-// lanes of its warp are idle; then the idle lanes take the next rays of the warp's current 32-ray
-// tile (and of the next tile from the global counter when it runs out). Rays stay in tile order,
-// so a warp holds angular neighbours from at most two adjacent tiles. The traversal itself is the
-// while-while loop of `trace` (same slab and leaf tests, same (t, id) rule), executed one outer
-// iteration at a time so that the refill check runs between leaf batches.
-// Tile dispenser: a CTA takes FGL_CHUNK consecutive tiles from the global counter at a time and
-// its warps share them, so the warps of a CTA (and of an SM) trace neighbouring rays and reuse each
-// other's nodes in L1. FGL_CHUNK = 1 is the plain per-warp global counter.
-#ifndef FGL_CHUNK
-#define FGL_CHUNK 1
-#endif
-struct ChunkState {
-    unsigned long long base;
-    unsigned int pos;
-};
-__device__ __forceinline__ unsigned long long next_tile(CastCounter *ctr, ChunkState &c) {
-    if (FGL_CHUNK == 1) return atomicAdd(&ctr->next, 1ull);
-    while (true) {
-        const unsigned int k = atomicAdd(&c.pos, 1u);
-        if (k < FGL_CHUNK) {
-            __threadfence_block();
-            return *(volatile unsigned long long *)&c.base + k;
-        }
-        if (k == FGL_CHUNK) {  // this warp refills the chunk
-            *(volatile unsigned long long *)&c.base = atomicAdd(&ctr->next, (unsigned long long)FGL_CHUNK);
-            __threadfence_block();
-            atomicExch(&c.pos, 0u);
-        } else {
-            while (*(volatile unsigned int *)&c.pos >= FGL_CHUNK) __nanosleep(32);
-        }
-    }
 }
 
 #ifndef FGL_FOLD
@@ -922,21 +937,52 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
     }
 }
 
+// The leaf phase of one while-while iteration: every lane holding a postponed leaf tests its
+// triangles (watertight test, (t, id) lexicographic minimum), then takes the next postponed leaf if
+// its descent ended on one.
+template <int PERM, bool kCount>
+__device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre &p, float tmin, bool active, Hit &h,
+                                       float &tlim, uint64_t *st, int &sp, int32_t &cur, int32_t &leaf) {
+    if (!active) return;
+    while (leaf < 0) {
+        const int32_t v = ~leaf;
+        const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
+        for (int32_t k = first; k < first + cnt; ++k) {
+            const float4 *tp = tri + 3 * (int64_t)k;
+            const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+            const int32_t id = __float_as_int(a.w);
+            if (kCount) ++h.tris;
+            float t;
+            if (hit_tri<PERM>(p, a, b, c, tmin, h.t, h.id, id, t)) {
+                h.t = t;
+                h.id = id;
+                tlim = t * kExpand;
+            }
+        }
+        leaf = 0;
+        if (cur < 0) {
+            leaf = cur;
+            cur = pop_live(st, sp, tlim);
+        }
+    }
+}
+
+#ifndef FGL_PERM
+#define FGL_PERM 0  // shear-permutation-specialised leaf phase (needs FGL_SHEAR_MATRIX = 0)
+#endif
 #ifndef FGL_OCTANT
 #define FGL_OCTANT 1  // octant-specialised descent when a warp's rays share an octant
 #endif
-#ifndef FGL_REFILL
-#define FGL_REFILL 32
-#endif
+// Per-ray BVH2 traversal, persistent warps: a warp takes a 32-ray tile from a self-resetting global
+// counter when all its lanes are done (refilling single lanes earlier was measured slower: it mixes
+// rays of distant tiles), generates the rays in registers and runs the while-while traversal of
+// Aila & Laine (2009) one outer iteration at a time. The output slot (and, for hit points, the ray)
+// is recomputed from (tile, lane) at the write, so neither is held in registers during traversal.
 template <class Gen, bool kCount>
-__global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
+__global__ void __launch_bounds__(kCastThreads, FGL_DYN_MINBLOCKS)
     k_cast_dyn(const SceneView sv, const Gen gen, int64_t ntiles, const CastOut out, CastCounter *ctr) {
     constexpr unsigned kFull = 0xffffffffu;
-    __shared__ ChunkState s_chunk;
-    if (threadIdx.x == 0) s_chunk.base = 0ull, s_chunk.pos = FGL_CHUNK;
-    __syncthreads();
     const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
     uint64_t st[kStack];  // (entry t bits << 32) | node ref
     int sp = 0;
     int32_t cur = kDone, leaf = 0;
@@ -945,91 +991,66 @@ __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
     Hit h{0.f, INT_MAX, 0, 0};
     float tlim = 0.f;  // h.t * kExpand, the pop bound, updated with h.t
     const Node64 *__restrict__ nodes = sv.nodes;
-    Ray r;
-    int64_t idx = 0;
-    float tmin = 0.f;
+    const float tmin = gen.interval_min();
     bool active = false;
     unsigned long long wtile = 0;
-    int wpos = 32;  // rays of the warp's current tile already handed out
-    bool exhausted = false;
     while (true) {
-        const unsigned idle = __ballot_sync(kFull, !active);
-        if (idle == kFull && exhausted) break;
-        if (!exhausted && __popc(idle) >= (idle == kFull ? 1 : FGL_REFILL)) {
-            const int need = __popc(idle), rank = __popc(idle & lt);
-            const int avail = 32 - wpos;
-            unsigned long long tile = wtile;
-            int slot = wpos + rank;
-            if (need > avail) {
-                unsigned long long nt = 0;
-                if (lane == 0) nt = next_tile(ctr, s_chunk);
-                nt = __shfl_sync(kFull, nt, 0);
-                if (rank >= avail) tile = nt, slot = rank - avail;
-                wtile = nt;
-                wpos = need - avail;
-                if (nt >= (unsigned long long)ntiles) exhausted = true;
-            } else {
-                wpos += need;
-            }
-            if (!active && tile < (unsigned long long)ntiles) {
-                float tmax;
-                if (gen.ray((int64_t)tile, slot, r, idx, tmin, tmax)) {
-                    p = precompute(r);
-                    oct = ray_octant(p);
-                    h = Hit{tmax, INT_MAX, 0, 0};
-                    tlim = tmax * kExpand;
-                    sp = 0, cur = 0, leaf = 0;
-                    active = true;
-                }
+        if (!__any_sync(kFull, active)) {
+            unsigned long long nt = 0;
+            if (lane == 0) nt = atomicAdd(&ctr->next, 1ull);
+            wtile = __shfl_sync(kFull, nt, 0);
+            if (wtile >= (unsigned long long)ntiles) break;
+            Ray r;
+            if (gen.ray_at((int64_t)wtile, lane, r)) {
+                p = precompute(r);
+                oct = ray_octant(p);
+                h = Hit{gen.interval_max(), INT_MAX, 0, 0};
+                tlim = h.t * kExpand;
+                sp = 0, cur = 0, leaf = 0;
+                active = true;
             }
         }
         // ---- one outer iteration of the while-while traversal ----
         // Every lane of the warp runs the descent loop (idle / finished lanes predicated off), so the
         // speculation vote is a plain full-warp vote. When all active lanes share a ray octant (the
         // usual case: a tile spans ~1.5 degrees) the loop is the octant-specialised instance.
-        const unsigned act = __ballot_sync(kFull, active);
-        if (act) {
 #if FGL_OCTANT
-            const int o0 = __shfl_sync(kFull, oct, __ffs(act) - 1);
-            if (__all_sync(kFull, !active || oct == o0)) {
-                switch (o0) {
-                    case 0: descend<0, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 1: descend<1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 2: descend<2, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 3: descend<3, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 4: descend<4, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 5: descend<5, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 6: descend<6, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    default: descend<7, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                }
-            } else
+        const unsigned act = __ballot_sync(kFull, active);
+        const int o0 = __shfl_sync(kFull, oct, __ffs(act) - 1);
+        if (__all_sync(kFull, !active || oct == o0)) {
+            switch (o0) {
+                case 0: descend<0, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 1: descend<1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 2: descend<2, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 3: descend<3, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 4: descend<4, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 5: descend<5, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 6: descend<6, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                default: descend<7, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+            }
+        } else
 #endif
-                descend<-1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf);
-        }
+            descend<-1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf);
+#if FGL_PERM
+        // leaf phase: the axis permutation of the watertight shear is warp-uniform in most tiles
+        const int q0 = __shfl_sync(kFull, p.perm, __ffs(__ballot_sync(kFull, active)) - 1);
+        if (__all_sync(kFull, !active || p.perm == q0)) {
+            switch (q0) {
+                case 0: leaves<0, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 1: leaves<1, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 2: leaves<2, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 3: leaves<3, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                case 4: leaves<4, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                default: leaves<5, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+            }
+        } else
+#endif
+            leaves<-1, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
         if (!active) continue;
-        while (leaf < 0) {
-            const int32_t v = ~leaf;
-            const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
-            for (int32_t k = first; k < first + cnt; ++k) {
-                const float4 *tp = sv.tri + 3 * (int64_t)k;
-                const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
-                const int32_t id = __float_as_int(a.w);
-                if (kCount) ++h.tris;
-                float t;
-                if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, t)) {
-                    h.t = t;
-                    h.id = id;
-                    tlim = t * kExpand;
-                }
-            }
-            leaf = 0;
-            if (cur < 0) {
-                leaf = cur;
-                cur = pop_live(st, sp, tlim);
-            }
-        }
         if (cur == kDone) {
-            write_out(out, idx, r, h);
+            Ray r{};
+            if (out.hit_xyz) gen.ray_at((int64_t)wtile, lane, r);
+            write_out(out, gen.index((int64_t)wtile, lane), r, h);
             active = false;
         }
     }
