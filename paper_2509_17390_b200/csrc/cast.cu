@@ -21,9 +21,6 @@ namespace fgl {
 
 namespace {
 
-#ifndef FGL_SHEAR_MATRIX
-#define FGL_SHEAR_MATRIX 0  // watertight shear as a 3x3 matrix (9 registers; else axis selects, 4)
-#endif
 #ifndef FGL_APPROX_PRE
 #define FGL_APPROX_PRE 1  // MUFU reciprocals for the per-ray slab / shear constants
 #endif
@@ -46,19 +43,14 @@ struct Ray {
 //    and the relative part into the 1 + 2^-20 factor on t_far. Conservative: never culls a box the
 //    exact ray touches.
 //  * watertight test (Woop, Benthin, Wald 2013): kz = argmax |d|, shear S; the axis permutation is
-//    folded into a 3x3 matrix M (rows e_kx - Sx e_kz, e_ky - Sy e_kz, Sz e_kz) so the transform is
-//    branch-free; the products by 0 and 1 are exact, so each sheared coordinate carries at most two
-//    roundings, identical for a vertex shared by two triangles (watertightness).
+//    a cyclic rotation of the coordinates chosen by selects (branch-free); each sheared coordinate
+//    carries at most two roundings, identical for a vertex shared by two triangles (watertightness).
 struct Pre {
     float ox, oy, oz;
     float Ix, Iy, Iz;
     float clx, chx, cly, chy, clz, chz;
-#if FGL_SHEAR_MATRIX
-    float m0x, m0y, m0z, m1x, m1y, m1z, m2x, m2y, m2z;
-#else
-    float Sx, Sy, Sz;
-    int perm;  // 2 kz + (d_kz < 0): kz = argmax |d_a|, kx = kz + 1, ky = kx + 1 (mod 3), swapped if d_kz < 0
-#endif
+    float Sx, Sy, Sz;  // shear: S_x = d_kx / d_kz, S_y = d_ky / d_kz, S_z = 1 / d_kz
+    int kz;            // argmax |d_a|; the shear axes are kx = kz + 1, ky = kz + 2 (mod 3)
 };
 
 // 1/x by MUFU.RCP (rcp.approx.ftz.f32, <= 1 ulp); |x| >= 2^-80 here, so no denormal is flushed
@@ -90,14 +82,10 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
     p.clz = p.Iz >= 0.f ? cz - az : cz + az, p.chz = p.Iz >= 0.f ? cz + az : cz - az;
     const float fx = fabsf(r.dx), fy = fabsf(r.dy), fz = fabsf(r.dz);
     const int kz = (fx >= fy) ? (fx >= fz ? 0 : 2) : (fy >= fz ? 1 : 2);
-    int kx = kz == 2 ? 0 : kz + 1;
-    int ky = kx == 2 ? 0 : kx + 1;
+    // no kx/ky swap for d_kz < 0: it only orients the winding (see shear), the test is two-sided
+    const int kx = kz == 2 ? 0 : kz + 1;
+    const int ky = kx == 2 ? 0 : kx + 1;
     const float dkz = kz == 0 ? r.dx : (kz == 1 ? r.dy : r.dz);
-    if (dkz < 0.f) {
-        const int t = kx;
-        kx = ky;
-        ky = t;
-    }
     const float dkx = kx == 0 ? r.dx : (kx == 1 ? r.dy : r.dz);
     const float dky = ky == 0 ? r.dx : (ky == 1 ? r.dy : r.dz);
 #if FGL_APPROX_PRE
@@ -105,20 +93,8 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
 #else
     const float Sx = __fdiv_rn(dkx, dkz), Sy = __fdiv_rn(dky, dkz), Sz = __frcp_rn(dkz);
 #endif
-#if FGL_SHEAR_MATRIX
-    p.m0x = kx == 0 ? 1.f : (kz == 0 ? -Sx : 0.f);
-    p.m0y = kx == 1 ? 1.f : (kz == 1 ? -Sx : 0.f);
-    p.m0z = kx == 2 ? 1.f : (kz == 2 ? -Sx : 0.f);
-    p.m1x = ky == 0 ? 1.f : (kz == 0 ? -Sy : 0.f);
-    p.m1y = ky == 1 ? 1.f : (kz == 1 ? -Sy : 0.f);
-    p.m1z = ky == 2 ? 1.f : (kz == 2 ? -Sy : 0.f);
-    p.m2x = kz == 0 ? Sz : 0.f;
-    p.m2y = kz == 1 ? Sz : 0.f;
-    p.m2z = kz == 2 ? Sz : 0.f;
-#else
     p.Sx = Sx, p.Sy = Sy, p.Sz = Sz;
-    p.perm = 2 * kz + (dkz < 0.f ? 1 : 0);
-#endif
+    p.kz = kz;
     return p;
 }
 
@@ -127,43 +103,26 @@ struct V3 {
 };
 
 // Sheared coordinates of a vertex relative to the ray origin: (A_kx - Sx A_kz, A_ky - Sy A_kz, Sz A_kz)
-// with A = v - o. PERM >= 0: the warp-uniform axis permutation, fixed at compile time; PERM = -1:
-// the ray's own permutation by selects. Both evaluate the same two roundings per coordinate, so a
-// vertex shared by two triangles gets the same sheared coordinates in either form (watertightness).
-template <int PERM>
+// with A = v - o (two roundings per coordinate, the same for every triangle sharing the vertex).
 __device__ __forceinline__ V3 shear(const Pre &p, float4 v) {
     const float X = v.x - p.ox, Y = v.y - p.oy, Z = v.z - p.oz;
-#if FGL_SHEAR_MATRIX
-    // the permutation folded into a 3x3 matrix (entries 1, -S or 0: the products by 0 and 1 are exact)
-    return V3{fmaf(p.m0z, Z, fmaf(p.m0y, Y, p.m0x * X)), fmaf(p.m1z, Z, fmaf(p.m1y, Y, p.m1x * X)),
-              fmaf(p.m2z, Z, fmaf(p.m2y, Y, p.m2x * X))};
-#else
-    float Ax, Ay, Az;
-    if constexpr (PERM >= 0) {
-        constexpr int kz = PERM >> 1, k1 = kz == 2 ? 0 : kz + 1, k2 = k1 == 2 ? 0 : k1 + 1;
-        constexpr int kx = (PERM & 1) ? k2 : k1, ky = (PERM & 1) ? k1 : k2;
-        Ax = kx == 0 ? X : (kx == 1 ? Y : Z);
-        Ay = ky == 0 ? X : (ky == 1 ? Y : Z);
-        Az = kz == 0 ? X : (kz == 1 ? Y : Z);
-    } else {
-        const int kz = p.perm >> 1, k1 = kz == 2 ? 0 : kz + 1, k2 = k1 == 2 ? 0 : k1 + 1;
-        const int kx = (p.perm & 1) ? k2 : k1, ky = (p.perm & 1) ? k1 : k2;
-        Ax = kx == 0 ? X : (kx == 1 ? Y : Z);
-        Ay = ky == 0 ? X : (ky == 1 ? Y : Z);
-        Az = kz == 0 ? X : (kz == 1 ? Y : Z);
-    }
+    // (A_kx, A_ky, A_kz) is the cyclic rotation of (X, Y, Z) that ends on kz, by branch-free selects.
+    // The swap of kx and ky for d_kz < 0 in Woop et al. only orients the winding: it negates U, V, W,
+    // T and det exactly (IEEE negation is exact), so a two-sided test returns the same t without it.
+    const bool r0 = p.kz == 0, r1 = p.kz == 1;
+    const float Ax = r0 ? Y : (r1 ? Z : X);
+    const float Ay = r0 ? Z : (r1 ? X : Y);
+    const float Az = r0 ? X : (r1 ? Y : Z);
     return V3{fmaf(-p.Sx, Az, Ax), fmaf(-p.Sy, Az, Ay), p.Sz * Az};
-#endif
 }
 
 // Watertight ray/triangle test (two-sided, inclusive edges). Edge functions are evaluated without
 // FMA contraction so that the two triangles of a shared edge see exactly opposite values; an
 // exactly-zero edge function is re-evaluated in double (float products are exact there).
 // Returns true and t when t is in [tmin, best_t] and (t, id) beats (best_t, best_id).
-template <int PERM = -1>
 __device__ __forceinline__ bool hit_tri(const Pre &p, float4 a, float4 b, float4 c, float tmin, float best_t,
                                         int32_t best_id, int32_t id, float &t_out) {
-    const V3 A = shear<PERM>(p, a), B = shear<PERM>(p, b), C = shear<PERM>(p, c);
+    const V3 A = shear(p, a), B = shear(p, b), C = shear(p, c);
     float U = __fsub_rn(__fmul_rn(C.x, B.y), __fmul_rn(C.y, B.x));
     float V = __fsub_rn(__fmul_rn(A.x, C.y), __fmul_rn(A.y, C.x));
     float W = __fsub_rn(__fmul_rn(B.x, A.y), __fmul_rn(B.y, A.x));
@@ -940,7 +899,7 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
 // The leaf phase of one while-while iteration: every lane holding a postponed leaf tests its
 // triangles (watertight test, (t, id) lexicographic minimum), then takes the next postponed leaf if
 // its descent ended on one.
-template <int PERM, bool kCount>
+template <bool kCount>
 __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre &p, float tmin, bool active, Hit &h,
                                        float &tlim, uint64_t *st, int &sp, int32_t &cur, int32_t &leaf) {
     if (!active) return;
@@ -953,7 +912,7 @@ __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre
             const int32_t id = __float_as_int(a.w);
             if (kCount) ++h.tris;
             float t;
-            if (hit_tri<PERM>(p, a, b, c, tmin, h.t, h.id, id, t)) {
+            if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, t)) {
                 h.t = t;
                 h.id = id;
                 tlim = t * kExpand;
@@ -967,9 +926,6 @@ __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre
     }
 }
 
-#ifndef FGL_PERM
-#define FGL_PERM 0  // shear-permutation-specialised leaf phase (needs FGL_SHEAR_MATRIX = 0)
-#endif
 #ifndef FGL_OCTANT
 #define FGL_OCTANT 1  // octant-specialised descent when a warp's rays share an octant
 #endif
@@ -1031,21 +987,7 @@ __global__ void __launch_bounds__(kCastThreads, FGL_DYN_MINBLOCKS)
         } else
 #endif
             descend<-1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf);
-#if FGL_PERM
-        // leaf phase: the axis permutation of the watertight shear is warp-uniform in most tiles
-        const int q0 = __shfl_sync(kFull, p.perm, __ffs(__ballot_sync(kFull, active)) - 1);
-        if (__all_sync(kFull, !active || p.perm == q0)) {
-            switch (q0) {
-                case 0: leaves<0, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 1: leaves<1, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 2: leaves<2, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 3: leaves<3, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 4: leaves<4, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                default: leaves<5, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-            }
-        } else
-#endif
-            leaves<-1, kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
+        leaves<kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
         if (!active) continue;
         if (cur == kDone) {
             Ray r{};
