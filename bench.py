@@ -858,7 +858,7 @@ def main():
             "nodes_per_ray": n_nodes, "tris_per_ray": n_tris,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": achieved / alu_peak, "traffic": traffic, "kernel": "k_cast",
-                         "note": f"issue-bound traversal (ncu: ~75% issue-slot use, DRAM idle, L2 hit ~85%): "
+                         "note": f"issue-bound traversal (ncu: ~77% issue-slot use, 40 warps/SM, DRAM nearly idle, L1/L2 hit ~72/85%): "
                                  f"algorithmic FP32 ops/ray = {OPS_NODE}*nodes + {OPS_TRI}*tris = {ops_per_ray:.0f} "
                                  f"(DESIGN.md §6); peak = 148 SM x 128 FP32 lanes x 1.965 GHz (unit counts + max "
                                  f"clock); t_cast from CUDA events on the launch stream; traffic = ncu DRAM bytes "

@@ -811,6 +811,9 @@ inline bool packet_mode() {
     return v == 1;
 }
 
+#ifndef FGL_DESCEND_UNROLL
+#define FGL_DESCEND_UNROLL 1  // node visits between two speculation votes
+#endif
 #ifndef FGL_FOLD
 #define FGL_FOLD 0  // octant descent: far-plane slack folded into the far-plane constants
 #endif
@@ -855,7 +858,10 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
     const FarPlanes fp = far_planes<OCT < 0 ? 0 : OCT>(p);
 #endif
     while (true) {
-        const bool go = active && cur >= 0 && cur != kDone;
+        bool go = false;
+#pragma unroll
+        for (int u = 0; u < FGL_DESCEND_UNROLL; ++u) {  // nodes per warp vote
+        go = active && cur >= 0 && cur != kDone;
         if (go) {
             float4 na, nb, nc, ndf;
             ldg_node(nodes + cur, na, nb, nc, ndf);
@@ -891,6 +897,7 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
                 leaf = cur;
                 cur = pop_live(st, sp, tlim);
             }
+        }
         }
         if (!__any_sync(0xffffffffu, go && leaf == 0)) break;
     }
