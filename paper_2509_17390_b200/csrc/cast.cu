@@ -811,6 +811,9 @@ inline bool packet_mode() {
     return v == 1;
 }
 
+#ifndef FGL_CARVEOUT
+#define FGL_CARVEOUT 10  // k_cast_dyn shared-memory carveout in percent (-1: driver default); 5-14 measured equal
+#endif
 #ifndef FGL_DESCEND_UNROLL
 #define FGL_DESCEND_UNROLL 1  // node visits between two speculation votes
 #endif
@@ -1015,8 +1018,14 @@ void launch_one(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastO
         int dev;
         FGL_CUDA(cudaGetDevice(&dev));
         FGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (kDyn)
+        if (kDyn) {
+#if FGL_CARVEOUT >= 0
+            // the kernel uses no shared memory: ask for the largest L1 share (node / triangle reuse)
+            FGL_CUDA(cudaFuncSetAttribute(k_cast_dyn<Gen, kCount>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          FGL_CARVEOUT));
+#endif
             FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast_dyn<Gen, kCount>, kCastThreads, 0));
+        }
         else
             FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast<Gen, kCount, kMode>, kCastThreads, 0));
         if (oc < 1) oc = 1;
