@@ -170,6 +170,27 @@ def _alu_peak_tops():
     return 148 * 128 * mhz * 1e6 / 1e12
 
 
+def _l2_read_gbs(fgl, torch, dev, stream):
+    """L2 read bandwidth measured in the run: libfgl's probe re-reads an L2-resident
+    buffer (half the L2) with 128-bit L1-bypassing loads from every SM; best of 5 timed launches."""
+    l2 = int(torch.cuda.get_device_properties(dev).L2_cache_size)
+    buf = torch.zeros(max(1 << 20, l2 // 2) // 16 * 4, dtype=torch.float32, device=dev)
+    sink = torch.zeros(1, dtype=torch.float32, device=dev)
+    iters = 40
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            fgl.l2_read_probe(buf, iters, sink)
+        best = float("inf")
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fgl.l2_read_probe(buf, iters, sink)
+            e1.record(stream)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+    return buf.numel() * 4 * iters / (best / 1000) / 1e9, l2
+
+
 def _ncu_traffic(config: str, kernel: str = "k_cast"):
     """dram read+write bytes per launch of the dominant kernel from the committed ncu summary."""
     try:
@@ -837,6 +858,10 @@ def main():
     if rank == 0 and world == 1 and not a.no_cpu:
         cpu = _cpu_baseline(cfg, a.cpu_seconds)
 
+    l2_gbs, l2_bytes = (None, None)
+    if rank == 0:
+        l2_gbs, l2_bytes = _l2_read_gbs(fgl, torch, dev, stream)  # after the launch count and timings
+
     if rank == 0:
         st = scene.stats()
         total_rays = rays_rank * world
@@ -866,7 +891,11 @@ def main():
             "memory": {"algorithmic_bytes_per_ray": bytes_per_ray,
                        "achieved_gbs": bytes_per_ray * rays_rank / (cms / 1000) / 1e9,
                        "hbm_peak_gbs": hbm_peak, "hbm_peak_kind": peak_kind,
-                       "note": "node (64 B) + triangle (48 B) fetches + 8 B output per ray, mostly L1/L2-served"},
+                       "l2_read_gbs": l2_gbs, "l2_bytes": l2_bytes, "l2_kind": "measured in this run (fgl_l2_read_probe)",
+                       "frac_of_l2": bytes_per_ray * rays_rank / (cms / 1000) / 1e9 / l2_gbs if l2_gbs else None,
+                       "note": "node (64 B) + triangle (48 B) fetches + 8 B output per ray, mostly L1/L2-served; "
+                               "frac_of_l2 = algorithmic bytes/s over the measured L2 read bandwidth (the scene's "
+                               "node + triangle working set fits in L2 for C2/C4; L1 hits serve part of it)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

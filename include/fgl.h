@@ -315,6 +315,16 @@ FGL_API fgl_status fgl_morton_codes(const float *points, int64_t n, const float 
  * (1..64), n < 2^30. Allocates its scratch with cudaMallocAsync on the stream. */
 FGL_API fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key_bits, void *cuda_stream);
 
+/* ---- measurement --------------------------------------------------------------------------
+ * L2 read-bandwidth probe (the roofline of an L2-resident traversal is the L2, whose
+ * bandwidth is measured in the run, not assumed). Enqueues on cuda_stream one kernel that reads the
+ * device buffer `buf` (`bytes` >= 16, a multiple of 16, 16-B aligned; pick it well below the L2
+ * size so it stays resident) `iters` >= 1 times with 128-bit L1-bypassing loads (ld.global.cg)
+ * from every SM, and writes one float (a checksum that keeps the loads alive) to `sink` (device).
+ * The caller times the launch with CUDA events: GB/s = bytes * iters / time. Errors: FGL_E_USAGE
+ * for NULL pointers / bad sizes, FGL_E_CUDA for launch failures. */
+FGL_API fgl_status fgl_l2_read_probe(const void *buf, int64_t bytes, int32_t iters, float *sink, void *cuda_stream);
+
 /* ---- misc ----------------------------------------------------------------------------- */
 FGL_API const char *fgl_last_error(void); /* thread-local; valid until the next fgl call on the thread */
 FGL_API const char *fgl_version(void);

@@ -725,6 +725,15 @@ fgl_status fgl_cast_spinning_gather(const fgl_scene *s, const fgl_spinning *patt
                                            stream);
 }
 
+fgl_status fgl_l2_read_probe(const void *buf, int64_t bytes, int32_t iters, float *sink, void *stream) {
+    FGL_API_BEGIN
+    if (!buf || !sink) throw Error(FGL_E_USAGE, "buffer / sink is NULL");
+    if (bytes < 16 || bytes % 16 || ((uintptr_t)buf & 15)) throw Error(FGL_E_USAGE, "bytes must be a positive multiple of 16, buffer 16-B aligned");
+    if (iters < 1) throw Error(FGL_E_USAGE, "iters must be >= 1");
+    fgl::launch_l2_read(buf, bytes, iters, sink, (cudaStream_t)stream);
+    FGL_API_END
+}
+
 fgl_status fgl_wait_flag(const int32_t *flag, int32_t target, void *stream) {
     FGL_API_BEGIN
     if (!flag) throw Error(FGL_E_USAGE, "flag is NULL");

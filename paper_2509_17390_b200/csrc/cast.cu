@@ -1207,6 +1207,25 @@ __global__ void k_wait_flag(const int32_t *flag, int32_t target) {
     }
 }
 
+// L2 read-bandwidth probe: grid-stride 128-bit L1-bypassing loads over an L2-resident buffer
+__global__ void __launch_bounds__(512) k_l2_read(const float4 *__restrict__ p, int64_t n4, int iters, float *sink) {
+    float acc = 0.f;
+    for (int it = 0; it < iters; ++it)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+            const float4 v = __ldcg(p + i);
+            acc += (v.x + v.y) + (v.z + v.w);
+        }
+    if (acc == 1234.5f) *sink = acc;  // never true for the zero-filled probe buffer; keeps the loads
+}
+
+void launch_l2_read(const void *buf, int64_t bytes, int iters, float *sink, cudaStream_t s) {
+    int dev, sms;
+    FGL_CUDA(cudaGetDevice(&dev));
+    FGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    k_l2_read<<<sms * 4, 512, 0, s>>>(reinterpret_cast<const float4 *>(buf), bytes / 16, iters, sink);
+    FGL_LAUNCHED("k_l2_read");
+}
+
 void launch_wait_flag(const int32_t *flag, int32_t target, cudaStream_t s) {
     k_wait_flag<<<1, 32, 0, s>>>(flag, target);
     FGL_LAUNCHED("k_wait_flag");

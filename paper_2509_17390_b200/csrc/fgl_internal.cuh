@@ -176,6 +176,7 @@ void launch_cast_bruteforce(const float *verts, int64_t V, const int32_t *tris, 
                             const float *dir,
                             int64_t R, float t_min, float t_max, float *range, int32_t *tri_id, cudaStream_t s);
 void launch_wait_flag(const int32_t *flag, int32_t target, cudaStream_t s);
+void launch_l2_read(const void *buf, int64_t bytes, int iters, float *sink, cudaStream_t s);
 // gauss.cu
 struct VoxGrid {
     double origin[3];

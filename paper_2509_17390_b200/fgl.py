@@ -86,6 +86,7 @@ _SIGS = {
     "fgl_cast_spinning_gather_signal": (c_int, [c_void_p, POINTER(SpinningC), c_void_p, c_int64, c_int64, c_void_p,
                                                 c_void_p, c_void_p, c_int32, c_void_p]),
     "fgl_wait_flag": (c_int, [c_void_p, c_int32, c_void_p]),
+    "fgl_l2_read_probe": (c_int, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     "fgl_scene_upload_points": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p]),
     "fgl_nearest": (c_int, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
     "fgl_cloud_metrics": (c_int, [c_void_p, c_int64, c_void_p, c_int64, c_float, c_void_p, c_void_p]),
@@ -671,6 +672,12 @@ def marching_cubes(phi: torch.Tensor, origin, spacing, iso: float = 0.0, normals
     if normals:
         res["normals"] = nrm[:sized[0]]
     return res
+
+
+def l2_read_probe(buf: torch.Tensor, iters: int, sink: torch.Tensor, stream=None) -> None:
+    """Enqueue the L2 read-bandwidth probe over the device tensor `buf` (fgl_l2_read_probe)."""
+    _check(lib().fgl_l2_read_probe(buf.data_ptr(), buf.numel() * buf.element_size(), int(iters), sink.data_ptr(),
+                                   _stream(stream)))
 
 
 def kernel_launches() -> int:

@@ -26,6 +26,23 @@ def test_bench_json_line():
     assert d["gpu_launches"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
+    m = d["memory"]
+    assert m["l2_read_gbs"] > m["hbm_peak_gbs"] * 0.5 and m["l2_bytes"] > 0 and m["frac_of_l2"] > 0
+
+
+def test_l2_probe_arguments():
+    import torch
+
+    import paper_2509_17390_b200 as fgl
+    buf = torch.zeros(1 << 16, dtype=torch.float32, device="cuda")
+    sink = torch.zeros(1, dtype=torch.float32, device="cuda")
+    fgl.l2_read_probe(buf, 2, sink)
+    torch.cuda.synchronize()
+    assert sink.item() == 0.0  # the checksum of a zero buffer is never stored
+    with pytest.raises(fgl.FglError):
+        fgl.l2_read_probe(buf[1:], 1, sink)  # 16-B misaligned, size not a multiple of 16
+    with pytest.raises(fgl.FglError):
+        fgl.l2_read_probe(buf, 0, sink)
 
 
 def test_voxel_bench_json_line():
