@@ -63,6 +63,9 @@ __device__ __forceinline__ bool bit_at(const uint32_t *__restrict__ v, const Dim
 
 // ---- Eq. 13-14 -------------------------------------------------------------------------------
 constexpr int kMaxTaps = 129;  // radius <= 64 voxels
+#ifndef FGL_BLUR_TILE
+#define FGL_BLUR_TILE 1  // shared-memory tiled y / z blur passes
+#endif
 struct Taps {
     float w[kMaxTaps];
     int R;
@@ -94,6 +97,33 @@ __global__ void __launch_bounds__(256) k_blur(const uint32_t *__restrict__ bits,
             }
         }
         out[i] = acc;
+    }
+}
+
+// y / z passes, tiled: a 64 x 4 block stages kBlurL output lines of its 64-wide x strip plus the
+// 2R halo lines in shared memory (each input read once from global memory instead of 2R + 1 times)
+// and sums the taps from there. Same taps, same order, same FMAs as k_blur (a halo line outside
+// the volume is staged as 0, and fma(w, 0, acc) = acc for acc >= 0), so the result is identical.
+constexpr int kBlurL = 32;
+__global__ void __launch_bounds__(256) k_blur_tile(const float *__restrict__ in, float *__restrict__ out, Dims d,
+                                                   int axis, Taps t) {
+    extern __shared__ float sm[];  // [kBlurL + 2R][64]
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int x = blockIdx.x * 64 + tx;
+    const int n = axis == 1 ? d.ny : d.nz;
+    const int64_t stride = axis == 1 ? d.nx : (int64_t)d.nx * d.ny;
+    const int64_t base = axis == 1 ? (int64_t)blockIdx.z * d.nx * d.ny : (int64_t)blockIdx.z * d.nx;
+    const int c0 = blockIdx.y * kBlurL, R = t.R, nl = kBlurL + 2 * R;
+    for (int l = ty; l < nl; l += 4) {
+        const int c = c0 - R + l;
+        sm[l * 64 + tx] = (x < d.nx && c >= 0 && c < n) ? __ldg(in + base + (int64_t)c * stride + x) : 0.f;
+    }
+    __syncthreads();
+    if (x >= d.nx) return;
+    for (int j = ty; j < kBlurL && c0 + j < n; j += 4) {
+        float acc = 0.f;
+        for (int k = -R; k <= R; ++k) acc = fmaf(t.w[k + R], sm[(j + k + R) * 64 + tx], acc);
+        out[base + (int64_t)(c0 + j) * stride + x] = acc;
     }
 }
 
@@ -796,8 +826,19 @@ void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, 
         double sum = 0;
         for (int k = -t.R; k <= t.R; ++k) sum += std::exp(-0.5 * (k / sv) * (k / sv));
         for (int k = -t.R; k <= t.R; ++k) t.w[k + t.R] = (float)(std::exp(-0.5 * (k / sv) * (k / sv)) / sum);
-        k_blur<<<grid2d(d), dim3(64, 4), 0, s>>>(occ, src, dst[ax], d, ax, t);
-        FGL_LAUNCHED("k_blur");
+        const int other = ax == 1 ? d.nz : d.ny;
+        if (ax > 0 && other <= 65535 && FGL_BLUR_TILE) {
+            const int n = ax == 1 ? d.ny : d.nz;
+            const dim3 g((d.nx + 63) / 64, (n + kBlurL - 1) / kBlurL, other);
+            const size_t smem = sizeof(float) * 64 * (kBlurL + 2 * t.R);
+            if (smem > 48 * 1024)
+                FGL_CUDA(cudaFuncSetAttribute(k_blur_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_blur_tile<<<g, dim3(64, 4), smem, s>>>(src, dst[ax], d, ax, t);
+            FGL_LAUNCHED("k_blur_tile");
+        } else {
+            k_blur<<<grid2d(d), dim3(64, 4), 0, s>>>(occ, src, dst[ax], d, ax, t);
+            FGL_LAUNCHED("k_blur");
+        }
         src = dst[ax];
     }
     if (!quantile) {
