@@ -589,18 +589,37 @@ struct Scan3 {
     uint32_t *a[3];
 };
 
+// Blocked layout: thread t of a tile owns the kScanItems consecutive elements [16 t, 16 t + 16),
+// read and written as four 128-bit words (arrays are 256-B aligned, tiles 4096 elements); the
+// ragged last tile falls back to scalar accesses.
+__device__ __forceinline__ void load16(const uint32_t *a, int64_t i, int64_t n, uint32_t (&v)[kScanItems]) {
+    if (i + kScanItems <= n) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(a + i);
+#pragma unroll
+        for (int k = 0; k < kScanItems / 4; ++k) {
+            const uint4 u = p[k];
+            v[4 * k] = u.x, v[4 * k + 1] = u.y, v[4 * k + 2] = u.z, v[4 * k + 3] = u.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) v[k] = i + k < n ? a[i + k] : 0u;
+    }
+}
+
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(Scan3 in, int64_t n, unsigned long long *__restrict__ part,
                                                               int nb) {
     __shared__ unsigned long long s_w[kScanThreads / 32];
-    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    const int64_t i0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[3][kScanItems];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) load16(in.a[q], i0, n, v[q]);  // all 12 loads in flight together
+#pragma unroll
     for (int q = 0; q < 3; ++q) {
-        unsigned long long v = 0;
-        for (int k = 0; k < kScanItems; ++k) {
-            const int64_t idx = base + k * kScanThreads + threadIdx.x;
-            if (idx < n) v += in.a[q][idx];
-        }
+        unsigned long long sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) sum += v[q][k];
         unsigned long long tot;
-        block_excl(v, s_w, tot);
+        block_excl(sum, s_w, tot);
         if (threadIdx.x == 0) part[q * nb + blockIdx.x] = tot;
     }
 }
@@ -621,38 +640,38 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_parts(unsigned long long 
     if (threadIdx.x == 0) total[q] = carry;
 }
 
-// in place: each block reads its tile before writing it; coalesced striped loads/stores through
-// shared memory, each thread scanning 16 consecutive elements (padded rows: no bank conflicts)
+// in place: each thread reads its 16 elements before writing them back
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(Scan3 io, int64_t n,
                                                             const unsigned long long *__restrict__ part, int nb) {
     __shared__ unsigned long long s_w[kScanThreads / 32];
-    __shared__ uint32_t s_v[kScanThreads * (kScanItems + 1)];
-    const int64_t tile = (int64_t)blockIdx.x * kScanTile;
-    const int t = threadIdx.x;
+    const int64_t i0 = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    uint32_t v[3][kScanItems];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) load16(io.a[q], i0, n, v[q]);
+#pragma unroll
     for (int q = 0; q < 3; ++q) {
-        for (int k = 0; k < kScanItems; ++k) {  // striped global -> blocked shared
-            const int e = k * kScanThreads + t;
-            const int64_t idx = tile + e;
-            s_v[(e / kScanItems) * (kScanItems + 1) + e % kScanItems] = idx < n ? io.a[q][idx] : 0u;
-        }
-        __syncthreads();
-        uint32_t *mine = s_v + t * (kScanItems + 1);
         unsigned long long sum = 0;
-        for (int k = 0; k < kScanItems; ++k) sum += mine[k];
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) sum += v[q][k];
         unsigned long long tot;
         unsigned long long run = block_excl(sum, s_w, tot) + part[q * nb + blockIdx.x];
+#pragma unroll
         for (int k = 0; k < kScanItems; ++k) {
-            const uint32_t v = mine[k];
-            mine[k] = (uint32_t)run;
-            run += v;
+            const uint32_t x = v[q][k];
+            v[q][k] = (uint32_t)run;
+            run += x;
         }
-        __syncthreads();
-        for (int k = 0; k < kScanItems; ++k) {  // blocked shared -> striped global
-            const int e = k * kScanThreads + t;
-            const int64_t idx = tile + e;
-            if (idx < n) io.a[q][idx] = s_v[(e / kScanItems) * (kScanItems + 1) + e % kScanItems];
+        uint32_t *a = io.a[q];
+        if (i0 + kScanItems <= n) {
+            uint4 *p = reinterpret_cast<uint4 *>(a + i0);
+#pragma unroll
+            for (int k = 0; k < kScanItems / 4; ++k)
+                p[k] = make_uint4(v[q][4 * k], v[q][4 * k + 1], v[q][4 * k + 2], v[q][4 * k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kScanItems; ++k)
+                if (i0 + k < n) a[i0 + k] = v[q][k];
         }
-        __syncthreads();
     }
 }
 
