@@ -194,32 +194,6 @@ __device__ __forceinline__ bool slab_oct(const Pre &p, float lx, float hx, float
     return tn <= tf * kExpand;
 }
 
-// Far planes with the 1 + 2^-20 slack folded in: t_far (1 + 2^-20) is evaluated directly as
-// fma(x, I kE, c_far kE) and compared against t* kE, saving the FMUL per box. The two extra
-// roundings (of I kE and c_far kE) add <= u|t| + 2u|c| (u = 2^-24) to the far value; the plane
-// offsets (4u|c|) and kE = 1 + 16u keep the test conservative.
-struct FarPlanes {
-    float Ix, Iy, Iz, cx, cy, cz;
-};
-template <int OCT>
-__device__ __forceinline__ FarPlanes far_planes(const Pre &p) {
-    constexpr bool sx = OCT & 1, sy = OCT & 2, sz = OCT & 4;
-    return FarPlanes{p.Ix * kExpand, p.Iy * kExpand, p.Iz * kExpand,
-                     (sx ? p.clx : p.chx) * kExpand, (sy ? p.cly : p.chy) * kExpand, (sz ? p.clz : p.chz) * kExpand};
-}
-template <int OCT>
-__device__ __forceinline__ bool slab_oct_fold(const Pre &p, const FarPlanes &f, float lx, float hx, float ly,
-                                              float hy, float lz, float hz, float tmin, float tlim, float &tn_out) {
-    constexpr bool sx = OCT & 1, sy = OCT & 2, sz = OCT & 4;
-    const float nx = fmaf(sx ? hx : lx, p.Ix, sx ? p.chx : p.clx), fx = fmaf(sx ? lx : hx, f.Ix, f.cx);
-    const float ny = fmaf(sy ? hy : ly, p.Iy, sy ? p.chy : p.cly), fy = fmaf(sy ? ly : hy, f.Iy, f.cy);
-    const float nz = fmaf(sz ? hz : lz, p.Iz, sz ? p.chz : p.clz), fz = fmaf(sz ? lz : hz, f.Iz, f.cz);
-    const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, tmin));
-    const float tf = fminf(fminf(fx, fy), fminf(fz, tlim));
-    tn_out = tn;
-    return tn <= tf;
-}
-
 __device__ __forceinline__ int ray_octant(const Pre &p) {
     return (p.Ix < 0.f ? 1 : 0) | (p.Iy < 0.f ? 2 : 0) | (p.Iz < 0.f ? 4 : 0);
 }
@@ -815,10 +789,8 @@ inline bool packet_mode() {
 #define FGL_CARVEOUT 10  // k_cast_dyn shared-memory carveout in percent (-1: driver default); 5-14 measured equal
 #endif
 #ifndef FGL_DESCEND_UNROLL
-#define FGL_DESCEND_UNROLL 1  // node visits between two speculation votes
-#endif
-#ifndef FGL_FOLD
-#define FGL_FOLD 0  // octant descent: far-plane slack folded into the far-plane constants
+#define FGL_DESCEND_UNROLL 1  // node visits between two speculation votes (the loop form, even at 1,
+                              // schedules measurably better than a plain body: keep it)
 #endif
 #ifndef FGL_LDG256
 #define FGL_LDG256 1
@@ -857,9 +829,6 @@ template <int OCT, bool kCount>
 __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const Pre &p, float tmin, bool active,
                                         Hit &h, float tlim, uint64_t *st, int &sp, int32_t &cur,
                                         int32_t &leaf) {
-#if FGL_FOLD
-    const FarPlanes fp = far_planes<OCT < 0 ? 0 : OCT>(p);
-#endif
     while (true) {
         bool go = false;
 #pragma unroll
@@ -872,19 +841,8 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
             if (kCount) ++h.nodes;
             const float lim = h.t;
             float t0, t1;
-#if FGL_FOLD
-            bool h0, h1;
-            if constexpr (OCT >= 0) {
-                h0 = slab_oct_fold<OCT>(p, fp, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, tlim, t0);
-                h1 = slab_oct_fold<OCT>(p, fp, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, tlim, t1);
-            } else {
-                h0 = slab_hit(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim, t0);
-                h1 = slab_hit(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim, t1);
-            }
-#else
             const bool h0 = slab_sel<OCT>(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, lim, t0);
             const bool h1 = slab_sel<OCT>(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim, t1);
-#endif
             if (h0 && h1) {
                 const bool swap = t1 < t0;
                 st[sp++] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
