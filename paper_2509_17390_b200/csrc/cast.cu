@@ -28,7 +28,10 @@ namespace {
 #define FGL_APPROX_NORM 0  // MUFU rsqrt for the direction normalisation (off: exact sqrt + division)
 #endif
 
-constexpr int kCastThreads = 128;
+#ifndef FGL_CAST_THREADS
+#define FGL_CAST_THREADS 128
+#endif
+constexpr int kCastThreads = FGL_CAST_THREADS;
 constexpr int kStack = 96;                   // > max depth of a Karras tree over 63-bit keys + index
 constexpr float kExpand = 1.0f + 0x1p-20f;   // conservative slab test: tfar * (1 + 2 gamma_3) (Ize 2013)
 
