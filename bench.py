@@ -59,6 +59,8 @@ def _args():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-latency", action="store_true", help="skip the single-frame latency measurement")
+    ap.add_argument("--latency-frames", type=int, default=1000, help="CUDA-graph replays of one frame")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU time of the oracle baseline")
     return ap.parse_args()
 
@@ -189,6 +191,39 @@ def _l2_read_gbs(fgl, torch, dev, stream):
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1))
     return buf.numel() * 4 * iters / (best / 1000) / 1e9, l2
+
+
+def _frame_latency(scene, pose1, pat, out, torch, stream, n):
+    """Latency of ONE frame (one pose, every beam) on the built scene: the cast captured in a CUDA
+    graph and replayed n times back to back, each replay bracketed by its own CUDA events on the
+    launch stream (median and p99 over the n replays; L2 warm, as in a frame-by-frame simulation)."""
+    o1 = dict(range=out["range"][:1], tri_id=out["tri_id"][:1])
+    side = torch.cuda.Stream()
+    side.wait_stream(stream)
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            scene.cast(pose1, pat, out=o1)
+    stream.wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        scene.cast(pose1, pat, out=o1)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for _ in range(20):
+            g.replay()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for e0, e1 in ev:
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+    torch.cuda.synchronize()
+    us = sorted(e0.elapsed_time(e1) * 1000.0 for e0, e1 in ev)
+    rays = int(o1["range"].numel())
+    med = us[len(us) // 2]
+    return {"frames": n, "rays_per_frame": rays, "median_us": med, "p99_us": us[min(n - 1, int(0.99 * n))],
+            "frames_per_s": 1e6 / med, "rays_per_s": rays / (med * 1e-6),
+            "note": "one pose per CUDA-graph replay (cast only, prebuilt scene), per-replay CUDA events"}
 
 
 def _ncu_traffic(config: str, kernel: str = "k_cast"):
@@ -788,6 +823,11 @@ def main():
     achieved = ops_per_ray * rays_rank / (cms / 1000) / 1e12
     traffic = _ncu_traffic(a.config)
 
+    # --- single-frame latency: one pose cast per CUDA-graph replay ------------------
+    latency = None
+    if rank == 0 and not a.no_latency:
+        latency = _frame_latency(scene, poses_d[:1].contiguous(), pat, out, torch, stream, a.latency_frames)
+
     # --- e2e through the public API with host buffers --------------------------------------
     # Every step copies its inputs (mesh + poses) from pinned host memory, builds, casts, and reads
     # its results back to pinned host memory. Steps are pipelined over two scenes: the upload of
@@ -896,6 +936,7 @@ def main():
                        "note": "node (64 B) + triangle (48 B) fetches + 8 B output per ray, mostly L1/L2-served; "
                                "frac_of_l2 = algorithmic bytes/s over the measured L2 read bandwidth (the scene's "
                                "node + triangle working set fits in L2 for C2/C4; L1 hits serve part of it)"},
+            "frame_latency": latency,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -26,6 +26,8 @@ def test_bench_json_line():
     assert d["gpu_launches"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle"
+    fl = d["frame_latency"]
+    assert fl["frames"] >= 100 and 0 < fl["median_us"] <= fl["p99_us"] and fl["rays_per_frame"] == 64 * 2048
     m = d["memory"]
     assert m["l2_read_gbs"] > m["hbm_peak_gbs"] * 0.5 and m["l2_bytes"] > 0 and m["frac_of_l2"] > 0
 
