@@ -127,6 +127,57 @@ __global__ void __launch_bounds__(256) k_blur_tile(const float *__restrict__ in,
     }
 }
 
+// x pass from the bit volume, one thread per 32-voxel word (R <= 32, compile time): the word and its
+// two neighbours are loaded once, bits outside [0, nx) are cleared, and every tap of every voxel is a
+// compile-time bit test + FADD. Same taps in the same order as k_blur (a tap whose bit is 0 or that
+// falls outside the row adds nothing there either), so the result is identical. A block covers 256
+// consecutive words of the row-major word array, whose voxels form one contiguous output range:
+// the outputs are staged in shared memory and written out coalesced.
+template <int R>
+__global__ void __launch_bounds__(256) k_blur_x(const uint32_t *__restrict__ bits, float *__restrict__ out, Dims d,
+                                                Taps t) {
+    __shared__ float so[256 * 32];
+    const int64_t nw = d.nw();
+    const int64_t w0 = (int64_t)blockIdx.x * 256, w = w0 + threadIdx.x;
+    float wt[2 * R + 1];
+#pragma unroll
+    for (int k = 0; k < 2 * R + 1; ++k) wt[k] = t.w[k];
+    // output range of the block: voxels of words [w0, w0 + 256) -> [row(w0) nx + x(w0), ...)
+    const int64_t row0 = w0 / d.nwx;
+    const int64_t o0 = row0 * d.nx + (int64_t)(w0 - row0 * d.nwx) * 32;
+    if (w < nw) {
+        const int64_t row = w / d.nwx;
+        const int q = (int)(w - row * d.nwx);
+        const uint32_t *rw = bits + row * d.nwx;
+        const int tail = d.nx - 32 * (d.nwx - 1);  // valid bits in a row's last word (1..32)
+        const uint32_t last_mask = tail >= 32 ? 0xffffffffu : ((1u << tail) - 1u);
+        uint32_t wl = q > 0 ? __ldg(rw + q - 1) : 0u, wc = __ldg(rw + q), wr = q + 1 < d.nwx ? __ldg(rw + q + 1) : 0u;
+        if (q == d.nwx - 1) wc &= last_mask;
+        if (q + 1 == d.nwx - 1) wr &= last_mask;
+        const int64_t ob = row * d.nx + (int64_t)q * 32 - o0;  // offset of this word's voxel 0 in the block range
+        const int nv = q == d.nwx - 1 ? tail : 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = -R; k <= R; ++k) {
+                const int b = j + k;
+                const uint32_t word = b < 0 ? wl : (b >= 32 ? wr : wc);
+                const int sh = b < 0 ? b + 32 : (b >= 32 ? b - 32 : b);
+                if ((word >> sh) & 1u) acc += wt[k + R];
+            }
+            if (j < nv) so[ob + j] = acc;
+        }
+    }
+    __syncthreads();
+    // the block's contiguous output range: up to the voxel after its last word
+    const int64_t wl_last = (w0 + 255 < nw ? w0 + 255 : nw - 1);
+    const int64_t rowl = wl_last / d.nwx;
+    const int ql = (int)(wl_last - rowl * d.nwx);
+    const int64_t o1 = rowl * d.nx + (int64_t)ql * 32 + (ql == d.nwx - 1 ? d.nx - 32 * (d.nwx - 1) : 32);
+    for (int64_t i = threadIdx.x; i < o1 - o0; i += 256) out[o0 + i] = so[i];
+}
+
 // ---- Eq. 14b: Quantile_q(V') by a three-pass radix select over the float bits (V' >= 0, so the
 // bit patterns order like the values): 11 + 11 + 10 bits, per-block shared histograms
 struct QSel {
@@ -854,6 +905,15 @@ void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, 
                 FGL_CUDA(cudaFuncSetAttribute(k_blur_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             k_blur_tile<<<g, dim3(64, 4), smem, s>>>(src, dst[ax], d, ax, t);
             FGL_LAUNCHED("k_blur_tile");
+        } else if (ax == 0 && t.R <= 4 && FGL_BLUR_TILE) {
+            const unsigned nb = (unsigned)((d.nw() + 255) / 256);
+            switch (t.R) {
+                case 1: k_blur_x<1><<<nb, 256, 0, s>>>(occ, dst[ax], d, t); break;
+                case 2: k_blur_x<2><<<nb, 256, 0, s>>>(occ, dst[ax], d, t); break;
+                case 3: k_blur_x<3><<<nb, 256, 0, s>>>(occ, dst[ax], d, t); break;
+                default: k_blur_x<4><<<nb, 256, 0, s>>>(occ, dst[ax], d, t); break;
+            }
+            FGL_LAUNCHED("k_blur_x");
         } else {
             k_blur<<<grid2d(d), dim3(64, 4), 0, s>>>(occ, src, dst[ax], d, ax, t);
             FGL_LAUNCHED("k_blur");

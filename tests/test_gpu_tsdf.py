@@ -51,10 +51,12 @@ def test_tsdf_bit_exact(case):
         assert np.array_equal(phi.view(np.uint32), ref.view(np.uint32)), (case, sp)
 
 
-@pytest.mark.parametrize("sigma_vox", [0.6, 1.5])
-def test_denoise_parity(sigma_vox):
+@pytest.mark.parametrize("sigma_vox,shape", [(0.6, (18, 21, 45)), (0.9, (7, 9, 64)), (1.2, (5, 40, 33)),
+                                             (1.5, (18, 21, 45)), (0.3, (3, 4, 97))])
+def test_denoise_parity(sigma_vox, shape):
+    # R = ceil(3 sigma) = 2, 3, 4 (word-per-thread x pass, full / ragged last words), 5 (gather x pass), 1
     rng = np.random.default_rng(1)
-    V = rng.uniform(size=(18, 21, 45)) < 0.5
+    V = rng.uniform(size=shape) < 0.5
     nz, ny, nx = V.shape
     h = 0.05
     tau = 0.5
