@@ -243,33 +243,30 @@ __global__ void k_qinit(QSel *sel, int64_t n, double q, float *thr_out) {
     (void)thr_out;
 }
 
+// one warp per output word (its 32 voxels read coalesced, the word is the warp's ballot): V~ = V' >= tau
+__device__ __forceinline__ void threshold_words(const float *__restrict__ vp, const Dims &d, float tau,
+                                                uint32_t *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < d.nw(); w += nwarps) {
+        const int64_t row = w / d.nwx;
+        const int x = (int)(w - row * d.nwx) * 32 + lane;
+        const bool on = x < d.nx && __ldg(vp + row * d.nx + x) >= tau;
+        const uint32_t b = __ballot_sync(0xffffffffu, on);  // padding lanes (x >= nx) vote 0
+        if (lane == 0) out[w] = b;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_threshold_q(const float *__restrict__ vp, Dims d, const QSel *sel,
                                                      uint32_t *__restrict__ out, float *thr_out) {
     const float tau = __uint_as_float(sel->prefix);
     if (thr_out && blockIdx.x == 0 && threadIdx.x == 0) *thr_out = tau;
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < d.nw(); w += (int64_t)gridDim.x * blockDim.x) {
-        const int wx = (int)(w % d.nwx);
-        const int64_t row = w / d.nwx;
-        const int x0 = wx * 32;
-        uint32_t b = 0;
-        for (int k = 0; k < 32 && x0 + k < d.nx; ++k)
-            if (vp[row * d.nx + x0 + k] >= tau) b |= 1u << k;
-        out[w] = b;
-    }
+    threshold_words(vp, d, tau, out);
 }
 
-// one thread per output word: V~ = V' >= tau (Eq. 14a), padding bits zero
 __global__ void __launch_bounds__(256) k_threshold(const float *__restrict__ vp, Dims d, float tau,
                                                    uint32_t *__restrict__ out) {
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < d.nw(); w += (int64_t)gridDim.x * blockDim.x) {
-        const int wx = (int)(w % d.nwx);
-        const int64_t row = w / d.nwx;
-        const int x0 = wx * 32;
-        uint32_t b = 0;
-        for (int k = 0; k < 32 && x0 + k < d.nx; ++k)
-            if (vp[row * d.nx + x0 + k] >= tau) b |= 1u << k;
-        out[w] = b;
-    }
+    threshold_words(vp, d, tau, out);
 }
 
 // ---- Eq. 15-17 -------------------------------------------------------------------------------
@@ -395,15 +392,30 @@ __device__ __forceinline__ uint32_t valid_mask(const Dims &d, int64_t w) {
 // S_0 (Eq. 15, the frame free): kappa = 0 there, 255 elsewhere; vis = S_0
 __global__ void __launch_bounds__(256) k_s0(const uint32_t *__restrict__ occ, Dims d, uint32_t *__restrict__ vis,
                                             uint8_t *__restrict__ kappa) {
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < d.nw(); w += (int64_t)gridDim.x * blockDim.x) {
-        const Nb n = neighbours(occ, d, w);
-        const uint32_t s = ((n.c ^ n.xm) | (n.c ^ n.xp) | (n.c ^ n.ym) | (n.c ^ n.yp) | (n.c ^ n.zm) | (n.c ^ n.zp)) &
-                           valid_mask(d, w);
-        vis[w] = s;
-        const int wx = (int)(w % d.nwx);
-        const int64_t base = (w / d.nwx) * d.nx + wx * 32;
-        const int cnt = min(32, d.nx - wx * 32);
-        for (int k = 0; k < cnt; ++k) kappa[base + k] = (s >> k) & 1u ? 0 : 255;
+    // a warp handles 32 consecutive words; the kappa bytes of each word are then written by the 32
+    // lanes together (coalesced) instead of 32 scattered byte stores per thread
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31; w0 < d.nw(); w0 += stride) {
+        const int64_t w = w0 + lane;
+        uint32_t s = 0;
+        int64_t base = 0;
+        int cnt = 0;
+        if (w < d.nw()) {
+            const Nb n = neighbours(occ, d, w);
+            s = ((n.c ^ n.xm) | (n.c ^ n.xp) | (n.c ^ n.ym) | (n.c ^ n.yp) | (n.c ^ n.zm) | (n.c ^ n.zp)) &
+                valid_mask(d, w);
+            vis[w] = s;
+            const int wx = (int)(w % d.nwx);
+            base = (w / d.nwx) * d.nx + wx * 32;
+            cnt = min(32, d.nx - wx * 32);
+        }
+        for (int j = 0; j < 32; ++j) {
+            const uint32_t sj = __shfl_sync(0xffffffffu, s, j);
+            const int64_t bj = __shfl_sync(0xffffffffu, base, j);
+            const int cj = __shfl_sync(0xffffffffu, cnt, j);
+            if (lane < cj) kappa[bj + lane] = (sj >> lane) & 1u ? 0 : 255;
+        }
     }
 }
 
@@ -921,7 +933,7 @@ void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, 
         src = dst[ax];
     }
     if (!quantile) {
-        k_threshold<<<grid1d(d.nw()), 256, 0, s>>>(vp, d, tau, out);
+        k_threshold<<<grid1d(d.nw() * 32), 256, 0, s>>>(vp, d, tau, out);
         FGL_LAUNCHED("k_threshold");
         if (thr_out) FGL_CUDA(cudaMemcpyAsync(thr_out, &tau, sizeof(float), cudaMemcpyHostToDevice, s));
     } else {  // tau is the quantile level q (Eq. 14b)
@@ -937,7 +949,7 @@ void launch_denoise(const uint32_t *occ, const int *dims, const float *spacing, 
             k_qpick<<<1, 256, 0, s>>>(gh, pass_bits[p], sel);
             FGL_LAUNCHED("k_qpick");
         }
-        k_threshold_q<<<grid1d(d.nw()), 256, 0, s>>>(vp, d, sel, out, thr_out);
+        k_threshold_q<<<grid1d(d.nw() * 32), 256, 0, s>>>(vp, d, sel, out, thr_out);
         FGL_LAUNCHED("k_threshold_q");
         sfree(sel, s), sfree(gh, s);
     }
