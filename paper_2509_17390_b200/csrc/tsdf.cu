@@ -320,6 +320,44 @@ __global__ void __launch_bounds__(256) k_cc_init(const uint32_t *__restrict__ oc
     }
 }
 
+// The same labels, one warp per row: the start of the run entering each word is a warp prefix max
+// over the words' highest occupied voxel, and the row's labels are written coalesced (32 voxels of
+// one word per store instruction) instead of one thread per voxel re-scanning the words before it.
+__global__ void __launch_bounds__(256) k_cc_init_rows(const uint32_t *__restrict__ occ, Dims d,
+                                                      int *__restrict__ lab) {
+    constexpr unsigned kFull = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int64_t nrows = (int64_t)d.ny * d.nz;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < nrows; row += nwarps) {
+        const uint32_t *rw = occ + row * d.nwx;
+        int carry = 0;  // (highest occupied voxel before this group of 32 words) + 1, or 0
+        for (int q0 = 0; q0 < d.nwx; q0 += 32) {
+            const int q = q0 + lane;
+            const uint32_t wv = q < d.nwx ? __ldg(rw + q) : 0u;
+            int hi = wv ? (q << 5) + 32 - __clz(wv) : 0;  // highest occupied voxel of word q, + 1
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, hi, o);
+                if (lane >= o) hi = max(hi, y);
+            }
+            int before = __shfl_up_sync(kFull, hi, 1);
+            before = max(lane == 0 ? 0 : before, carry);  // run start for a voxel with nothing below it in its word
+            const int nq = min(32, d.nwx - q0);
+            for (int k = 0; k < nq; ++k) {
+                const uint32_t wk = __shfl_sync(kFull, wv, k);
+                const int bk = __shfl_sync(kFull, before, k);
+                const int x = ((q0 + k) << 5) + lane;
+                if (x < d.nx) {
+                    const uint32_t m = wk & ((1u << lane) - 1u);
+                    const int rs = m ? ((q0 + k) << 5) + 32 - __clz(m) : bk;
+                    lab[row * d.nx + x] = ((wk >> lane) & 1u) ? -1 : (int)(row * d.nx + rs);
+                }
+            }
+            carry = __shfl_sync(kFull, hi, 31);
+        }
+    }
+}
+
 // union the runs of neighbouring rows (y - 1, z - 1) where they begin to overlap: at x = the later
 // of the two run starts, so each overlapping pair of runs is united once
 __global__ void __launch_bounds__(256) k_cc_merge(const uint32_t *__restrict__ occ, Dims d, int *lab) {
@@ -964,7 +1002,10 @@ void launch_tsdf(const uint32_t *occ, const int *dims, const float *spacing, flo
     uint32_t *v0 = salloc<uint32_t>(d.nw(), s), *v1 = salloc<uint32_t>(d.nw(), s);
     FGL_CUDA(cudaMemsetAsync(oroot, 0, d.n(), s));
     const dim3 g2 = grid2d(d);
-    k_cc_init<<<g2, dim3(64, 4), 0, s>>>(occ, d, lab);
+    if (FGL_BLUR_TILE)
+        k_cc_init_rows<<<grid1d((int64_t)d.ny * d.nz * 32), 256, 0, s>>>(occ, d, lab);
+    else
+        k_cc_init<<<g2, dim3(64, 4), 0, s>>>(occ, d, lab);
     FGL_LAUNCHED("k_cc_init");
     k_cc_merge<<<g2, dim3(64, 4), 0, s>>>(occ, d, lab);
     FGL_LAUNCHED("k_cc_merge");

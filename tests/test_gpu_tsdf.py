@@ -38,10 +38,13 @@ def _volumes():
     out.append(rng.uniform(size=(7, 5, 70)) < 0.6)  # noisy, thin in z
     out.append(np.ones((4, 4, 4), bool))  # full grid
     out.append(np.zeros((3, 5, 33), bool))  # empty grid
+    W = rng.uniform(size=(3, 4, 1100)) < 0.97  # long rows: 35 words (> one warp), long free runs
+    W[1, 2, 40:1060] = False
+    out.append(W)
     return out
 
 
-@pytest.mark.parametrize("case", range(6))
+@pytest.mark.parametrize("case", range(7))
 def test_tsdf_bit_exact(case):
     V = _volumes()[case]
     nz, ny, nx = V.shape
