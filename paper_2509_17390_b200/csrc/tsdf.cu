@@ -57,6 +57,15 @@ struct Dims {
     __host__ __device__ int64_t nw() const { return (int64_t)nwx * ny * nz; }
 };
 
+// (x, y, z) of linear voxel index i; nx ny nz <= 2^31 (fgl.h), so 32-bit unsigned divisions suffice
+// (a 64-bit division is a ~70-instruction software routine)
+__device__ __forceinline__ void voxel_xyz(int64_t i, const Dims &d, int &x, int &y, int &z) {
+    const uint32_t u = (uint32_t)i, r = u / (uint32_t)d.nx;
+    x = (int)(u - r * (uint32_t)d.nx);
+    const uint32_t zz = r / (uint32_t)d.ny;
+    y = (int)(r - zz * (uint32_t)d.ny), z = (int)zz;
+}
+
 __device__ __forceinline__ bool bit_at(const uint32_t *__restrict__ v, const Dims &d, int x, int y, int z) {
     return (v[((int64_t)z * d.ny + y) * d.nwx + (x >> 5)] >> (x & 31)) & 1u;
 }
@@ -407,9 +416,9 @@ struct Nb {
     uint32_t c, xm, xp, ym, yp, zm, zp;
 };
 __device__ __forceinline__ Nb neighbours(const uint32_t *__restrict__ v, const Dims &d, int64_t w) {
-    const int wx = (int)(w % d.nwx);
-    const int64_t r = w / d.nwx;
-    const int y = (int)(r % d.ny), z = (int)(r / d.ny);
+    const uint32_t u = (uint32_t)w, r = u / (uint32_t)d.nwx;  // nw <= nx ny nz <= 2^31
+    const int wx = (int)(u - r * (uint32_t)d.nwx);
+    const int z = (int)(r / (uint32_t)d.ny), y = (int)(r - (uint32_t)z * (uint32_t)d.ny);
     Nb n;
     n.c = v[w];
     n.xm = (n.c << 1) | (wx > 0 ? v[w - 1] >> 31 : 0u);
@@ -641,9 +650,8 @@ __global__ void __launch_bounds__(256) k_mc_count(const float *__restrict__ phi,
                                                   uint8_t *__restrict__ eflag, uint32_t *__restrict__ ecnt,
                                                   uint32_t *__restrict__ tcnt, uint32_t *__restrict__ ccnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(i % d.nx);
-        const int64_t r = i / d.nx;
-        const int y = (int)(r % d.ny), z = (int)(r / d.ny);
+        int x, y, z;
+        voxel_xyz(i, d, x, y, z);
         const bool in0 = __ldg(phi + i) < iso;
         uint32_t f = 0;
         if (x + 1 < d.nx && ((__ldg(phi + i + 1) < iso) != in0)) f |= 1u;
@@ -809,9 +817,8 @@ __global__ void __launch_bounds__(256) k_mc_verts(const float *__restrict__ phi,
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t f = eflag[i];
         if (!f) continue;
-        const int x = (int)(i % d.nx);
-        const int64_t r = i / d.nx;
-        const int y = (int)(r % d.ny), z = (int)(r / d.ny);
+        int x, y, z;
+        voxel_xyz(i, d, x, y, z);
         const int64_t stride[3] = {1, d.nx, (int64_t)d.nx * d.ny};
         const int c[3] = {x, y, z}, nn[3] = {d.nx, d.ny, d.nz};
         const float pa = __ldg(phi + i);
@@ -870,9 +877,8 @@ __global__ void __launch_bounds__(256) k_mc_tris(const float *__restrict__ phi, 
                                                  int32_t *__restrict__ tris) {
     const uint32_t ne = (uint32_t)*nedge;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.n(); i += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(i % d.nx);
-        const int64_t r = i / d.nx;
-        const int y = (int)(r % d.ny), z = (int)(r / d.ny);
+        int x, y, z;
+        voxel_xyz(i, d, x, y, z);
         if (x + 1 >= d.nx || y + 1 >= d.ny || z + 1 >= d.nz) continue;
         const int cs = cube_case(phi, d, i, a.iso);
         const int nt = c_mc.ntri[cs];
