@@ -684,9 +684,10 @@ struct RosetteGen {
     static constexpr bool kCoherent = true;
     RosetteParams rp;
     const float *poses;
-    int ntile;  // tiles per pose
+    int ntile;      // tiles per pose
+    FastDiv ntile_d;  // the same, as a multiply-shift divisor (tile < 2^31, checked at launch)
     __device__ __forceinline__ bool ray(int64_t tile, int lane, Ray &r, int64_t &idx, float &tmin, float &tmax) const {
-        const int64_t p = tile / ntile;
+        const int64_t p = fdiv((uint32_t)tile, ntile_d);
         const int k = (int)(tile - p * ntile) * 32 + lane;
         tmin = rp.t_min, tmax = rp.t_max;
         if (k >= rp.n) return false;
@@ -700,7 +701,7 @@ struct RosetteGen {
         return ray(tile, lane, r, idx, a, b);
     }
     __device__ __forceinline__ int64_t index(int64_t tile, int lane) const {
-        const int64_t p = tile / ntile;
+        const int64_t p = fdiv((uint32_t)tile, ntile_d);
         return p * rp.n + (int)(tile - p * ntile) * 32 + lane;
     }
     __device__ __forceinline__ float interval_min() const { return rp.t_min; }
@@ -1143,6 +1144,8 @@ void launch_cast_rosette(const SceneView &sv, const RosetteParams &p, const floa
     g.rp = p;
     g.poses = poses;
     g.ntile = (p.n + 31) / 32;
+    g.ntile_d = make_fastdiv((uint32_t)g.ntile);
+    if (P * (int64_t)g.ntile >= (int64_t(1) << 31)) throw Error(1, "rosette cast: more than 2^31 ray tiles in one call");
     launch_persistent(sv, g, P * (int64_t)g.ntile, o, ctr, s);
 }
 
