@@ -163,7 +163,11 @@ OPS_TRI = 60
 
 
 def _alu_peak_tops():
-    """FP32 lane throughput: 148 SMs x 4 SMSPs x 32 lanes x max SM clock (B200_PROFILING.md)."""
+    """Issue ceiling in lane operations: 148 SMs x 4 SMSPs x 32 lanes x max SM clock (unit counts and
+    clock: B200_PROFILING.md). Each SMSP issues one warp instruction per cycle; the FMA pipe (FFMA,
+    FMUL) and the ALU pipe (FMNMX, FSETP, LOP3, PRMT) each accept one every second cycle
+    (B300_MICROARCH.md), so the two together sustain the issue rate and an FP32 min/max costs the
+    same issue slot as an FFMA: for an issue-bound kernel this one number is the ALU roofline."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             mhz = float(json.load(f).get("sm_max_mhz", 1965.0))
@@ -226,20 +230,47 @@ def _frame_latency(scene, pose1, pat, out, torch, stream, n):
             "note": "one pose per CUDA-graph replay (cast only, prebuilt scene), per-replay CUDA events"}
 
 
-def _ncu_traffic(config: str, kernel: str = "k_cast"):
-    """dram read+write bytes per launch of the dominant kernel from the committed ncu summary."""
+def _ncu_summary(config: str, kernel: str = "k_cast") -> dict:
+    """The committed ncu summary of the dominant kernel for this config (profiles/ncu_summary.json)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            s = json.load(f)
-        return s[config][kernel]["dram_bytes_per_launch"]
+            return json.load(f)[config][kernel]
     except Exception:
-        return None
+        return {}
+
+
+def _ncu_traffic(config: str, kernel: str = "k_cast"):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu summary."""
+    return _ncu_summary(config, kernel).get("dram_bytes_per_launch")
 
 
 # ----------------------------------------------------------------------------------------------
-def _cpu_baseline(cfg, seconds: float):
+def _host_cpu():
+    """CPU model, physical cores and hardware threads of this host (SURVEY 8(d) timing protocol)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False)
+    except Exception:
+        phys = None
+    return {"model": model, "physical_cores": phys, "threads": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None}
+
+
+def _cpu_baseline(cfg, seconds: float, gpu_range=None, gpu_tri=None, parity_rays: int = 2048):
     """The oracle (CPU double brute force, Eq. 20 by the naive scan P:291-294), as it stands, on a
-    bounded seeded sample of the workload's rays, on this host's cores."""
+    bounded seeded sample of the workload's rays, on this host's cores; plus its 1-thread rate on a
+    1/64 subset of that sample, and — when the GPU's results for pose 0 are given — the parity of
+    this bench run: the oracle classifies `parity_rays` of the sampled rays (mode A: its own double
+    rays) and judges the GPU's range / tri_id on them."""
     import oracle
     m, pat = cfg["mesh"], cfg["pattern"]
     o, d = oracle.pattern_rays(pat, cfg["poses_rank"][:1])
@@ -254,9 +285,32 @@ def _cpu_baseline(cfg, seconds: float):
     t0 = time.perf_counter()
     oracle.cast(m.verts, m.tris, o[idx], d[idx], pat.t_min, pat.t_max)
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
-            "sample": f"{n} seeded rays of pose 0 of {cfg['name']} vs all {m.T} triangles "
-                      f"({n * m.T:.3g} double MT tests, {dt:.1f} s)"}
+    threads = oracle.threads()
+    # 1-thread rate on a 1/64 subset (per-core speed; the multi-thread rate / cores shows the scaling)
+    sub = idx[: max(1, n // 64)]
+    oracle.set_threads(1)
+    try:
+        t1 = time.perf_counter()
+        oracle.cast(m.verts, m.tris, o[sub], d[sub], pat.t_min, pat.t_max)
+        dt1 = time.perf_counter() - t1
+    finally:
+        oracle.set_threads(threads)
+    out = {"value": n / dt, "unit": "rays/s", "cores": threads, "kind": "oracle",
+           "sample": f"{n} seeded rays of pose 0 of {cfg['name']} vs all {m.T} triangles "
+                     f"({n * m.T:.3g} double MT tests, {dt:.1f} s)",
+           "one_thread_rays_per_s": len(sub) / dt1, "one_thread_sample": f"{len(sub)} rays (1/64 of the sample)",
+           "host": _host_cpu()}
+    parity = None
+    if gpu_range is not None:
+        pidx = np.sort(idx[:parity_rays])
+        v = oracle.cast_and_classify(m.verts, m.tris, o[pidx], d[pidx], pat.t_min, pat.t_max,
+                                     eps_rel=oracle.EPS_MODE_A)
+        j = oracle.judge(v, gpu_range[pidx], gpu_tri[pidx])
+        parity = {"rays": int(j["n"]), "mode": "A (oracle's own double rays vs the bench's cast of pose 0)",
+                  "ambiguous": int(j["ambiguous"]), "unambiguous_mismatch": int(len(j["unamb_mismatch"])),
+                  "ambiguous_outside": int(len(j["amb_outside"])),
+                  "tolerance": "unambiguous rays: tri_id exact, |range - t*| <= 1e-4 t* + 1e-5 m (DESIGN.md §4)"}
+    return out, parity
 
 
 def run_reference(a):
@@ -839,12 +893,17 @@ def main():
     cres = scene.cast(poses_d, pat, counts=True)
     n_nodes = cres["node_counts"].double().mean().item()
     n_tris = cres["tri_counts"].double().mean().item()
-    bytes_per_ray = 64.0 * n_nodes + 48.0 * n_tris + 8.0
+    node_bytes = 96.0 if a.width == 8 else (128.0 if a.width == 4 and not a.quantized else 64.0)
+    bytes_per_ray = node_bytes * n_nodes + 48.0 * n_tris + 8.0
     hbm_peak, peak_kind = _peaks()
-    ops_per_ray = OPS_NODE * n_nodes + OPS_TRI * n_tris
+    # a visit tests every child box of the node: 2 (width 2), 4 (width 4), or 8 quantised boxes whose
+    # 6 planes are decoded first (width 8: 6 decodes + 19 per box)
+    ops_node = {8: 8 * 25, 4: 4 * (19 + (6 if a.quantized else 0))}.get(a.width, OPS_NODE)
+    ops_per_ray = ops_node * n_nodes + OPS_TRI * n_tris
     alu_peak = _alu_peak_tops()
     achieved = ops_per_ray * rays_rank / (cms / 1000) / 1e12
-    traffic = _ncu_traffic(a.config)
+    ncu = _ncu_summary(a.config)
+    traffic = ncu.get("dram_bytes_per_launch")
 
     # --- single-frame latency: one pose cast per CUDA-graph replay ------------------
     latency = None
@@ -918,8 +977,14 @@ def main():
         del scs
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        cpu = _cpu_baseline(cfg, a.cpu_seconds)
+        # the bench's own results for pose 0 (the step's last cast) are judged by the oracle
+        scene.cast(poses_d[:1], pat, out=dict(range=out["range"][:1], tri_id=out["tri_id"][:1]))
+        torch.cuda.synchronize()
+        g_rng = out["range"][0].reshape(-1).cpu().numpy()
+        g_tid = out["tri_id"][0].reshape(-1).cpu().numpy()
+        cpu, parity = _cpu_baseline(cfg, a.cpu_seconds, g_rng, g_tid)
 
     l2_gbs, l2_bytes = (None, None)
     if rank == 0:
@@ -946,21 +1011,27 @@ def main():
             "nodes_per_ray": n_nodes, "tris_per_ray": n_tris,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                          "frac": achieved / alu_peak, "traffic": traffic, "kernel": "k_cast",
-                         "note": f"issue-bound traversal (ncu: ~77% issue-slot use, 40 warps/SM, DRAM nearly idle, L1/L2 hit ~72/85%): "
-                                 f"algorithmic FP32 ops/ray = {OPS_NODE}*nodes + {OPS_TRI}*tris = {ops_per_ray:.0f} "
-                                 f"(DESIGN.md §6); peak = 148 SM x 128 FP32 lanes x 1.965 GHz (unit counts + max "
-                                 f"clock); t_cast from CUDA events on the launch stream; traffic = ncu DRAM bytes "
-                                 f"per launch (profiles/ncu_summary.json)"},
+                         "issue_slot_frac": ncu.get("issue_slot_frac"),
+                         "thread_inst_per_ray": ncu.get("thread_inst_per_ray"),
+                         "warp_inst_per_ray_x32": ncu.get("lane_slots_per_ray"),
+                         "simt_lanes": ncu.get("simt_lanes"), "ncu_source": ncu.get("source"),
+                         "note": f"issue-bound traversal: achieved = algorithmic FP32 ops/ray ({ops_node}*nodes + "
+                                 f"{OPS_TRI}*tris = {ops_per_ray:.0f}, DESIGN.md §6) x rays / t_cast (CUDA events on "
+                                 f"the launch stream); peak = the issue ceiling, 148 SM x 4 SMSP x 32 lanes x max "
+                                 f"clock (one lane op per issue slot); issue_slot_frac / thread_inst_per_ray / "
+                                 f"simt_lanes / traffic (DRAM bytes per launch) from the committed ncu capture of "
+                                 f"this kernel (profiles/ncu_summary.json): the slots the algorithm does not use go "
+                                 f"to control flow, the stack, ray setup and idle lanes"},
             "memory": {"algorithmic_bytes_per_ray": bytes_per_ray,
                        "achieved_gbs": bytes_per_ray * rays_rank / (cms / 1000) / 1e9,
                        "hbm_peak_gbs": hbm_peak, "hbm_peak_kind": peak_kind,
                        "l2_read_gbs": l2_gbs, "l2_bytes": l2_bytes, "l2_kind": "measured in this run (fgl_l2_read_probe)",
-                       "frac_of_l2": bytes_per_ray * rays_rank / (cms / 1000) / 1e9 / l2_gbs if l2_gbs else None,
-                       "note": "node (64 B) + triangle (48 B) fetches + 8 B output per ray, mostly L1/L2-served; "
-                               "frac_of_l2 = algorithmic bytes/s over the measured L2 read bandwidth (the scene's "
-                               "node + triangle working set fits in L2 for C2/C4; L1 hits serve part of it)"},
+                       "note": "node + triangle fetches + 8 B output per ray; served mostly by L1 (node sectors "
+                               "~70% L1 hits) and L2, DRAM nearly idle (roofline.traffic), so neither the HBM nor "
+                               "the L2 bandwidth bounds this kernel (context only)"},
             "frame_latency": latency,
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,

@@ -59,8 +59,15 @@ typedef struct {
     int32_t morton_box;  /* 0 = cubic scene box (default): every axis uses L = max_a L_a, the box
                             [o, o+L] read as a cube (isotropic cells; reading R22);
                             1 = per-axis box, L_x, L_y, L_z separately                         */
-    int32_t width;       /* traversal node width: 2 (binary "node64", default) or 4 ("node128")    */
-    int32_t quantized;   /* width 4 only: 1 = 8-bit child boxes, outward-rounded ("node64q")      */
+    int32_t width;       /* traversal node width: 2 (binary "node64", default), 4 ("node128") or 8
+                            ("node96q": the Karras tree collapsed by the SAH dynamic program of
+                            Ylitie et al. 2017 into 8-wide nodes with 8-bit outward-rounded child
+                            boxes and octant-ordered slots, leaves of <= 3 triangles; SURVEY A7 /
+                            NEXT-4). Width 8 needs a scene extent below 2^120; a tree
+                            deeper than the cast's traversal stack makes casts a no-op and
+                            fgl_scene_check report FGL_E_DATA                                   */
+    int32_t quantized;   /* width 4: 1 = 8-bit child boxes, outward-rounded ("node64q"); width 8
+                            is always 8-bit (0 or 1 accepted)                                  */
     int32_t restructure; /* width 2 only: 0 = plain LBVH (default); k = 1..8 passes of agglomerative
                             treelet restructuring: SAH-guided re-clustering of
                             7-leaf treelets bottom-up, 1-triangle leaves (leaf_size ignored)     */

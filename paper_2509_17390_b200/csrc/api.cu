@@ -86,7 +86,7 @@ void free_build(fgl_scene *s) {
     fgl::BuildBuffers &b = s->b;
     void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.sort_status, b.sort_tiles,
                   b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth, b.agg,
-                  b.cost, b.tsize};
+                  b.cost, b.tsize, b.cost8, b.wq, b.wctr};
     for (void *p : ps)
         if (p) cudaFree(p);
     b = fgl::BuildBuffers();
@@ -110,7 +110,8 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.ghist, 8 * 256);
     dalloc(s, &b.sort_status, (size_t)256 * fgl::sort_tile_blocks(T));
     FGL_CUDA(cudaMemset(b.sort_status, 0, sizeof(uint64_t) * 256 * fgl::sort_tile_blocks(T)));
-    dalloc(s, &b.sort_tiles, 8);
+    dalloc(s, &b.sort_tiles, 16);
+    FGL_CUDA(cudaMemset(b.sort_tiles, 0, 16 * sizeof(uint32_t)));  // tile counters + device sort epoch
     dalloc(s, &b.tri, 3 * T);
     dalloc(s, &b.child, nin);
     dalloc(s, &b.range, nin);
@@ -128,10 +129,13 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.depth, nin);
     dalloc(s, &b.cost, nin);
     dalloc(s, &b.tsize, nin);
+    dalloc(s, &b.cost8, 8 * nin);
+    dalloc(s, &b.wq, T);
+    dalloc(s, &b.wctr, 4);
 }
 
 fgl::SceneView view(const fgl_scene *s) {
-    return fgl::SceneView{s->b.tri, s->b.nodes, s->b.nodes4, s->b.width, s->b.quantized};
+    return fgl::SceneView{s->b.tri, s->b.nodes, s->b.nodes4, s->b.width, s->b.quantized, s->b.wctr + 3, s->vflag};
 }
 
 fgl::CastCounter *next_counter(const fgl_scene *s) {
@@ -523,6 +527,8 @@ fgl_status fgl_scene_check(fgl_scene *s, void *stream) {
     FGL_CUDA(cudaStreamSynchronize(st));
     if (*s->hflag & 1u) throw Error(FGL_E_DATA, "triangle index out of range [0, V)");
     if (*s->hflag & 2u) throw Error(FGL_E_DATA, "non-finite vertex coordinate");
+    if (*s->hflag & 4u)
+        throw Error(FGL_E_DATA, "width-8 tree needs a deeper traversal stack than the cast has; casts were refused");
     FGL_API_END
 }
 
@@ -538,7 +544,7 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
         if (opts->quantized < 0 || opts->quantized > 1) throw Error(FGL_E_USAGE, "quantized must be 0 or 1");
         quant = opts->quantized;
         if (opts->width) width = opts->width;
-        if (width != 2 && width != 4) throw Error(FGL_E_USAGE, "width must be 2 or 4");
+        if (width != 2 && width != 4 && width != 8) throw Error(FGL_E_USAGE, "width must be 2, 4 or 8");
         if (opts->morton_box < 0 || opts->morton_box > 1) throw Error(FGL_E_USAGE, "morton_box must be 0 or 1");
         cubic = opts->morton_box == 0;
         for (int i = 0; i < 2; ++i)
@@ -557,7 +563,8 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     FGL_CUDA(cudaStreamIsCapturing(st, &cap));
     const bool timed = cap == cudaStreamCaptureStatusNone;  // build_ms is not recorded inside a graph
     if (timed) FGL_CUDA(cudaEventRecord(s->ev0, st));
-    if (quant && width != 4) throw Error(FGL_E_USAGE, "quantized nodes need width 4");
+    if (quant && width == 2) throw Error(FGL_E_USAGE, "quantized nodes need width 4 or 8");
+    if (width == 8) quant = 1;  // the 8-wide node is always the compressed node96q
     if (s->gauss) {
         if (width != 2 || quant) throw Error(FGL_E_USAGE, "a Gaussian scene builds width-2 nodes only");
         if (!cubic) throw Error(FGL_E_USAGE, "a Gaussian scene uses the cubic Morton box");
@@ -885,11 +892,11 @@ fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key
     const size_t nstat = (size_t)256 * fgl::sort_tile_blocks(n);
     FGL_CUDA(cudaMallocAsync((void **)&status, nstat * sizeof(uint64_t), st));
     FGL_CUDA(cudaMemsetAsync(status, 0, nstat * sizeof(uint64_t), st));
-    FGL_CUDA(cudaMallocAsync((void **)&tiles, 8 * sizeof(uint32_t), st));
+    FGL_CUDA(cudaMallocAsync((void **)&tiles, 16 * sizeof(uint32_t), st));
+    FGL_CUDA(cudaMemsetAsync(tiles, 0, 16 * sizeof(uint32_t), st));
     FGL_CUDA(cudaMallocAsync((void **)&ghist, 8 * 256 * sizeof(uint32_t), st));
     int slot = 0;
-    uint32_t epoch = 0;
-    fgl::radix_sort_pairs(keys, vals, k1, v1, n, key_bits, status, tiles, ghist, false, &epoch, &slot, st);
+    fgl::radix_sort_pairs(keys, vals, k1, v1, n, key_bits, status, tiles, ghist, false, &slot, st);
     if (slot == 1) {
         FGL_CUDA(cudaMemcpyAsync(keys, k1, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
         FGL_CUDA(cudaMemcpyAsync(vals, v1, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));

@@ -733,7 +733,7 @@ void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s) {
     FGL_LAUNCHED("k_morton");
     int slot = 0;
     radix_sort_pairs(b.keys[0], ps ? nullptr : b.vals[0], b.keys[1], ps ? nullptr : b.vals[1], T, key_bits,
-                     b.sort_status, b.sort_tiles, b.ghist, true, &b.sort_epoch, &slot, s, ps);
+                     b.sort_status, b.sort_tiles, b.ghist, true, &slot, s, ps);
     b.sorted_slot = slot;
 }
 
@@ -785,16 +785,23 @@ static void launch_single(BuildBuffers &b, int width, cudaStream_t s) {
 void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s, int restructure) {
     const int64_t T = b.T;
     b.width = width;
-    b.quantized = width == 4 ? quantized : 0;
+    b.quantized = width == 4 ? quantized : (width == 8 ? 1 : 0);
     b.restructured = 0;
     AggLevels L = launch_aggregates(b, s);
     if (T == 1) {
-        launch_single(b, width, s);
+        if (width == 8)
+            launch_wide8(b, s);
+        else
+            launch_single(b, width, s);
         return;
     }
     k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[b.sorted_slot], (int)T, b.packed_shift, b.child,
                                                             b.range, b.parent, L, b.nodebox);
     FGL_LAUNCHED("k_karras");
+    if (width == 8) {  // SAH collapse of the Karras tree (single-triangle leaves) to node96q
+        launch_wide8(b, s);
+        return;
+    }
     if (restructure > 0 && width == 2) {
         // costs / sizes bottom-up once, then `restructure` treelet passes; nodes over 1-triangle leaves
         for (int pass = 0; pass <= restructure; ++pass) {
@@ -823,7 +830,10 @@ void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
     FGL_LAUNCHED("k_reorder");
     AggLevels L = launch_aggregates(b, s);
     if (T == 1) {
-        launch_single(b, b.width, s);
+        if (b.width == 8)
+            launch_wide8(b, s);
+        else
+            launch_single(b, b.width, s);
         return;
     }
     if (b.restructured) {  // free topology: boxes bottom-up over the kept child links
@@ -838,6 +848,10 @@ void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
     }
     k_refit_boxes<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>((int)T, b.range, L, b.nodebox);
     FGL_LAUNCHED("k_refit_boxes");
+    if (b.width == 8) {  // the binary topology is kept; the SAH collapse is redone over the new boxes
+        launch_wide8(b, s);
+        return;
+    }
     launch_nodes(b, leaf_size, b.width, true, s);
 }
 

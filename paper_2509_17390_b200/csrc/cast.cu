@@ -14,6 +14,7 @@
 #include <climits>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "fgl_internal.cuh"
 
@@ -26,6 +27,10 @@ namespace {
 #endif
 #ifndef FGL_APPROX_NORM
 #define FGL_APPROX_NORM 0  // MUFU rsqrt for the direction normalisation (off: exact sqrt + division)
+#endif
+
+#ifndef FGL_LEAF_RCP
+#define FGL_LEAF_RCP 1  // leaf test: t = T * rcp(det) instead of the IEEE division (R15)
 #endif
 
 #ifndef FGL_CAST_THREADS
@@ -140,10 +145,18 @@ __device__ __forceinline__ bool hit_tri(const Pre &p, float4 a, float4 b, float4
     const float det = U + V + W;
     if (det == 0.f) return false;
     const float T = U * A.z + V * B.z + W * C.z;
+#if FGL_LEAF_RCP
+    // t = T / det by the MUFU reciprocal (<= 1 ulp) and one rounding: within 2 ulp of the correctly
+    // rounded quotient (R15), deterministic, and the same in every kernel that calls hit_tri; a
+    // |det| below 2^-100 (where rcp.approx.ftz would flush) takes the IEEE division
+    float t = T * rcp_approx(det);
+    if (fabsf(det) < 0x1p-100f) t = __fdiv_rn(T, det);
+#else
     // cheap conservative reject before the division: t = T/det outside [tmin, best_t] by > 2^-20
     const float ad = fabsf(det), Ts = det < 0.f ? -T : T;
     if (Ts > best_t * ad * (1.f + 0x1p-20f) || Ts < tmin * ad * (1.f - 0x1p-20f)) return false;
     const float t = __fdiv_rn(T, det);
+#endif
     if (!(t >= tmin && t <= best_t)) return false;
     if (t == best_t && id >= best_id) return false;
     t_out = t;
@@ -555,8 +568,11 @@ __device__ __forceinline__ void write_out(const CastOut &o, int64_t idx, const R
 // slot; with a fused all-gather it also signals every rank (own flag included) after a system-scope
 // fence by every warp, so a rank waiting for W signals knows all peers' stores into its buffer landed.
 __device__ __forceinline__ void cast_epilogue(const CastOut &out, CastCounter *ctr, int lane) {
+    // every lane fences its own peer stores at system scope (a fence orders only the calling thread's
+    // accesses), then the warp reconverges before lane 0 counts the warp as done
+    if (out.nsignal) __threadfence_system();
+    __syncwarp();
     if (lane == 0) {
-        if (out.nsignal) __threadfence_system();
         const unsigned int total = gridDim.x * (blockDim.x >> 5);
         if (atomicAdd(&ctr->done, 1u) == total - 1) {
             ctr->next = 0ull;
@@ -743,7 +759,7 @@ struct RaysGen {
 #ifndef FGL_DYN_MINBLOCKS
 #define FGL_DYN_MINBLOCKS 10  // k_cast_dyn: 10 CTAs x 4 warps per SM (48 registers; measured best)
 #endif
-enum TraversalMode { kRay2 = 0, kPacket2 = 1, kRay4 = 2, kRay4Q = 3 };
+enum TraversalMode { kRay2 = 0, kPacket2 = 1, kRay4 = 2, kRay4Q = 3, kRay8Q = 4 };
 
 template <class Gen, bool kCount, int kMode>
 __global__ void __launch_bounds__(kCastThreads, FGL_CAST_MINBLOCKS)
@@ -816,11 +832,49 @@ __device__ __forceinline__ void ldg_node(const Node64 *__restrict__ n, float4 &a
 #endif
 }
 
+#ifndef FGL_SSTACK
+#define FGL_SSTACK 0  // traversal-stack entries per lane held in shared memory (0: all in local memory)
+#endif
+constexpr int kSStack = FGL_SSTACK;
+// Per-lane traversal stack of (entry t bits << 32 | node ref) words. The first kSStack entries live
+// in shared memory, one column per thread (entry i of thread x at [i][x]: lanes at different depths
+// still hit distinct banks), deeper entries in local memory. A local-memory stack costs one 32-B L1
+// sector per lane and access when the lanes' depths differ (1.9 useful bytes per sector measured)
+// and its lines crowd the nodes and triangles out of L1; the shared part avoids both.
+template <int kCap>
+struct LaneStackN {
+    uint64_t *sh;                                    // &s_stack[0][threadIdx.x]
+    uint64_t loc[kCap - kSStack > 0 ? kCap - kSStack : 1];
+    __device__ __forceinline__ void push(int &sp, uint64_t e) {
+        if (kSStack > 0 && sp < kSStack)
+            sh[sp * kCastThreads] = e;
+        else
+            loc[sp - kSStack] = e;
+        ++sp;
+    }
+    __device__ __forceinline__ uint64_t at(int i) const {
+        return (kSStack > 0 && i < kSStack) ? sh[i * kCastThreads] : loc[i - kSStack];
+    }
+};
+
+#ifndef FGL_PREFETCH
+#define FGL_PREFETCH 0  // 1: L1-prefetch the children nodes at each visit; 2: also the leaves' first triangle
+#endif
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+using LaneStack = LaneStackN<kStack>;
+// width 8: every hit child is pushed; the build bounds the depth this needs (k_collapse) and the
+// cast refuses a tree that would exceed it (fgl_scene_check reports it)
+constexpr int kStack8 = 192;
+using LaneStack8 = LaneStackN<kStack8>;
+
 // Pop the nearest stacked subtree that can still hold a hit (entry t <= t* (1 + 2^-20)).
-__device__ __forceinline__ int32_t pop_live(const uint64_t *st, int &sp, float tlim) {
+template <class Stack>
+__device__ __forceinline__ int32_t pop_live(const Stack &st, int &sp, float tlim) {
     while (sp > 0) {
         --sp;
-        if (__uint_as_float((uint32_t)(st[sp] >> 32)) <= tlim) return (int32_t)(uint32_t)st[sp];
+        const uint64_t e = st.at(sp);
+        if (__uint_as_float((uint32_t)(e >> 32)) <= tlim) return (int32_t)(uint32_t)e;
     }
     return kDone;
 }
@@ -830,8 +884,9 @@ __device__ __forceinline__ int32_t pop_live(const uint64_t *st, int &sp, float t
 // postpones it and keeps descending until every active lane of the warp holds a leaf. OCT >= 0:
 // all active lanes travel in ray octant OCT (slab_oct); OCT = -1: mixed octants (slab_hit).
 template <int OCT, bool kCount>
-__device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const Pre &p, float tmin, bool active,
-                                        Hit &h, float tlim, uint64_t *st, int &sp, int32_t &cur,
+__device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const float4 *__restrict__ tri, const Pre &p,
+                                        float tmin, bool active,
+                                        Hit &h, float tlim, LaneStack &st, int &sp, int32_t &cur,
                                         int32_t &leaf) {
     while (true) {
         bool go = false;
@@ -842,6 +897,17 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
             float4 na, nb, nc, ndf;
             ldg_node(nodes + cur, na, nb, nc, ndf);
             const int4 nd = make_int4(__float_as_int(ndf.x), __float_as_int(ndf.y), 0, 0);
+#if FGL_PREFETCH
+            // L1 prefetch of both children as soon as their refs are known: the box test below
+            // (~25 issue slots of this warp, interleaved with the SM's other warps) covers most of an
+            // L2 round trip, so the next visit's node load usually hits L1
+            if (nd.x >= 0) prefetch_l1(nodes + nd.x);
+            if (nd.y >= 0) prefetch_l1(nodes + nd.y);
+#if FGL_PREFETCH > 1
+            if (nd.x < 0 && nd.x != kEmptyRef) prefetch_l1(tri + 3 * (int64_t)((~nd.x) >> kLeafShift));
+            if (nd.y < 0 && nd.y != kEmptyRef) prefetch_l1(tri + 3 * (int64_t)((~nd.y) >> kLeafShift));
+#endif
+#endif
             if (kCount) ++h.nodes;
             const float lim = h.t;
             float t0, t1;
@@ -849,7 +915,7 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
             const bool h1 = slab_sel<OCT>(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim, t1);
             if (h0 && h1) {
                 const bool swap = t1 < t0;
-                st[sp++] = ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y);
+                st.push(sp, ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y));
                 cur = swap ? nd.y : nd.x;
             } else if (h0) {
                 cur = nd.x;
@@ -871,9 +937,9 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
 // The leaf phase of one while-while iteration: every lane holding a postponed leaf tests its
 // triangles (watertight test, (t, id) lexicographic minimum), then takes the next postponed leaf if
 // its descent ended on one.
-template <bool kCount>
+template <bool kCount, class Stack>
 __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre &p, float tmin, bool active, Hit &h,
-                                       float &tlim, uint64_t *st, int &sp, int32_t &cur, int32_t &leaf) {
+                                       float &tlim, Stack &st, int &sp, int32_t &cur, int32_t &leaf) {
     if (!active) return;
     while (leaf < 0) {
         const int32_t v = ~leaf;
@@ -898,6 +964,104 @@ __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre
     }
 }
 
+// 8-bit plane byte j of word w as v = 1 + q 2^-15, exactly: one PRMT places q in bits 8..15 of the
+// mantissa of 1.0f (no integer-to-float conversion, which runs on a quarter-rate pipe)
+__device__ __forceinline__ float qv(uint32_t w, int j) {
+    return __uint_as_float(__byte_perm(w, 0x3F800000u, 0x7604u | ((uint32_t)j << 4)));
+}
+
+// Per-axis constants of a node96q visit. Plane q of the axis is at p + q 2^e, so its ray parameter
+// is t = v A + B with v = 1 + q 2^-15, A = I 2^(e+15) (exact: a power-of-two scaling of I) and
+// B = fma(p, I, c) - A. The two extra roundings (fma, subtraction) and the final fma's are each
+// <= 2^-24 of |B| + |A| + |t| <= 2 (|B| + 2 |A|), and I's own error adds <= 2^-23 |t|: the near
+// plane's B is pushed down and the far plane's up by s = (|B| + 2 |A|) 2^-20, which bounds all of
+// them, so the decoded box test stays conservative, like the fp32 slab test.
+__device__ __forceinline__ void axis8(float pa, float I, float c_near, float c_far, uint32_t E, float &A, float &Bn,
+                                      float &Bf) {
+    A = I * __uint_as_float(E << 23);
+    const float bn = fmaf(pa, I, c_near) - A, bf = fmaf(pa, I, c_far) - A;
+    const float sl = fmaf(fabsf(A), 2.f, fabsf(bn)) * 0x1p-20f;
+    Bn = bn - sl;
+    Bf = bf + sl;
+}
+
+// The descent phase over node96q (width 8): a visit fetches the node in three 256-bit loads, tests
+// the eight 8-bit child boxes and pushes every hit child with its entry distance in reverse visiting
+// order (Ylitie et al.'s octant order: slot k ^ X(OCT), X with x and y most significant), then pops
+// the first one — so the nearest-ordered child is visited next and the rest are culled by t* on pop
+// exactly as in the binary traversal. OCT = -1: mixed octants (planes chosen per lane, slot order).
+template <int OCT, bool kCount>
+__device__ __forceinline__ void descend8(const Node8 *__restrict__ nodes8, const Pre &p, float tmin, bool active,
+                                         Hit &h, float tlim, LaneStack8 &st, int &sp, int32_t &cur, int32_t &leaf) {
+    while (true) {
+        bool go = active && cur >= 0 && cur != kDone;
+        if (go) {
+            const float *q = reinterpret_cast<const float *>(nodes8 + cur);
+            float4 c0a, c0bf, c1af, c1bf, r0f, r1f;
+            asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=f"(c0a.x), "=f"(c0a.y), "=f"(c0a.z), "=f"(c0a.w), "=f"(c0bf.x), "=f"(c0bf.y), "=f"(c0bf.z),
+                  "=f"(c0bf.w)
+                : "l"(q));
+            asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=f"(c1af.x), "=f"(c1af.y), "=f"(c1af.z), "=f"(c1af.w), "=f"(c1bf.x), "=f"(c1bf.y), "=f"(c1bf.z),
+                  "=f"(c1bf.w)
+                : "l"(q + 8));
+            asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                : "=f"(r0f.x), "=f"(r0f.y), "=f"(r0f.z), "=f"(r0f.w), "=f"(r1f.x), "=f"(r1f.y), "=f"(r1f.z),
+                  "=f"(r1f.w)
+                : "l"(q + 16));
+            if (kCount) ++h.nodes;
+            const uint32_t meta = __float_as_uint(c0a.w);
+            const bool nx = OCT >= 0 ? (OCT & 1) != 0 : p.Ix < 0.f;
+            const bool ny = OCT >= 0 ? (OCT & 2) != 0 : p.Iy < 0.f;
+            const bool nz = OCT >= 0 ? (OCT & 4) != 0 : p.Iz < 0.f;
+            float Ax, Bnx, Bfx, Ay, Bny, Bfy, Az, Bnz, Bfz;
+            axis8(c0a.x, p.Ix, nx ? p.chx : p.clx, nx ? p.clx : p.chx, meta & 0xFFu, Ax, Bnx, Bfx);
+            axis8(c0a.y, p.Iy, ny ? p.chy : p.cly, ny ? p.cly : p.chy, (meta >> 8) & 0xFFu, Ay, Bny, Bfy);
+            axis8(c0a.z, p.Iz, nz ? p.chz : p.clz, nz ? p.clz : p.chz, (meta >> 16) & 0xFFu, Az, Bnz, Bfz);
+            // plane words (lo / hi bytes of children 0-3 and 4-7); the near plane is lo iff I >= 0
+            const uint32_t lx0 = __float_as_uint(c0bf.x), lx1 = __float_as_uint(c0bf.y);
+            const uint32_t hx0 = __float_as_uint(c0bf.z), hx1 = __float_as_uint(c0bf.w);
+            const uint32_t ly0 = __float_as_uint(c1af.x), ly1 = __float_as_uint(c1af.y);
+            const uint32_t hy0 = __float_as_uint(c1af.z), hy1 = __float_as_uint(c1af.w);
+            const uint32_t lz0 = __float_as_uint(c1bf.x), lz1 = __float_as_uint(c1bf.y);
+            const uint32_t hz0 = __float_as_uint(c1bf.z), hz1 = __float_as_uint(c1bf.w);
+            const uint32_t nwx[2] = {nx ? hx0 : lx0, nx ? hx1 : lx1}, fwx[2] = {nx ? lx0 : hx0, nx ? lx1 : hx1};
+            const uint32_t nwy[2] = {ny ? hy0 : ly0, ny ? hy1 : ly1}, fwy[2] = {ny ? ly0 : hy0, ny ? ly1 : hy1};
+            const uint32_t nwz[2] = {nz ? hz0 : lz0, nz ? hz1 : lz1}, fwz[2] = {nz ? lz0 : hz0, nz ? lz1 : hz1};
+            const int32_t ref[8] = {__float_as_int(r0f.x), __float_as_int(r0f.y), __float_as_int(r0f.z),
+                                    __float_as_int(r0f.w), __float_as_int(r1f.x), __float_as_int(r1f.y),
+                                    __float_as_int(r1f.z), __float_as_int(r1f.w)};
+            const float lim = h.t;
+            float tk[8];
+            bool hk[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int w = k >> 2, j = k & 3;
+                const float tnx = fmaf(qv(nwx[w], j), Ax, Bnx), tfx = fmaf(qv(fwx[w], j), Ax, Bfx);
+                const float tny = fmaf(qv(nwy[w], j), Ay, Bny), tfy = fmaf(qv(fwy[w], j), Ay, Bfy);
+                const float tnz = fmaf(qv(nwz[w], j), Az, Bnz), tfz = fmaf(qv(fwz[w], j), Az, Bfz);
+                const float tn = fmaxf(fmaxf(tnx, tny), fmaxf(tnz, tmin));
+                const float tf = fminf(fminf(tfx, tfy), fminf(tfz, lim));
+                hk[k] = tn <= tf && ((meta >> (24 + k)) & 1u);
+                tk[k] = tn;
+            }
+            constexpr int X = OCT >= 0 ? (((OCT & 1) << 2) | (OCT & 2) | ((OCT >> 2) & 1)) : 0;
+#pragma unroll
+            for (int pos = 7; pos >= 0; --pos) {
+                const int k = pos ^ X;
+                if (hk[k]) st.push(sp, ((uint64_t)__float_as_uint(tk[k]) << 32) | (uint32_t)ref[k]);
+            }
+            cur = pop_live(st, sp, tlim);
+            if (cur < 0 && leaf == 0) {
+                leaf = cur;
+                cur = pop_live(st, sp, tlim);
+            }
+        }
+        if (!__any_sync(0xffffffffu, go && leaf == 0)) break;
+    }
+}
+
 #ifndef FGL_OCTANT
 #define FGL_OCTANT 1  // octant-specialised descent when a warp's rays share an octant
 #endif
@@ -906,12 +1070,22 @@ __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre
 // rays of distant tiles), generates the rays in registers and runs the while-while traversal of
 // Aila & Laine (2009) one outer iteration at a time. The output slot (and, for hit points, the ray)
 // is recomputed from (tile, lane) at the write, so neither is held in registers during traversal.
-template <class Gen, bool kCount>
-__global__ void __launch_bounds__(kCastThreads, FGL_DYN_MINBLOCKS)
+#ifndef FGL_DYN8_MINBLOCKS
+#define FGL_DYN8_MINBLOCKS 8  // width 8: 8 CTAs x 4 warps per SM (64 registers: the node96q visit holds more)
+#endif
+template <class Gen, bool kCount, int kW>
+__global__ void __launch_bounds__(kCastThreads, kW == 8 ? FGL_DYN8_MINBLOCKS : FGL_DYN_MINBLOCKS)
     k_cast_dyn(const SceneView sv, const Gen gen, int64_t ntiles, const CastOut out, CastCounter *ctr) {
     constexpr unsigned kFull = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    uint64_t st[kStack];  // (entry t bits << 32) | node ref
+    using Stack = std::conditional_t<kW == 8, LaneStack8, LaneStack>;
+    Stack st;
+#if FGL_SSTACK > 0
+    __shared__ uint64_t s_stack[kSStack][kCastThreads];
+    st.sh = &s_stack[0][threadIdx.x];
+#else
+    st.sh = nullptr;
+#endif
     int sp = 0;
     int32_t cur = kDone, leaf = 0;
     Pre p;
@@ -919,17 +1093,31 @@ __global__ void __launch_bounds__(kCastThreads, FGL_DYN_MINBLOCKS)
     Hit h{0.f, INT_MAX, 0, 0};
     float tlim = 0.f;  // h.t * kExpand, the pop bound, updated with h.t
     const Node64 *__restrict__ nodes = sv.nodes;
+    const Node8 *__restrict__ nodes8 = reinterpret_cast<const Node8 *>(sv.nodes4);
+    // width 8: a tree whose stack bound (k_collapse) exceeds the stack is refused, loudly
+    const bool refuse = kW == 8 && __ldg(sv.wneed) > (unsigned int)kStack8;
+    if (refuse && threadIdx.x == 0) atomicOr(sv.err, 4u);
     const float tmin = gen.interval_min();
-    bool active = false;
+    bool active = false;  // the lane's ray is still being traversed
+    bool valid = false;   // the lane holds a ray of the current tile (result not yet written)
     unsigned long long wtile = 0;
     while (true) {
         if (!__any_sync(kFull, active)) {
+            // the whole tile is done: every lane writes its result now, in one full-warp store per
+            // output array (a tile's 8 columns are contiguous), instead of a partial-warp write each
+            // time some lane finishes
+            if (valid) {
+                Ray r{};
+                if (out.hit_xyz) gen.ray_at((int64_t)wtile, lane, r);
+                write_out(out, gen.index((int64_t)wtile, lane), r, h);
+            }
             unsigned long long nt = 0;
             if (lane == 0) nt = atomicAdd(&ctr->next, 1ull);
             wtile = __shfl_sync(kFull, nt, 0);
-            if (wtile >= (unsigned long long)ntiles) break;
+            if (wtile >= (unsigned long long)ntiles || refuse) break;
             Ray r;
-            if (gen.ray_at((int64_t)wtile, lane, r)) {
+            valid = gen.ray_at((int64_t)wtile, lane, r);
+            if (valid) {
                 p = precompute(r);
                 oct = ray_octant(p);
                 h = Hit{gen.interval_max(), INT_MAX, 0, 0};
@@ -946,27 +1134,39 @@ __global__ void __launch_bounds__(kCastThreads, FGL_DYN_MINBLOCKS)
         const unsigned act = __ballot_sync(kFull, active);
         const int o0 = __shfl_sync(kFull, oct, __ffs(act) - 1);
         if (__all_sync(kFull, !active || oct == o0)) {
-            switch (o0) {
-                case 0: descend<0, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 1: descend<1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 2: descend<2, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 3: descend<3, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 4: descend<4, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 5: descend<5, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                case 6: descend<6, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                default: descend<7, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+            if constexpr (kW == 8) {
+                switch (o0) {
+                    case 0: descend8<0, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 1: descend8<1, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 2: descend8<2, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 3: descend8<3, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 4: descend8<4, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 5: descend8<5, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 6: descend8<6, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    default: descend8<7, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                }
+            } else {
+                switch (o0) {
+                    case 0: descend<0, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 1: descend<1, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 2: descend<2, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 3: descend<3, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 4: descend<4, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 5: descend<5, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 6: descend<6, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    default: descend<7, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                }
             }
         } else
 #endif
-            descend<-1, kCount>(nodes, p, tmin, active, h, tlim, st, sp, cur, leaf);
-        leaves<kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
-        if (!active) continue;
-        if (cur == kDone) {
-            Ray r{};
-            if (out.hit_xyz) gen.ray_at((int64_t)wtile, lane, r);
-            write_out(out, gen.index((int64_t)wtile, lane), r, h);
-            active = false;
+        {
+            if constexpr (kW == 8)
+                descend8<-1, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf);
+            else
+                descend<-1, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
         }
+        leaves<kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
+        if (cur == kDone) active = false;
     }
     cast_epilogue(out, ctr, lane);
 }
@@ -974,28 +1174,36 @@ __global__ void __launch_bounds__(kCastThreads, FGL_DYN_MINBLOCKS)
 template <class Gen, bool kCount, int kMode>
 void launch_one(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
                 cudaStream_t s) {
-    static int oc = 0, sms = 0;
-    constexpr bool kDyn = kMode == kRay2;
+    // occupancy and SM count per device (a process may drive several GPUs)
+    constexpr int kMaxDev = 64;
+    static int oc_dev[kMaxDev] = {0}, sms_dev[kMaxDev] = {0};
+    constexpr bool kDyn = kMode == kRay2 || kMode == kRay8Q;
+    constexpr int kW = kMode == kRay8Q ? 8 : 2;
+    int dev;
+    FGL_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDev) throw Error(1, "CUDA device index out of range");
+    int &oc = oc_dev[dev], &sms = sms_dev[dev];
     if (!oc) {
-        int dev;
-        FGL_CUDA(cudaGetDevice(&dev));
         FGL_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (kDyn) {
+        if constexpr (kDyn) {
 #if FGL_CARVEOUT >= 0
-            // the kernel uses no shared memory: ask for the largest L1 share (node / triangle reuse)
-            FGL_CUDA(cudaFuncSetAttribute(k_cast_dyn<Gen, kCount>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                          FGL_CARVEOUT));
+            // the largest L1 share that still holds the resident CTAs' shared-memory stacks (plus the
+            // 1 KB per CTA the system reserves): node / triangle reuse lives in L1
+            const int need = (kW == 8 ? FGL_DYN8_MINBLOCKS : FGL_DYN_MINBLOCKS) * (kSStack * kCastThreads * 8 + 1024);
+            const int pct = std::max(FGL_CARVEOUT, (int)((100ll * need + 233471) / 233472));
+            FGL_CUDA(cudaFuncSetAttribute(k_cast_dyn<Gen, kCount, kW>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          std::min(pct, 100)));
 #endif
-            FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast_dyn<Gen, kCount>, kCastThreads, 0));
-        }
-        else
+            FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast_dyn<Gen, kCount, kW>, kCastThreads, 0));
+        } else {
             FGL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_cast<Gen, kCount, kMode>, kCastThreads, 0));
+        }
         if (oc < 1) oc = 1;
     }
     int64_t blocks = std::min<int64_t>((int64_t)sms * oc, (ntiles + kCastThreads / 32 - 1) / (kCastThreads / 32));
     blocks = std::max<int64_t>(blocks, 1);
-    if (kDyn)
-        k_cast_dyn<Gen, kCount><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
+    if constexpr (kDyn)
+        k_cast_dyn<Gen, kCount, kW><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
     else
         k_cast<Gen, kCount, kMode><<<(unsigned)blocks, kCastThreads, 0, s>>>(sv, gen, ntiles, o, ctr);
     FGL_LAUNCHED("k_cast");
@@ -1004,7 +1212,9 @@ void launch_one(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastO
 template <class Gen, bool kCount>
 void launch_mode(const SceneView &sv, const Gen &gen, int64_t ntiles, const CastOut &o, CastCounter *ctr,
                  cudaStream_t s) {
-    if (sv.width == 4 && sv.quantized)
+    if (sv.width == 8)
+        launch_one<Gen, kCount, kRay8Q>(sv, gen, ntiles, o, ctr, s);
+    else if (sv.width == 4 && sv.quantized)
         launch_one<Gen, kCount, kRay4Q>(sv, gen, ntiles, o, ctr, s);
     else if (sv.width == 4)
         launch_one<Gen, kCount, kRay4>(sv, gen, ntiles, o, ctr, s);

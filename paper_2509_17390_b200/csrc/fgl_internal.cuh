@@ -57,6 +57,14 @@ struct __align__(16) NodeQ {
     float4 f0;
     int4 q0, q1, q2;
 };
+// 8-wide compressed node ("node96q", wide.cu): c0a = (px, py, pz, meta = Ex | Ey << 8 | Ez << 16 |
+// valid << 24), c0b = (qlo_x[0..3], qlo_x[4..7], qhi_x[0..3], qhi_x[4..7]) bytes, c1a / c1b the same
+// for y / z, ref0 / ref1 = child refs of slots 0-3 / 4-7. Child plane = p + q 2^(E - 142).
+struct __align__(32) Node8 {
+    float4 c0a;
+    uint4 c0b, c1a, c1b;
+    int4 ref0, ref1;
+};
 constexpr float kFarBox = 3.0e38f;  // empty child: a degenerate box no ray with t <= t_max reaches
 constexpr int32_t kEmptyRef = INT32_MIN;
 constexpr int kLeafShift = 3;
@@ -86,8 +94,7 @@ struct BuildBuffers {
     uint32_t *vals[2] = {nullptr, nullptr};
     uint32_t *ghist = nullptr;     // [8][256] digit histograms
     uint64_t *sort_status = nullptr;  // [nblk][256] look-back status words (epoch | flag | count)
-    uint32_t *sort_tiles = nullptr;   // [8] per-pass tile counters
-    uint32_t sort_epoch = 0;
+    uint32_t *sort_tiles = nullptr;   // [16]: [0..7] per-pass tile counters, [8] device epoch counter
     float4 *tri = nullptr;         // [3T] tri48 in leaf order
     int2 *child = nullptr;         // [T-1]
     int2 *range = nullptr;         // [T-1]
@@ -106,6 +113,9 @@ struct BuildBuffers {
     float *cost = nullptr;         // [T-1] SAH cost of each internal node's subtree (restructuring)
     int32_t *tsize = nullptr;      // [T-1] leaves under each internal node (restructuring)
     int restructured = 0;          // 1: treelet-restructured tree (1-triangle leaves, free topology)
+    float *cost8 = nullptr;        // [T-1][8] SAH collapse costs C(n, 1..8) (width 8)
+    int32_t *wq = nullptr;         // [T] top-down collapse work queue (width 8)
+    unsigned int *wctr = nullptr;  // [4] queue head, tail, done, max stack need (width 8)
 };
 
 constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
@@ -114,9 +124,9 @@ constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
 // sort.cu
 int sort_tile_blocks(int64_t n);
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
-                      uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready, uint32_t *epoch,
-                      int *result_slot, cudaStream_t s, int shift0 = 0);  // vals0 == nullptr: key-only passes
-                                                                          // over bits [shift0, shift0 + key_bits)
+                      uint64_t *status, uint32_t *tile_ctr /*[16], zeroed once at allocation*/, uint32_t *ghist,
+                      bool ghist_ready, int *result_slot, cudaStream_t s,
+                      int shift0 = 0);  // vals0 == nullptr: key-only passes over bits [shift0, shift0 + key_bits)
 void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s,
                       int shift0 = 0);
 
@@ -128,6 +138,7 @@ void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t
 void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s);
 void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s, int restructure = 0);
 void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int leaf_size, cudaStream_t s);
+void launch_wide8(BuildBuffers &b, cudaStream_t s);  // wide.cu: SAH collapse to node96q
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
                           uint64_t *codes, cudaStream_t s);
 
@@ -162,9 +173,11 @@ struct CastOut {
 struct SceneView {
     const float4 *tri;
     const Node64 *nodes;
-    const Node128 *nodes4;
+    const Node128 *nodes4;  // node128 / node64q (width 4) or node96q (width 8, reinterpreted)
     int width;
     int quantized;
+    const unsigned int *wneed;  // width 8: the tree's traversal-stack bound (BuildBuffers::wctr[3])
+    unsigned int *err;          // sticky scene error flags (bit 2: width-8 stack bound exceeded)
 };
 void launch_cast_spinning(const SceneView &sv, const SpinParams &p, const float *poses, int64_t P, const CastOut &o,
                           CastCounter *ctr, cudaStream_t s);

@@ -7,7 +7,10 @@
 // per-digit counts, looks back over earlier tiles' published prefixes to find its global offsets
 // (base = keys with a smaller digit, from the all-pass histogram computed once up front — fused
 // into the Morton kernel for the build) and scatters keys and values: one read and one write of
-// each key per pass. Status words carry a per-pass epoch so they never need clearing.
+// each key per pass. Status words carry a per-pass epoch so they never need clearing; the epoch
+// counter lives in device memory and is advanced by k_sort_begin on the stream, so a sort captured
+// in a CUDA graph gets fresh epochs on every replay (a host-side epoch would be baked into the
+// graph and let a replay accept the previous replay's status words).
 #include <cuda/atomic>
 
 #include "fgl_internal.cuh"
@@ -60,7 +63,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
                                                           const uint32_t *__restrict__ vin,
                                                           uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
                                                           int64_t n, int shift, const uint32_t *__restrict__ hist,
-                                                          uint64_t *status, uint32_t *tile_ctr, uint32_t epoch) {
+                                                          uint64_t *status, uint32_t *tile_ctr,
+                                                          const uint32_t *epoch_end, int pass, int npass) {
     static_assert(kThreads == 256, "one thread per digit");
     constexpr int kT = kThreads * kIt, kSpan = kT / kWarps;
     __shared__ uint32_t wh[kWarps][256];
@@ -71,6 +75,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
     __shared__ uint64_t s_key[kT];
     __shared__ uint32_t s_val[kVals ? kT : 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, d = threadIdx.x;
+    // this sort's epochs are (end - npass, end]: written by k_sort_begin earlier on the stream
+    const uint32_t epoch = *epoch_end - (uint32_t)npass + 1u + (uint32_t)pass;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
     for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&wh[0][0])[i] = 0;
     // block-wide exclusive scan over the 256 digits (one value per thread)
@@ -179,6 +185,18 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
         if constexpr (kVals) vout[pos] = s_val[p];
     }
 }
+// Per-sort setup on the stream: zero the per-pass tile counters and reserve npass fresh epochs
+// (ctl[8] = the last epoch of this sort; epoch 0 marks never-written status words and is skipped
+// at wrap-around).
+__global__ void k_sort_begin(uint32_t *ctl, int npass) {
+    if (threadIdx.x < 8) ctl[threadIdx.x] = 0u;
+    if (threadIdx.x == 8) {
+        const uint32_t e = ctl[8];
+        uint32_t ne = e + (uint32_t)npass;
+        if (ne < e) ne = (uint32_t)npass;  // wrapped past 0: restart at 1..npass
+        ctl[8] = ne;
+    }
+}
 }  // namespace
 
 int sort_tile_blocks(int64_t n) { return (int)((n + kMinTile - 1) / kMinTile); }
@@ -193,7 +211,7 @@ void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *g
 }
 
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
-                      uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready, uint32_t *epoch,
+                      uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready,
                       int *result_slot, cudaStream_t s, int shift0) {
     *result_slot = 0;
     if (n <= 1) return;
@@ -203,20 +221,20 @@ void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_
     const bool kv = vals0 != nullptr;
     const int64_t tile = (int64_t)kThreads * (kv ? kItemsKV : kItemsK);
     const unsigned nblk = (unsigned)((n + tile - 1) / tile);
-    FGL_CUDA(cudaMemsetAsync(tile_ctr, 0, sizeof(uint32_t) * 8, s));
+    k_sort_begin<<<1, 32, 0, s>>>(tile_ctr, npass);
+    FGL_LAUNCHED("k_sort_begin");
     uint64_t *k[2] = {keys0, keys1};
     uint32_t *v[2] = {vals0, vals1};
     int cur = 0;
     for (int p = 0; p < npass; ++p) {
-        if (++*epoch == 0) ++*epoch;  // epoch 0 marks never-written status words
         if (kv)
             k_onesweep<kItemsKV, true><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n,
                                                                  shift0 + 8 * p, ghist + 256 * p, status,
-                                                                 tile_ctr + p, *epoch);
+                                                                 tile_ctr + p, tile_ctr + 8, p, npass);
         else
             k_onesweep<kItemsK, false><<<nblk, kThreads, 0, s>>>(k[cur], nullptr, k[cur ^ 1], nullptr, n,
                                                                  shift0 + 8 * p, ghist + 256 * p, status,
-                                                                 tile_ctr + p, *epoch);
+                                                                 tile_ctr + p, tile_ctr + 8, p, npass);
         FGL_LAUNCHED("k_onesweep");
         cur ^= 1;
     }

@@ -42,7 +42,14 @@ class PeerGather:
     NCCL pass): every rank owns global [P][...] output buffers allocated by libfgl, the ranks
     exchange CUDA IPC handles (over `cpu_group`, e.g. gloo), and the cast kernel stores each ray's
     result into all ranks' buffers (P2P stores over NVLink/NVSwitch) while it traces — no separate
-    collective. Call `cast(...)` with this rank's pose block, then `sync()` before reading."""
+    collective. Call `cast(...)` with this rank's pose block, then `wait()` (device) or `sync()`
+    (host) before reading `range` / `tri_id`.
+
+    The outputs are double-buffered: step k writes buffer k % 2. A peer can start step k + 1 as soon
+    as its own wait for step k returns, but it writes the other buffer; it reaches buffer k % 2 again
+    only in step k + 2, which waits for this rank's step-(k + 1) signal. So a rank that consumes
+    step k's results on its stream before launching its own step-(k + 1) cast (the stream orders
+    the reads before the cast, hence before its signal) never has them overwritten while it reads."""
 
     def __init__(self, P: int, pattern, device, cpu_group=None):
         from . import fgl as _f
@@ -53,9 +60,11 @@ class PeerGather:
         self.pattern = pattern
         self.shape = (P, len(pattern.elev_deg), int(pattern.columns))
         self.device = torch.device(device)
+        # [range, tri_id] x 2 parities, then the completion counter
         self._own = [_f.DeviceBuffer(self.shape, torch.float32, device), _f.DeviceBuffer(self.shape, torch.int32, device),
+                     _f.DeviceBuffer(self.shape, torch.float32, device), _f.DeviceBuffer(self.shape, torch.int32, device),
                      _f.DeviceBuffer((8,), torch.int32, device)]
-        self._own[2].tensor.zero_()
+        self._own[4].tensor.zero_()
         torch.cuda.synchronize(self.device)
         self.steps = 0
         handles = tuple(b.ipc_handle() for b in self._own)
@@ -65,33 +74,35 @@ class PeerGather:
         else:
             allh = [handles]
         self._peers = []
-        for r, (hr, ht, hf) in enumerate(allh):
+        for r, hs in enumerate(allh):
             if r == self.rank:
                 continue
-            self._peers.append((_f.DeviceBuffer.open_ipc(hr, self.shape, torch.float32, device),
-                                _f.DeviceBuffer.open_ipc(ht, self.shape, torch.int32, device),
-                                _f.DeviceBuffer.open_ipc(hf, (8,), torch.int32, device)))
-        self.range_ptrs = [self._own[0].ptr] + [p[0].ptr for p in self._peers]
-        self.tri_ptrs = [self._own[1].ptr] + [p[1].ptr for p in self._peers]
-        self.flag_ptrs = [self._own[2].ptr] + [p[2].ptr for p in self._peers]
+            dts = (torch.float32, torch.int32, torch.float32, torch.int32)
+            self._peers.append(tuple(_f.DeviceBuffer.open_ipc(h, self.shape, dt, device) for h, dt in zip(hs[:4], dts))
+                               + (_f.DeviceBuffer.open_ipc(hs[4], (8,), torch.int32, device),))
+        self.range_ptrs = [[self._own[2 * b].ptr] + [p[2 * b].ptr for p in self._peers] for b in (0, 1)]
+        self.tri_ptrs = [[self._own[2 * b + 1].ptr] + [p[2 * b + 1].ptr for p in self._peers] for b in (0, 1)]
+        self.flag_ptrs = [self._own[4].ptr] + [p[4].ptr for p in self._peers]
 
     @property
     def range(self) -> torch.Tensor:
-        return self._own[0].tensor
+        """This rank's gathered ranges of the latest step (valid after wait() / sync())."""
+        return self._own[2 * ((self.steps - 1) % 2)].tensor
 
     @property
     def tri_id(self) -> torch.Tensor:
-        return self._own[1].tensor
+        return self._own[2 * ((self.steps - 1) % 2) + 1].tensor
 
     def shard(self):
         return shard_range(self.P, self.world, self.rank)
 
     def cast(self, scene, poses_all: torch.Tensor, stream=None):
         """Cast this rank's contiguous pose block of `poses_all` ([P][3][4]) into every rank's output
-        and signal every rank's completion counter (device side)."""
+        buffer of this step's parity and signal every rank's completion counter (device side)."""
         from . import fgl as _f
         lo, hi = self.shard()
-        _f.cast_spinning_gather(scene, poses_all[lo:hi], self.pattern, lo, self.range_ptrs, self.tri_ptrs,
+        b = self.steps % 2
+        _f.cast_spinning_gather(scene, poses_all[lo:hi], self.pattern, lo, self.range_ptrs[b], self.tri_ptrs[b],
                                 self.flag_ptrs, stream)
         self.steps += 1
 
