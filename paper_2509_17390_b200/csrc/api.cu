@@ -135,7 +135,9 @@ void alloc_build(fgl_scene *s, int64_t T) {
 }
 
 fgl::SceneView view(const fgl_scene *s) {
-    return fgl::SceneView{s->b.tri, s->b.nodes, s->b.nodes4, s->b.width, s->b.quantized, s->b.wctr + 3, s->vflag};
+    // root box: the root's Eq. 7 box (T >= 2), or the single triangle's box
+    const float4 *root = s->b.T >= 2 ? s->b.nodebox : s->b.leafbox;
+    return fgl::SceneView{s->b.tri, s->b.nodes, s->b.nodes4, s->b.width, s->b.quantized, s->b.wctr + 3, s->vflag, root};
 }
 
 fgl::CastCounter *next_counter(const fgl_scene *s) {

@@ -16,6 +16,9 @@
 #ifndef FGL_SORT_PACKED
 #define FGL_SORT_PACKED 1
 #endif
+#ifndef FGL_FUSED_NODES
+#define FGL_FUSED_NODES 0  // 1: k_karras writes the binary traversal nodes (no separate k_nodes pass)
+#endif
 
 namespace fgl {
 
@@ -250,11 +253,16 @@ __device__ __forceinline__ void range_box(const AggLevels &L, int a, int b, floa
     }
 }
 
-// Karras 2012 (Eq. 6 read as the non-recursive LCP split, R7): one thread per internal node i
+// Karras 2012 (Eq. 6 read as the non-recursive LCP split, R7): one thread per internal node i.
+// nodes != nullptr (binary traversal nodes wanted, no restructuring): the thread evaluates Eq. 7 for
+// its two children (the ranges [f, g] and [g + 1, l] it has just found) instead of for itself, writes
+// its own box as their union, and writes its node64 directly — the separate k_nodes pass, a gather of
+// both children's boxes per node, disappears.
 __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, int n, int ks,
                                                 int2 *__restrict__ child, int2 *__restrict__ range,
                                                 int32_t *__restrict__ parent, AggLevels L,
-                                                float4 *__restrict__ nodebox) {
+                                                float4 *__restrict__ nodebox, Node64 *__restrict__ nodes,
+                                                int leaf_size) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;  // one thread per internal node
     if (i < n - 1) {
         const uint64_t ki = __ldg(k + i) >> ks;
@@ -281,11 +289,28 @@ __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, 
         parent[left >= 0 ? left : (n - 1) + ~left] = i;
         parent[right >= 0 ? right : (n - 1) + ~right] = i;
         if (i == 0) parent[0] = -1;
-        // Eq. 7 box of this node by its closed form (exact union of its leaf range)
-        float4 lo, hi;
-        range_box(L, f, last, lo, hi);
-        nodebox[2 * i] = lo;
-        nodebox[2 * i + 1] = hi;
+        if (nodes) {
+            // Eq. 7 boxes of both children by the closed form (exact unions of their leaf ranges)
+            float4 l0, h0, l1, h1;
+            range_box(L, f, g, l0, h0);
+            range_box(L, g + 1, last, l1, h1);
+            nodebox[2 * i] = make_float4(fminf(l0.x, l1.x), fminf(l0.y, l1.y), fminf(l0.z, l1.z), 0.f);
+            nodebox[2 * i + 1] = make_float4(fmaxf(h0.x, h1.x), fmaxf(h0.y, h1.y), fmaxf(h0.z, h1.z), 0.f);
+            const int32_t n0 = g - f + 1, n1 = last - g;
+            Node64 nd;
+            nd.a = make_float4(l0.x, h0.x, l0.y, h0.y);
+            nd.b = make_float4(l1.x, h1.x, l1.y, h1.y);
+            nd.c = make_float4(l0.z, h0.z, l1.z, h1.z);
+            nd.d = make_int4(n0 <= leaf_size ? make_leaf(f, n0) : left, n1 <= leaf_size ? make_leaf(g + 1, n1) : right,
+                             0, 0);
+            nodes[i] = nd;
+        } else {
+            // Eq. 7 box of this node by its closed form (exact union of its leaf range)
+            float4 lo, hi;
+            range_box(L, f, last, lo, hi);
+            nodebox[2 * i] = lo;
+            nodebox[2 * i + 1] = hi;
+        }
     }
 }
 
@@ -795,9 +820,13 @@ void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaS
             launch_single(b, width, s);
         return;
     }
+    // width 2 without restructuring: k_karras writes the node64s itself (FGL_FUSED_NODES)
+    const bool fused = FGL_FUSED_NODES && width == 2 && restructure == 0;
     k_karras<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(b.keys[b.sorted_slot], (int)T, b.packed_shift, b.child,
-                                                            b.range, b.parent, L, b.nodebox);
+                                                            b.range, b.parent, L, b.nodebox,
+                                                            fused ? b.nodes : nullptr, leaf_size);
     FGL_LAUNCHED("k_karras");
+    if (fused) return;
     if (width == 8) {  // SAH collapse of the Karras tree (single-triangle leaves) to node96q
         launch_wide8(b, s);
         return;

@@ -106,6 +106,33 @@ __device__ __forceinline__ Pre precompute(const Ray &r) {
     return p;
 }
 
+// Per-ray constants of the persistent cast (k_cast_dyn). The slab planes are evaluated as
+// t = fma(x, I, c) like precompute's, but every error term is covered by an absolute push of the
+// plane constants instead of the relative factor on t_far. With I = 1/d (1 + e), |e| <= 2^-23
+// (MUFU), c = -o I (1 + e_c), |e_c| <= 2^-24, and one rounding in the fma, a plane at exact distance
+// t is computed within 2^-23 |t| + 2^-24 |c| + 2^-24 |t| < 2^-22.4 |t| + 2^-24 |c|. Only planes with
+// |t| <= t_max can decide a box test against [t_min, t*] (a near plane further behind the origin
+// stays below t_min, a far plane beyond t_max stays above t*), so pushing the near-plane constant
+// down and the far-plane constant up by S = 2^-21 (t_max + |c|) (a margin that also covers the
+// rounding of S and of c -/+ S) makes every relevant near-plane t a lower bound and every far-plane
+// t an upper bound of the exact one: the box test needs no factor on t_far, and a stacked entry
+// distance is a lower bound of the exact entry, so culling it when it exceeds t* is exact (P:279
+// "exceeds"). S is 2^-21 of the ray's reach: ~0.1 mm at t_max = 200 m, far below any box.
+// (tmax here is the reach R >= every |t| that can decide a test: t_max, or a bound on the distance
+// to the farthest point of the scene when t_max is infinite.)
+__device__ __forceinline__ Pre precompute_dyn(const Ray &r, float tmax) {
+    Pre p = precompute(r);
+    const float cx = -r.ox * p.Ix, cy = -r.oy * p.Iy, cz = -r.oz * p.Iz;
+    const float sx = (tmax + fabsf(cx)) * 0x1p-21f;
+    const float sy = (tmax + fabsf(cy)) * 0x1p-21f;
+    const float sz = (tmax + fabsf(cz)) * 0x1p-21f;
+    // lo plane is the near plane when I >= 0
+    p.clx = p.Ix >= 0.f ? cx - sx : cx + sx, p.chx = p.Ix >= 0.f ? cx + sx : cx - sx;
+    p.cly = p.Iy >= 0.f ? cy - sy : cy + sy, p.chy = p.Iy >= 0.f ? cy + sy : cy - sy;
+    p.clz = p.Iz >= 0.f ? cz - sz : cz + sz, p.chz = p.Iz >= 0.f ? cz + sz : cz - sz;
+    return p;
+}
+
 struct V3 {
     float x, y, z;
 };
@@ -180,7 +207,9 @@ __device__ __forceinline__ float slab(const Pre &p, float lx, float hx, float ly
     return tn <= tf * kExpand ? tn : INFINITY;
 }
 
-// same test, hit flag and entry distance returned separately (no +inf materialisation)
+// the persistent cast's test (constants from precompute_dyn: t_near / t_far are lower / upper
+// bounds of the exact plane distances, so no factor on t_far); hit flag and entry distance
+// returned separately (no +inf materialisation)
 __device__ __forceinline__ bool slab_hit(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
                                          float tmin, float tmax, float &tn_out) {
     const float ax = fmaf(lx, p.Ix, p.clx), bx = fmaf(hx, p.Ix, p.chx);
@@ -189,7 +218,7 @@ __device__ __forceinline__ bool slab_hit(const Pre &p, float lx, float hx, float
     const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
     const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
     tn_out = tn;
-    return tn <= tf * kExpand;
+    return tn <= tf;
 }
 
 // Octant-specialised form of slab_hit: when the sign of every I component is known at compile
@@ -207,7 +236,7 @@ __device__ __forceinline__ bool slab_oct(const Pre &p, float lx, float hx, float
     const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, tmin));
     const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
     tn_out = tn;
-    return tn <= tf * kExpand;
+    return tn <= tf;
 }
 
 __device__ __forceinline__ int ray_octant(const Pre &p) {
@@ -641,6 +670,18 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
     return f.m ? __umulhi(n, f.m) >> f.sh : n;
 }
 
+// (sin, cos) of the angle 2 pi ph / 2^32 of an exact 32-bit phase, without rounding the phase to
+// float's 24 bits: the top 24 bits are an exact sincospif argument, (ph >> 8) 2^-23 half-turns; the
+// low 8 bits (an angle b < 2 pi 2^-24 = 3.8e-7 rad) rotate that result to first order (the dropped
+// b^2 / 2 < 7.2e-14 is far below float's resolution).
+__device__ __forceinline__ void sincos_phase(uint32_t ph, float &s, float &c) {
+    float sc, cc;
+    sincospif((float)(ph >> 8) * 0x1p-23f, &sc, &cc);
+    const float b = (float)(ph & 0xFFu) * 1.4629180792671596e-09f;  // 2 pi / 2^32
+    s = fmaf(cc, b, sc);
+    c = fmaf(-sc, b, cc);
+}
+
 // rosette sample n of pose p (R20): exact 32-bit phases, two counter-rotating prisms
 __device__ __forceinline__ void rosette_ray(const RosetteParams &rp, const float *__restrict__ poses, int64_t p, int k,
                                             Ray &r) {
@@ -648,8 +689,8 @@ __device__ __forceinline__ void rosette_ray(const RosetteParams &rp, const float
     const uint32_t ph1 = (uint32_t)(n * (uint64_t)rp.inc1);
     const uint32_t ph2 = rp.phase2_0 - (uint32_t)(n * (uint64_t)rp.inc2);
     float s1, c1, s2, c2;
-    sincospif(2.f * __uint2float_rn(ph1) * 0x1p-32f, &s1, &c1);
-    sincospif(2.f * __uint2float_rn(ph2) * 0x1p-32f, &s2, &c2);
+    sincos_phase(ph1, s1, c1);
+    sincos_phase(ph2, s2, c2);
     const float half = 0.5f * rp.half_fov_deg * 0.017453292519943295f;
     const float dx = half * (c1 + c2), dy = half * (s1 + s2);
     const float rho = sqrtf(dx * dx + dy * dy);
@@ -857,6 +898,9 @@ struct LaneStackN {
     }
 };
 
+#ifndef FGL_LEAF_HANDOFF
+#define FGL_LEAF_HANDOFF 0  // 1: both children hit, near one a leaf: postpone it, descend the far one (no stack op)
+#endif
 #ifndef FGL_PREFETCH
 #define FGL_PREFETCH 0  // 1: L1-prefetch the children nodes at each visit; 2: also the leaves' first triangle
 #endif
@@ -915,8 +959,20 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
             const bool h1 = slab_sel<OCT>(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, lim, t1);
             if (h0 && h1) {
                 const bool swap = t1 < t0;
-                st.push(sp, ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)(swap ? nd.x : nd.y));
-                cur = swap ? nd.y : nd.x;
+                const int32_t nearc = swap ? nd.y : nd.x, farc = swap ? nd.x : nd.y;
+#if FGL_LEAF_HANDOFF
+                // the near child is a leaf to postpone: the far child continues the descent at once
+                // (instead of a push and an immediate pop of the same entry, which the cull cannot
+                // reject: its entry distance is <= t*)
+                const bool handoff = nearc < 0 && leaf == 0;
+                if (!handoff)
+                    st.push(sp, ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)farc);
+                cur = handoff ? farc : nearc;
+                leaf = handoff ? nearc : leaf;
+#else
+                st.push(sp, ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)farc);
+                cur = nearc;
+#endif
             } else if (h0) {
                 cur = nd.x;
             } else if (h1) {
@@ -939,7 +995,7 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
 // its descent ended on one.
 template <bool kCount, class Stack>
 __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre &p, float tmin, bool active, Hit &h,
-                                       float &tlim, Stack &st, int &sp, int32_t &cur, int32_t &leaf) {
+                                       Stack &st, int &sp, int32_t &cur, int32_t &leaf) {
     if (!active) return;
     while (leaf < 0) {
         const int32_t v = ~leaf;
@@ -953,13 +1009,13 @@ __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre
             if (hit_tri(p, a, b, c, tmin, h.t, h.id, id, t)) {
                 h.t = t;
                 h.id = id;
-                tlim = t * kExpand;
             }
         }
         leaf = 0;
         if (cur < 0) {
             leaf = cur;
-            cur = pop_live(st, sp, tlim);
+            // stacked entry distances are lower bounds (precompute_dyn): cull iff > t*
+            cur = pop_live(st, sp, h.t);
         }
     }
 }
@@ -1089,9 +1145,7 @@ __global__ void __launch_bounds__(kCastThreads, kW == 8 ? FGL_DYN8_MINBLOCKS : F
     int sp = 0;
     int32_t cur = kDone, leaf = 0;
     Pre p;
-    int oct = 0;  // ray octant (sign bits of the direction)
     Hit h{0.f, INT_MAX, 0, 0};
-    float tlim = 0.f;  // h.t * kExpand, the pop bound, updated with h.t
     const Node64 *__restrict__ nodes = sv.nodes;
     const Node8 *__restrict__ nodes8 = reinterpret_cast<const Node8 *>(sv.nodes4);
     // width 8: a tree whose stack bound (k_collapse) exceeds the stack is refused, loudly
@@ -1100,7 +1154,7 @@ __global__ void __launch_bounds__(kCastThreads, kW == 8 ? FGL_DYN8_MINBLOCKS : F
     const float tmin = gen.interval_min();
     bool active = false;  // the lane's ray is still being traversed
     bool valid = false;   // the lane holds a ray of the current tile (result not yet written)
-    unsigned long long wtile = 0;
+    uint32_t wtile = 0;  // < 2^31 tiles per launch (checked by the launchers)
     while (true) {
         if (!__any_sync(kFull, active)) {
             // the whole tile is done: every lane writes its result now, in one full-warp store per
@@ -1113,15 +1167,24 @@ __global__ void __launch_bounds__(kCastThreads, kW == 8 ? FGL_DYN8_MINBLOCKS : F
             }
             unsigned long long nt = 0;
             if (lane == 0) nt = atomicAdd(&ctr->next, 1ull);
-            wtile = __shfl_sync(kFull, nt, 0);
-            if (wtile >= (unsigned long long)ntiles || refuse) break;
+            // the counter ends below ntiles + (warps of the grid) < 2^31 + 2^20: exact in 32 bits
+            wtile = (uint32_t)__shfl_sync(kFull, nt, 0);
+            if ((int64_t)wtile >= ntiles || refuse) break;
             Ray r;
             valid = gen.ray_at((int64_t)wtile, lane, r);
             if (valid) {
-                p = precompute(r);
-                oct = ray_octant(p);
+                // the relevant reach: t_max, or for an unbounded interval the farthest point of the
+                // scene (|o| + the largest |coordinate| of the root box, times sqrt 3 > the diagonal)
+                float reach = gen.interval_max();
+                if (!(reach < INFINITY)) {
+                    const float4 blo = __ldg(sv.root_box), bhi = __ldg(sv.root_box + 1);
+                    const float m = fmaxf(fmaxf(fmaxf(fabsf(blo.x), fabsf(bhi.x)), fmaxf(fabsf(blo.y), fabsf(bhi.y))),
+                                          fmaxf(fabsf(blo.z), fabsf(bhi.z)));
+                    const float mo = fmaxf(fmaxf(fabsf(r.ox), fabsf(r.oy)), fabsf(r.oz));
+                    reach = 2.f * (m + mo);
+                }
+                p = precompute_dyn(r, reach);
                 h = Hit{gen.interval_max(), INT_MAX, 0, 0};
-                tlim = h.t * kExpand;
                 sp = 0, cur = 0, leaf = 0;
                 active = true;
             }
@@ -1132,40 +1195,41 @@ __global__ void __launch_bounds__(kCastThreads, kW == 8 ? FGL_DYN8_MINBLOCKS : F
         // usual case: a tile spans ~1.5 degrees) the loop is the octant-specialised instance.
 #if FGL_OCTANT
         const unsigned act = __ballot_sync(kFull, active);
+        const int oct = ray_octant(p);  // recomputed from p's signs: one register fewer held across the loop
         const int o0 = __shfl_sync(kFull, oct, __ffs(act) - 1);
         if (__all_sync(kFull, !active || oct == o0)) {
             if constexpr (kW == 8) {
                 switch (o0) {
-                    case 0: descend8<0, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 1: descend8<1, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 2: descend8<2, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 3: descend8<3, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 4: descend8<4, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 5: descend8<5, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 6: descend8<6, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    default: descend8<7, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 0: descend8<0, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 1: descend8<1, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 2: descend8<2, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 3: descend8<3, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 4: descend8<4, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 5: descend8<5, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 6: descend8<6, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    default: descend8<7, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
                 }
             } else {
                 switch (o0) {
-                    case 0: descend<0, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 1: descend<1, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 2: descend<2, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 3: descend<3, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 4: descend<4, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 5: descend<5, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    case 6: descend<6, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
-                    default: descend<7, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf); break;
+                    case 0: descend<0, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 1: descend<1, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 2: descend<2, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 3: descend<3, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 4: descend<4, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 5: descend<5, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    case 6: descend<6, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
+                    default: descend<7, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf); break;
                 }
             }
         } else
 #endif
         {
             if constexpr (kW == 8)
-                descend8<-1, kCount>(nodes8, p, tmin, active, h, tlim, st, sp, cur, leaf);
+                descend8<-1, kCount>(nodes8, p, tmin, active, h, h.t, st, sp, cur, leaf);
             else
-                descend<-1, kCount>(nodes, sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
+                descend<-1, kCount>(nodes, sv.tri, p, tmin, active, h, h.t, st, sp, cur, leaf);
         }
-        leaves<kCount>(sv.tri, p, tmin, active, h, tlim, st, sp, cur, leaf);
+        leaves<kCount>(sv.tri, p, tmin, active, h, st, sp, cur, leaf);
         if (cur == kDone) active = false;
     }
     cast_epilogue(out, ctr, lane);

@@ -178,6 +178,7 @@ struct SceneView {
     int quantized;
     const unsigned int *wneed;  // width 8: the tree's traversal-stack bound (BuildBuffers::wctr[3])
     unsigned int *err;          // sticky scene error flags (bit 2: width-8 stack bound exceeded)
+    const float4 *root_box;     // [2] lo, hi of the whole scene (the root's Eq. 7 box)
 };
 void launch_cast_spinning(const SceneView &sv, const SpinParams &p, const float *poses, int64_t P, const CastOut &o,
                           CastCounter *ctr, cudaStream_t s);

@@ -91,7 +91,9 @@ def test_raygen_spinning_matches_oracle(fgl):
         oo, dd = oracle.pattern_rays(pat, poses)
         assert np.array_equal(o.cpu().numpy().astype(np.float64), oo)     # x_s = t_s exactly
         err = np.abs(d.cpu().numpy().astype(np.float64) - dd).max()
-        assert err < 8 * 2.0 ** -23, (name, err)                           # <= 8 float32 ulps
+        # <= 2^-21 (measured <= 2^-21.1 over 4 sensors x 32 poses, tools/raygen_err.py);
+        # the mode-A classifier's eps_rel = 2^-19 covers the worst-case bound 12 x 2^-24 ~ 2^-20.4
+        assert err <= 2.0 ** -21, (name, err)
 
 
 def test_raygen_rosette_matches_oracle(fgl):
@@ -100,7 +102,9 @@ def test_raygen_rosette_matches_oracle(fgl):
     for ff in (0, 999, 123456789):
         o, d = fgl.export_rays(ros, poses, first_frame=ff)
         oo, dd = oracle.pattern_rays(ros, poses, ff)
-        assert np.abs(d.cpu().numpy().astype(np.float64) - dd).max() < 2e-6
+        # exact 32-bit phases turned into angles without rounding to 24 bits (cast.cu sincos_phase):
+        # measured <= 2^-22.5; the bound asserted is the spinning one, 2^-21 (< mode-A eps 2^-19)
+        assert np.abs(d.cpu().numpy().astype(np.float64) - dd).max() <= 2.0 ** -21
         assert np.array_equal(o.cpu().numpy().astype(np.float64), oo)
 
 
