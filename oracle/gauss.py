@@ -125,6 +125,34 @@ def density_tiled(g, grid, kappa: float, tile: int = 8):
     return D, fsum, marg
 
 
+def density_tiled_literal(g, grid, kappa: float, tile: int = 8):
+    """Eqs. 8-9 read literally (no R25 truncation): every voxel of a tile sums exp(-m^2/2) f over
+    the WHOLE candidate set C_tile of Eq. 8, however far outside the kappa ellipsoid a candidate's
+    m^2 lies. The result depends on the tile partition (the reason for R25); it is kept as the
+    literal reading against which R25 is pinned (tests/test_oracle_gauss.py). Returns (D, excess)
+    where excess is the sum over candidates with m^2 > kappa^2 of f (each such term is below
+    exp(-kappa^2/2) f, so |D_literal - D_R25| <= exp(-kappa^2/2) excess)."""
+    v = centers(grid.origin, grid.h, grid.dims)
+    lo, hi = aabb(g.mu, g.quat, g.scale, kappa)
+    A = precision(g.quat, g.scale)
+    mu = g.mu.astype(np.float64)
+    f = g.opacity.astype(np.float64)
+    nx, ny, nz = grid.dims
+    D = np.zeros((nz, ny, nx))
+    excess = np.zeros_like(D)
+    for z0 in range(0, nz, tile):
+        for y0 in range(0, ny, tile):
+            for x0 in range(0, nx, tile):
+                sel = (slice(z0, min(z0 + tile, nz)), slice(y0, min(y0 + tile, ny)), slice(x0, min(x0 + tile, nx)))
+                tv = v[sel].reshape(-1, 3)
+                for n in tile_candidates(lo, hi, tv.min(axis=0), tv.max(axis=0)):
+                    d = v[sel] - mu[n]
+                    m2 = np.einsum("...i,ij,...j->...", d, A[n], d)
+                    D[sel] += np.exp(-0.5 * m2) * f[n]
+                    excess[sel] += np.where(m2 > kappa * kappa, f[n], 0.0)
+    return D, excess
+
+
 def density(g, grid, kappa: float):
     """Eq. 9 with R25, each Gaussian scattered to the voxels whose centres lie in its Eq. 4 box
     (the kappa ellipsoid lies inside that box, so nothing else can receive a contribution).

@@ -265,6 +265,7 @@ void fgl_scene_destroy(fgl_scene *s) {
 fgl_status fgl_scene_upload_mesh(fgl_scene *s, const float *verts, int64_t V, const int32_t *tris, int64_t T,
                                  int ptr_kind, void *stream) {
     FGL_API_BEGIN
+    fgl::NvtxRange nvtx_range_("fgl upload (A1)");
     if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
     const bool async = (ptr_kind & FGL_ASYNC) != 0;
     ptr_kind &= ~FGL_ASYNC;
@@ -536,6 +537,7 @@ fgl_status fgl_scene_check(fgl_scene *s, void *stream) {
 
 fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *stream) {
     FGL_API_BEGIN
+    fgl::NvtxRange nvtx_range_("fgl build");
     if (!s) throw Error(FGL_E_USAGE, "scene is NULL");
     if (s->T <= 0) throw Error(FGL_E_USAGE, "no mesh uploaded");
     // default b (R7): 10 bits per axis (30-bit keys, four sort passes) below 4 M primitives, where
@@ -582,6 +584,7 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
 
 fgl_status fgl_scene_refit(fgl_scene *s, const float *verts, int64_t V, int ptr_kind, void *stream) {
     FGL_API_BEGIN
+    fgl::NvtxRange nvtx_range_("fgl refit");
     check_built(s);
     if (s->gauss) throw Error(FGL_E_USAGE, "refit is for triangle / point scenes");
     const bool async = (ptr_kind & FGL_ASYNC) != 0;
@@ -632,6 +635,7 @@ fgl_status fgl_cast_spinning(const fgl_scene *s, const fgl_spinning *pattern, co
                              float *range, int32_t *tri_id, float *hit_xyz, int32_t *node_counts, int32_t *tri_counts,
                              void *stream) {
     FGL_API_BEGIN
+    fgl::NvtxRange nvtx_range_("fgl cast spinning (A8-A11)");
     check_cast(s);
     fgl::SpinParams sp = spin_params(pattern);
     if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
@@ -647,6 +651,7 @@ fgl_status fgl_cast_rosette(const fgl_scene *s, const fgl_rosette *pattern, cons
                             int64_t first_frame, float *range, int32_t *tri_id, float *hit_xyz, int32_t *node_counts,
                             int32_t *tri_counts, void *stream) {
     FGL_API_BEGIN
+    fgl::NvtxRange nvtx_range_("fgl cast rosette (A8-A11)");
     check_cast(s);
     fgl::RosetteParams rp = rosette_params(pattern, first_frame);
     if (P < 0) throw Error(FGL_E_USAGE, "P must be >= 0");
@@ -661,6 +666,7 @@ fgl_status fgl_cast_rosette(const fgl_scene *s, const fgl_rosette *pattern, cons
 fgl_status fgl_cast_rays(const fgl_scene *s, const float *orig, const float *dir, int64_t R, float t_min, float t_max,
                          float *range, int32_t *tri_id, void *stream) {
     FGL_API_BEGIN
+    fgl::NvtxRange nvtx_range_("fgl cast rays (A9-A11)");
     check_cast(s);
     check_interval(t_min, t_max);
     if (R < 0) throw Error(FGL_E_USAGE, "R must be >= 0");
@@ -692,6 +698,7 @@ fgl_status fgl_cast_spinning_gather_signal(const fgl_scene *s, const fgl_spinnin
                                            int32_t *const *tri_bufs, int32_t *const *flags, int32_t npeer,
                                            void *stream) {
     FGL_API_BEGIN
+    fgl::NvtxRange nvtx_range_("fgl cast + gather (A8-A12)");
     check_cast(s);
     fgl::SpinParams sp = spin_params(pattern);
     if (P < 0 || first_pose < 0) throw Error(FGL_E_USAGE, "P and first_pose must be >= 0");

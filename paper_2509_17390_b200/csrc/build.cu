@@ -16,6 +16,9 @@
 #ifndef FGL_SORT_PACKED
 #define FGL_SORT_PACKED 1
 #endif
+#ifndef FGL_RANGEBOX_DYN
+#define FGL_RANGEBOX_DYN 0  // 1: Eq. 7 closed form by loops with exact trip counts (measured slower)
+#endif
 #ifndef FGL_FUSED_NODES
 #define FGL_FUSED_NODES 0  // 1: k_karras writes the binary traversal nodes (no separate k_nodes pass)
 #endif
@@ -235,20 +238,33 @@ __device__ __forceinline__ void range_box(const AggLevels &L, int a, int b, floa
         if (lv + 1 < L.nlev) {
             const int rem = B - A;
             const int nf = min((8 - (A & 7)) & 7, rem);
+#if FGL_RANGEBOX_DYN
+            // loops with the exact trip count: a predicated-off unrolled copy still takes an issue slot
+            for (int k = 0; k < nf; ++k) acc(lo, hi, p, A + k);
+#else
 #pragma unroll
             for (int k = 0; k < 7; ++k)
                 if (k < nf) acc(lo, hi, p, A + k);
+#endif
             A += nf;
             const int nb = min(B & 7, B - A);
+#if FGL_RANGEBOX_DYN
+            for (int k = 0; k < nb; ++k) acc(lo, hi, p, B - 1 - k);
+#else
 #pragma unroll
             for (int k = 0; k < 7; ++k)
                 if (k < nb) acc(lo, hi, p, B - 1 - k);
+#endif
             B -= nb;
             A >>= 3, B >>= 3;
         } else {
+#if FGL_RANGEBOX_DYN
+            for (int k = A; k < B; ++k) acc(lo, hi, p, k);
+#else
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 if (A + k < B) acc(lo, hi, p, A + k);
+#endif
         }
     }
 }
@@ -289,6 +305,7 @@ __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, 
         parent[left >= 0 ? left : (n - 1) + ~left] = i;
         parent[right >= 0 ? right : (n - 1) + ~right] = i;
         if (i == 0) parent[0] = -1;
+#if FGL_FUSED_NODES
         if (nodes) {
             // Eq. 7 boxes of both children by the closed form (exact unions of their leaf ranges)
             float4 l0, h0, l1, h1;
@@ -304,13 +321,14 @@ __global__ void __launch_bounds__(256) k_karras(const uint64_t *__restrict__ k, 
             nd.d = make_int4(n0 <= leaf_size ? make_leaf(f, n0) : left, n1 <= leaf_size ? make_leaf(g + 1, n1) : right,
                              0, 0);
             nodes[i] = nd;
-        } else {
-            // Eq. 7 box of this node by its closed form (exact union of its leaf range)
-            float4 lo, hi;
-            range_box(L, f, last, lo, hi);
-            nodebox[2 * i] = lo;
-            nodebox[2 * i + 1] = hi;
+            return;
         }
+#endif
+        // Eq. 7 box of this node by its closed form (exact union of its leaf range)
+        float4 lo, hi;
+        range_box(L, f, last, lo, hi);
+        nodebox[2 * i] = lo;
+        nodebox[2 * i + 1] = hi;
     }
 }
 
@@ -887,14 +905,25 @@ void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
                   int cubic, int width, int quantized, cudaStream_t s, int restructure) {
     const int64_t T = b.T;
-    k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
-    FGL_LAUNCHED("k_prep");
-    launch_morton_sort(b, bits, cubic, s);
+    {
+        NvtxRange r("fgl build: A2 prep (centroids, scene box)");
+        k_prep<<<kPrepBlocks, 256, 0, s>>>(verts, V, tris, T, b.cent, b.partial, b.sync, b.box);
+        FGL_LAUNCHED("k_prep");
+    }
+    {
+        NvtxRange r("fgl build: A3-A4 Morton codes + radix sort");
+        launch_morton_sort(b, bits, cubic, s);
+    }
     const int ps = b.packed_shift, slot = b.sorted_slot;
-    // leaf-order records, leaf boxes and the 8-ary box aggregates used by the Eq. 7 boxes
-    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
-                                                          ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox, b.agg);
-    FGL_LAUNCHED("k_reorder");
+    {
+        // leaf-order records, leaf boxes and the 8-ary box aggregates used by the Eq. 7 boxes
+        NvtxRange r("fgl build: A7 leaf-order records + leaf boxes");
+        k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
+                                                              ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox,
+                                                              b.agg);
+        FGL_LAUNCHED("k_reorder");
+    }
+    NvtxRange r("fgl build: A5-A7 Karras tree, Eq. 7 boxes, traversal nodes");
     launch_tree(b, leaf_size, width, quantized, s, restructure);
 }
 

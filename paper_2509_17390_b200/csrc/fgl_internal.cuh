@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -25,6 +26,15 @@ struct Error : std::runtime_error {
     } while (0)
 
 void note_launch();  // process-wide count of libfgl kernel launches (fgl_kernel_launches)
+
+// NVTX range over a scope (host-side enqueue of a build stage or a cast; header-only NVTX v3, a no-op
+// unless a profiler injects itself) so an nsys / ncu timeline attributes device work to the call
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 #define FGL_LAUNCHED(what)                                                                              \
     do {                                                                                                \

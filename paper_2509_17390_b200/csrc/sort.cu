@@ -29,6 +29,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef FGL_SORT_ITEMS_K
 #define FGL_SORT_ITEMS_K 12
 #endif
+#ifndef FGL_SORT_WIN
+#define FGL_SORT_WIN 8  // look-back window: predecessor tiles read per round
+#endif
 #ifndef FGL_SORT_BACKOFF
 #define FGL_SORT_BACKOFF 0
 #endif
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
     // published tile counts until the nearest published inclusive prefix
     uint32_t excl = 0;
     if (tile != 0) {
-        constexpr int kWin = 8;
+        constexpr int kWin = FGL_SORT_WIN;
         int64_t t = (int64_t)tile - 1;
         bool done = false;
         while (!done) {
