@@ -754,6 +754,9 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         if a.dist_backend == "nccl":
+            # communicator set-up lines (rank count, transport) in the log, for the record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
@@ -813,8 +816,11 @@ def main():
                 scene.cast(poses_d[sl], pat, out=dict(range=out["range"][sl], tri_id=out["tri_id"][sl]))
                 comm.wait_stream(stream)
                 with torch.cuda.stream(comm):
-                    works.append(dist.all_gather_into_tensor(gather[0][c], out["range"][sl], async_op=True))
-                    works.append(dist.all_gather_into_tensor(gather[1][c], out["tri_id"][sl], async_op=True))
+                    # output viewed flat along its first dim ([world * Pc][...]): the form every backend takes
+                    works.append(dist.all_gather_into_tensor(gather[0][c].view((world * Pc,) + shape[1:]),
+                                                             out["range"][sl], async_op=True))
+                    works.append(dist.all_gather_into_tensor(gather[1][c].view((world * Pc,) + shape[1:]),
+                                                             out["tri_id"][sl], async_op=True))
             for w in works:
                 w.wait()
             stream.wait_stream(comm)
@@ -889,6 +895,28 @@ def main():
         ms, cms = t.tolist()
     clocks = clk.summary()
 
+    # --- W = N vs W = 1: the gathered results equal, bit for bit, one GPU casting every pose --------
+    gather_check = None
+    if world > 1 and (peer is not None or gather is not None):
+        if peer is not None:
+            peer.sync()
+            g_r, g_t = peer.range, peer.tri_id
+        else:
+            torch.cuda.synchronize()
+            # chunk-major gathered layout g[c][r][j] = pose r * P + c * Pc + j
+            g_r = gather[0].transpose(0, 1).reshape((world * P,) + shape[1:])
+            g_t = gather[1].transpose(0, 1).reshape((world * P,) + shape[1:])
+        if rank == 0:
+            poses_all = torch.from_numpy(np.ascontiguousarray(cfg["poses"])).to(dev)
+            ref = scene.cast(poses_all, pat)
+            torch.cuda.synchronize()
+            eq = bool(torch.equal(ref["tri_id"], g_t)) and bool(
+                torch.equal(ref["range"].view(torch.int32), g_r.view(torch.int32)))
+            gather_check = {"equal": eq, "poses": int(world * P), "mode": "fused P2P" if peer is not None else "nccl",
+                            "note": "rank 0's single-GPU cast of all W x P poses vs the gathered result, bitwise"}
+        if world > 1:
+            dist.barrier()
+
     # --- Eq. 21 counters on the same rays (COUNT variant, untimed) -> algorithmic bytes ------
     cres = scene.cast(poses_d, pat, counts=True)
     n_nodes = cres["node_counts"].double().mean().item()
@@ -912,28 +940,32 @@ def main():
 
     # --- e2e through the public API with host buffers --------------------------------------
     # Every step copies its inputs (mesh + poses) from pinned host memory, builds, casts, and reads
-    # its results back to pinned host memory. Steps are pipelined over two scenes: the upload of
-    # step i+1 (H2D copy engine) and the read-back of step i (D2H copy engine) overlap the build and
-    # cast of the neighbouring steps on the SMs.
+    # its results back to pinned host memory. Steps are pipelined over three scenes: the upload of
+    # step i+1 (H2D copy engine) and the read-back of step i (D2H copy engine, one copy per output
+    # after the whole cast) overlap the build and cast of the neighbouring steps on the SMs. Measured
+    # (tools/e2e_probe.py): 2 scenes / 8 read-back chunks 1.74 ms per step, 3 scenes / 1 chunk 1.57 ms
+    # (chunking the cast into 8 launches costs more than the overlap it buys); the PCIe bound is the
+    # 67 MB read-back at 57 GB/s, 1.18 ms (tools/pcie_bw.py).
     e2e = None
     if not a.no_e2e:
         vh = torch.from_numpy(m.verts).pin_memory()
         th = torch.from_numpy(m.tris).pin_memory()
         ph = torch.from_numpy(np.ascontiguousarray(cfg["poses_rank"])).pin_memory()
-        rh = [torch.empty(shape, dtype=torch.float32).pin_memory() for _ in range(2)]
-        ih = [torch.empty(shape, dtype=torch.int32).pin_memory() for _ in range(2)]
-        pds = [torch.empty_like(poses_d) for _ in range(2)]
+        NS = 3
+        rh = [torch.empty(shape, dtype=torch.float32).pin_memory() for _ in range(NS)]
+        ih = [torch.empty(shape, dtype=torch.int32).pin_memory() for _ in range(NS)]
+        pds = [torch.empty_like(poses_d) for _ in range(NS)]
         scs = [fgl.Scene(device=dev, leaf_size=a.leaf_size, morton_box=a.morton_box, width=a.width,
                          morton_bits=a.morton_bits, quantized=a.quantized, restructure=a.restructure)
-               for _ in range(2)]
+               for _ in range(NS)]
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         scratch = [dict(range=torch.empty(shape, dtype=torch.float32, device=dev),
-                        tri_id=torch.empty(shape, dtype=torch.int32, device=dev)) for _ in range(2)]
-        done = [None, None]
+                        tri_id=torch.empty(shape, dtype=torch.int32, device=dev)) for _ in range(NS)]
+        done = [None] * NS
 
         def e2e_steps(n):
             for i in range(n):
-                S = i % 2
+                S = i % NS
                 if done[S] is not None:
                     s_in.wait_event(done[S])  # scene S's previous read-back has finished
                 if i == 0:
@@ -945,7 +977,7 @@ def main():
                 up.record(s_in)
                 stream.wait_event(up)
                 scs[S].build()
-                done[S] = scs[S].cast_to_host(pds[S], pat, rh[S], ih[S], chunks=8, copy_stream=s_out,
+                done[S] = scs[S].cast_to_host(pds[S], pat, rh[S], ih[S], chunks=1, copy_stream=s_out,
                                               scratch=scratch[S], wait=False)
             for ev_ in done:
                 if ev_ is not None:
@@ -972,8 +1004,8 @@ def main():
         e2e = {"value": rays_rank * world / (ems / 1000), "unit": "rays/s",
                "h2d_bytes_per_step": int(m.verts.nbytes + m.tris.nbytes + cfg["poses_rank"].nbytes),
                "d2h_bytes_per_step": int(rh[0].numel() * 4 + ih[0].numel() * 4), "ms_per_step": ems,
-               "note": "pinned host in/out every step; steps pipelined over two scenes (H2D of step i+1 and "
-                       "D2H of step i overlap the build/cast on the SMs)"}
+               "note": "pinned host in/out every step; steps pipelined over three scenes (H2D of step i+1 and "
+                       "D2H of step i overlap the build/cast on the SMs); PCIe bound: the D2H at ~57 GB/s"}
         del scs
 
     cpu = None
@@ -1032,6 +1064,7 @@ def main():
             "frame_latency": latency,
             "cpu_baseline": cpu,
             "parity": parity,
+            "gather_check": gather_check,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,

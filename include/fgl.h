@@ -70,7 +70,10 @@ typedef struct {
                             is always 8-bit (0 or 1 accepted)                                  */
     int32_t restructure; /* width 2 only: 0 = plain LBVH (default); k = 1..8 passes of agglomerative
                             treelet restructuring: SAH-guided re-clustering of
-                            7-leaf treelets bottom-up, 1-triangle leaves (leaf_size ignored)     */
+                            7-leaf treelets bottom-up, 1-triangle leaves (leaf_size ignored);
+                            -k = k PARALLEL passes: treelets of <= 8 leaves over a depth
+                            partition (roots at depth = pass mod 3), all re-clustered at once in
+                            one launch per pass (no bottom-up chain), 1-triangle leaves        */
     int32_t reserved[2]; /* must be zero                                                     */
 } fgl_build_opts;
 

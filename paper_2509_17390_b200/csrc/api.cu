@@ -531,7 +531,8 @@ fgl_status fgl_scene_check(fgl_scene *s, void *stream) {
     if (*s->hflag & 1u) throw Error(FGL_E_DATA, "triangle index out of range [0, V)");
     if (*s->hflag & 2u) throw Error(FGL_E_DATA, "non-finite vertex coordinate");
     if (*s->hflag & 4u)
-        throw Error(FGL_E_DATA, "width-8 tree needs a deeper traversal stack than the cast has; casts were refused");
+        throw Error(FGL_E_DATA, "the tree needs a deeper traversal stack than the cast has (width 8, or a restructured "
+                                "tree deeper than 94 levels); casts were refused");
     FGL_API_END
 }
 
@@ -553,7 +554,7 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
         cubic = opts->morton_box == 0;
         for (int i = 0; i < 2; ++i)
             if (opts->reserved[i]) throw Error(FGL_E_USAGE, "fgl_build_opts.reserved must be zero");
-        if (opts->restructure < 0 || opts->restructure > 8) throw Error(FGL_E_USAGE, "restructure must be in [0, 8]");
+        if (opts->restructure < -8 || opts->restructure > 8) throw Error(FGL_E_USAGE, "restructure must be in [-8, 8]");
         restructure = opts->restructure;
         if (opts->morton_bits) bits = opts->morton_bits;
         if (opts->leaf_size) leaf = opts->leaf_size;

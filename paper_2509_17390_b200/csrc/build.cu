@@ -489,6 +489,102 @@ __global__ void __launch_bounds__(256) k_treelet(int32_t T, int2 *child, int32_t
     }
 }
 
+// ---- NEXT-4: parallel treelet restructuring over a depth partition ----------------------------
+// The internal nodes are partitioned into treelets: a treelet is rooted at every internal node whose
+// depth is = off (mod 3) (and at the root) and holds its descendants down to two levels below the
+// root; its leaves (<= 8) are triangles or the roots of the next treelets. A treelet's restructuring
+// changes only its own internal nodes (child links, boxes, parents of its leaves): its leaves keep
+// their subtrees and boxes and its root keeps its box, so every treelet of one pass is independent
+// and the pass is ONE launch with no bottom-up dependency chain (the sequential pass above climbs the
+// tree, ~2.7 ms at 1 M triangles). Re-clustering: the greedy agglomeration of treelet_node (merge the
+// pair with the smallest union area), kept when the treelet's internal SAH area sum drops. Passes at
+// offsets 0, 1, 2 move the treelet boundaries; depths are recomputed between passes (k_depth).
+__global__ void __launch_bounds__(128) k_treelet_par(int32_t T, int2 *child, int32_t *parent, float4 *nodebox,
+                                                     const float4 *__restrict__ leafbox,
+                                                     const int32_t *__restrict__ depth, int off) {
+    const int32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= T - 1) return;
+    if (n != 0 && depth[n] % 3 != off) return;
+    if (n == 0 && off != 0) return;
+    // gather the treelet: internal nodes I (root first), leaves L with their boxes
+    int32_t I[7], Lr[8];
+    float4 Ll[8], Lh[8];
+    int ni = 0, nl = 0;
+    int32_t q[7];
+    int qd[7], qh = 0, qt = 0;
+    q[qt] = n, qd[qt++] = 0;
+    while (qh < qt) {
+        const int32_t m = q[qh];
+        const int d = qd[qh++];
+        I[ni++] = m;
+        const int2 c = child[m];
+        const int32_t cc[2] = {c.x, c.y};
+        for (int k = 0; k < 2; ++k) {
+            const int32_t r = cc[k];
+            if (r >= 0 && d < 2) {
+                q[qt] = r, qd[qt++] = d + 1;
+            } else {
+                Lr[nl] = r;
+                if (r >= 0)
+                    Ll[nl] = nodebox[2 * (int64_t)r], Lh[nl] = nodebox[2 * (int64_t)r + 1];
+                else
+                    Ll[nl] = __ldg(leafbox + 2 * (int64_t)~r), Lh[nl] = __ldg(leafbox + 2 * (int64_t)~r + 1);
+                ++nl;
+            }
+        }
+    }
+    if (nl <= 2) return;
+    float old_cost = 0.f;
+    for (int k = 0; k < ni; ++k) old_cost += area(nodebox[2 * (int64_t)I[k]], nodebox[2 * (int64_t)I[k] + 1]);
+    // greedy agglomeration; new internal node s takes index I[s] (the last merge -> I[0] = n)
+    int32_t Wr[8];
+    float4 Wl[8], Wh[8];
+    for (int k = 0; k < nl; ++k) Wr[k] = Lr[k], Wl[k] = Ll[k], Wh[k] = Lh[k];
+    int nw = nl, slot = ni - 1;
+    int2 nc[7];
+    float4 nlo[7], nhi[7];
+    float new_cost = 0.f;
+    while (nw > 1) {
+        int bi = 0, bj = 1;
+        float bu = INFINITY;
+        for (int i = 0; i < nw; ++i)
+            for (int j = i + 1; j < nw; ++j) {
+                float4 ul = Wl[i], uh = Wh[i];
+                unite(ul, uh, Wl[j], Wh[j]);
+                const float u = area(ul, uh);
+                if (u < bu) bu = u, bi = i, bj = j;
+            }
+        float4 ml = Wl[bi], mh = Wh[bi];
+        unite(ml, mh, Wl[bj], Wh[bj]);
+        new_cost += bu;
+        nc[slot] = make_int2(Wr[bi], Wr[bj]);
+        nlo[slot] = ml, nhi[slot] = mh;
+        Wr[bi] = I[slot], Wl[bi] = ml, Wh[bi] = mh;
+        --slot;
+        --nw;
+        Wr[bj] = Wr[nw], Wl[bj] = Wl[nw], Wh[bj] = Wh[nw];
+    }
+    if (!(new_cost < old_cost * (1.f - 1e-5f))) return;
+    for (int k = 0; k < ni; ++k) {
+        const int32_t idx = I[k];
+        child[idx] = nc[k];
+        if (k > 0) nodebox[2 * (int64_t)idx] = nlo[k], nodebox[2 * (int64_t)idx + 1] = nhi[k];
+        const int32_t r0 = nc[k].x, r1 = nc[k].y;
+        parent[r0 >= 0 ? r0 : (T - 1) + ~r0] = idx;
+        parent[r1 >= 0 ? r1 : (T - 1) + ~r1] = idx;
+    }
+}
+
+// the cast's stack bound for a freely restructured binary tree: its depth + 1 (one push per level at
+// most), as the maximum over the internal nodes' depths (k_depth), into *need
+__global__ void __launch_bounds__(256) k_depth_max(int64_t n, const int32_t *__restrict__ depth, unsigned int *need) {
+    int32_t m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n - 1; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, depth[i]);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(need, (unsigned int)(m + 2));
+}
+
 // traversal nodes for single-triangle leaves from child refs and boxes (any topology)
 __global__ void __launch_bounds__(256) k_nodes_free(int64_t n, const int2 *__restrict__ child,
                                                     const float4 *__restrict__ leafbox,
@@ -825,8 +921,21 @@ static void launch_single(BuildBuffers &b, int width, cudaStream_t s) {
     }
 }
 
+// stack bound word (BuildBuffers::wctr[3]) of a restructured width-2 tree: depth + 2 from k_depth
+static void launch_stack_bound(BuildBuffers &b, cudaStream_t s) {
+    const int64_t T = b.T;
+    FGL_CUDA(cudaMemsetAsync(b.wctr + 3, 0, sizeof(unsigned int), s));
+    k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
+    FGL_LAUNCHED("k_depth");
+    k_depth_max<<<grid_for(T - 1, 256, 148 * 4), 256, 0, s>>>(T, b.depth, b.wctr + 3);
+    FGL_LAUNCHED("k_depth_max");
+}
+
 void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s, int restructure) {
     const int64_t T = b.T;
+    // a Karras tree's depth is bounded by its key and index bits (< the cast's stack): no check;
+    // restructured and width-8 trees set the bound themselves
+    if (width != 8) FGL_CUDA(cudaMemsetAsync(b.wctr + 3, 0, sizeof(unsigned int), s));
     b.width = width;
     b.quantized = width == 4 ? quantized : (width == 8 ? 1 : 0);
     b.restructured = 0;
@@ -849,6 +958,22 @@ void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaS
         launch_wide8(b, s);
         return;
     }
+    if (restructure < 0 && width == 2) {
+        // -k: k parallel treelet passes over the depth partition (offsets 0, 1, 2, 0, ...), depths
+        // recomputed before each; nodes over 1-triangle leaves
+        for (int pass = 0; pass < -restructure; ++pass) {
+            k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
+            FGL_LAUNCHED("k_depth");
+            k_treelet_par<<<(unsigned)((T - 1 + 127) / 128), 128, 0, s>>>((int32_t)T, b.child, b.parent, b.nodebox,
+                                                                           b.leafbox, b.depth, pass % 3);
+            FGL_LAUNCHED("k_treelet_par");
+        }
+        k_nodes_free<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, b.child, b.leafbox, b.nodebox, b.nodes);
+        FGL_LAUNCHED("k_nodes_free");
+        launch_stack_bound(b, s);
+        b.restructured = 1;
+        return;
+    }
     if (restructure > 0 && width == 2) {
         // costs / sizes bottom-up once, then `restructure` treelet passes; nodes over 1-triangle leaves
         for (int pass = 0; pass <= restructure; ++pass) {
@@ -860,6 +985,7 @@ void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaS
         }
         k_nodes_free<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, b.child, b.leafbox, b.nodebox, b.nodes);
         FGL_LAUNCHED("k_nodes_free");
+        launch_stack_bound(b, s);
         b.restructured = 1;
         return;
     }

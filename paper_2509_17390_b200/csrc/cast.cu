@@ -26,7 +26,9 @@ namespace {
 #define FGL_APPROX_PRE 1  // MUFU reciprocals for the per-ray slab / shear constants
 #endif
 #ifndef FGL_APPROX_NORM
-#define FGL_APPROX_NORM 0  // MUFU rsqrt for the direction normalisation (off: exact sqrt + division)
+#define FGL_APPROX_NORM 1  // MUFU rsqrt for the direction normalisation (0: exact sqrt + division); the
+                           // same in the cast and the ray export; measured max direction error 2^-21.1
+                           // either way (tools/raygen_err.py), +1% cast
 #endif
 
 #ifndef FGL_LEAF_RCP
@@ -850,8 +852,8 @@ inline bool packet_mode() {
 #define FGL_CARVEOUT 10  // k_cast_dyn shared-memory carveout in percent (-1: driver default); 5-14 measured equal
 #endif
 #ifndef FGL_DESCEND_UNROLL
-#define FGL_DESCEND_UNROLL 1  // node visits between two speculation votes (the loop form, even at 1,
-                              // schedules measurably better than a plain body: keep it)
+#define FGL_DESCEND_UNROLL 2  // node visits between two speculation votes (2: +0.5% over 1 with the
+                              // round-2 kernel; the loop form schedules better than a plain body)
 #endif
 #ifndef FGL_LDG256
 #define FGL_LDG256 1
@@ -1148,8 +1150,9 @@ __global__ void __launch_bounds__(kCastThreads, kW == 8 ? FGL_DYN8_MINBLOCKS : F
     Hit h{0.f, INT_MAX, 0, 0};
     const Node64 *__restrict__ nodes = sv.nodes;
     const Node8 *__restrict__ nodes8 = reinterpret_cast<const Node8 *>(sv.nodes4);
-    // width 8: a tree whose stack bound (k_collapse) exceeds the stack is refused, loudly
-    const bool refuse = kW == 8 && __ldg(sv.wneed) > (unsigned int)kStack8;
+    // a tree whose stack bound exceeds the stack (width 8: k_collapse; restructured width 2: its
+    // depth, k_depth_max) is refused, loudly (fgl_scene_check)
+    const bool refuse = __ldg(sv.wneed) > (unsigned int)(kW == 8 ? kStack8 : kStack);
     if (refuse && threadIdx.x == 0) atomicOr(sv.err, 4u);
     const float tmin = gen.interval_min();
     bool active = false;  // the lane's ray is still being traversed

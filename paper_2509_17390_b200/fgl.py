@@ -317,9 +317,13 @@ class Scene:
         cs = copy_stream or torch.cuda.Stream(device=dev)
         poses = _dev(poses, torch.float32, dev).reshape(-1, 3, 4)
         P = int(poses.shape[0])
-        if scratch is None:
+        own_scratch = scratch is None
+        if own_scratch:
             scratch = dict(range=torch.empty(range_out.shape, dtype=torch.float32, device=dev),
                            tri_id=torch.empty(tri_id_out.shape, dtype=torch.int32, device=dev))
+            # the copies read it on `cs`: keep the allocator from reusing it before they finish
+            scratch["range"].record_stream(cs)
+            scratch["tri_id"].record_stream(cs)
         step = max(1, -(-P // max(1, chunks)))
         for a in range(0, P, step):
             b = min(P, a + step)

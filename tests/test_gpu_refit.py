@@ -117,7 +117,7 @@ def _tree_checks(ex, T):
     return depth
 
 
-@pytest.mark.parametrize("passes", [1, 3])
+@pytest.mark.parametrize("passes", [1, 3, -1, -3, -6])  # < 0: parallel depth-partition passes
 def test_restructure_tree_valid_and_cast_parity(fgl, passes):
     cfg = synth.config("C1")
     m, pat, poses = cfg["mesh"], cfg["pattern"], cfg["poses"]
@@ -130,18 +130,21 @@ def test_restructure_tree_valid_and_cast_parity(fgl, passes):
                                   d.cpu().numpy().astype(np.float64), pat.t_min, pat.t_max, eps_rel=oracle.EPS_MODE_B)
     j = oracle.judge(vd, res["range"].reshape(-1).cpu().numpy(), res["tri_id"].reshape(-1).cpu().numpy())
     assert len(j["unamb_mismatch"]) == 0 and len(j["amb_outside"]) == 0
+    s.check()  # the stack bound of the restructured tree was met (no refused cast)
 
 
-def test_restructure_rooms_same_hits_fewer_nodes(fgl):
+@pytest.mark.parametrize("passes", [2, -3])
+def test_restructure_rooms_same_hits_fewer_nodes(fgl, passes):
     m = synth.scene_rooms(2)
     plain = fgl.Scene(m.verts, m.tris)
-    rs = fgl.Scene(m.verts, m.tris, restructure=2)
+    rs = fgl.Scene(m.verts, m.tris, restructure=passes)
     assert _tree_checks(rs.export(), m.T) < 90
     pat = synth.spinning_preset("HDL64")
     poses = synth.poses_yaw_offsets((9.0, 7.5, 1.5), 2, 0.01)
     a = plain.cast(poses, pat, counts=True)
     b = rs.cast(poses, pat, counts=True)
     assert (a["tri_id"] == b["tri_id"]).float().mean().item() > 0.9999
+    assert b["node_counts"].float().mean().item() < a["node_counts"].float().mean().item() + 1.5
     # a refit of the restructured tree keeps it exact
     v2 = _deform(m.verts, 0.02)
     rs.refit(v2)

@@ -1,5 +1,6 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck): build + casts of
-every kind + point metrics on small scenes."""
+every kind (widths 2 / 4 / 4-quantised / 8, restructured, refitted) + sort + point metrics +
+voxelizer / denoise / TSDF / marching cubes on small inputs."""
 import os
 import sys
 
@@ -29,5 +30,27 @@ k = torch.randint(0, 2 ** 62, (50000,), device="cuda", dtype=torch.int64)
 v = torch.arange(50000, device="cuda", dtype=torch.int32)
 fgl.sort_pairs(k, v, 63)
 fgl.cloud_metrics(r["hit_xyz"].reshape(-1, 3), r["hit_xyz"].reshape(-1, 3) + 0.01, 0.02)
+# round 2: the compressed 8-wide layout (SAH collapse queue + cast), quantised width 4, treelet
+# restructuring, refit, the graph-safe sort epoch (two sorts), voxelizer + masks, denoise, TSDF, MC
+s8 = fgl.Scene(soup.verts, soup.tris, width=8)
+s8.cast(cfg["poses"], cfg["pattern"])
+s8.cast_rays(o, d, 0.1, 200.0)
+s8.check()
+s4q = fgl.Scene(soup.verts, soup.tris, width=4, quantized=1)
+s4q.cast(cfg["poses"], cfg["pattern"])
+sr = fgl.Scene(soup.verts, soup.tris, restructure=1)
+sr.cast(cfg["poses"], cfg["pattern"])
+s.refit(m.verts + np.float32(0.01))
+s.cast(cfg["poses"], cfg["pattern"])
+fgl.sort_pairs(k, v, 63)
+g = synth.gaussians_random(300, 4)
+grid = synth.grid_for(g, 20)
+gs = fgl.GaussianScene(g.mu, g.quat, g.scale, g.opacity)
+vox = gs.voxelize(grid.origin, grid.h, grid.dims, 0.5, density=True)
+occ = vox["occupancy"] if isinstance(vox, dict) else vox
+dims, sp = grid.dims, (grid.h, grid.h, grid.h)
+dn = fgl.denoise(occ, dims, sp, 0.7, 0.35)
+phi = fgl.tsdf(dn if isinstance(dn, torch.Tensor) else dn["occupancy"], dims, sp, 3.0 * grid.h)
+fgl.marching_cubes(phi, grid.origin, sp, 0.0, normals=True)
 torch.cuda.synchronize()
 print("sanitize workload done")
