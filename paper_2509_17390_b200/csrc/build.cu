@@ -16,6 +16,9 @@
 #ifndef FGL_SORT_PACKED
 #define FGL_SORT_PACKED 1
 #endif
+#ifndef FGL_TREELET4
+#define FGL_TREELET4 1  // parallel restructuring: exhaustive 4-leaf treelets (0: greedy 8-leaf treelets)
+#endif
 #ifndef FGL_RANGEBOX_DYN
 #define FGL_RANGEBOX_DYN 0  // 1: Eq. 7 closed form by loops with exact trip counts (measured slower)
 #endif
@@ -575,6 +578,135 @@ __global__ void __launch_bounds__(128) k_treelet_par(int32_t T, int2 *child, int
     }
 }
 
+// Exhaustive 4-leaf treelets over a depth partition (roots at depth = off mod 2): a root n, its two
+// children and their children (the treelet leaves: triangles or the next treelets' roots). With the
+// root fixed, 4 leaves have 15 binary topologies (3 pairings 2+2, 12 of the form 1 + (1 + 2)); all
+// are costed from the 6 pair and 4 triple unions of the leaf boxes (compile-time code, registers
+// only) and the one with the smallest sum of its two non-root internal areas is kept — the root's
+// box and the leaves' subtrees are unchanged, so every treelet of a pass is independent (one
+// launch, no chain). 3-leaf treelets (one child a leaf) choose among their 3 pairings.
+__device__ __forceinline__ float4 fmin4(float4 a, float4 b) {
+    return make_float4(fminf(a.x, b.x), fminf(a.y, b.y), fminf(a.z, b.z), 0.f);
+}
+__device__ __forceinline__ float4 fmax4(float4 a, float4 b) {
+    return make_float4(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z), 0.f);
+}
+
+__global__ void __launch_bounds__(256) k_treelet4(int32_t T, int2 *child, int32_t *parent, float4 *nodebox,
+                                                  const float4 *__restrict__ leafbox,
+                                                  const int32_t *__restrict__ depth, int off) {
+    const int32_t n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= T - 1 || (depth[n] & 1) != off) return;
+    const int2 c = child[n];
+    if (c.x < 0 && c.y < 0) return;  // 2 leaves: nothing to choose
+    // leaves in fixed slots: children of c.x at 0, 1 (or c.x itself at 0), of c.y at 2, 3
+    int32_t L[4];
+    int nl;
+    int2 g0 = make_int2(0, 0), g1 = make_int2(0, 0);
+    if (c.x >= 0) g0 = child[c.x];
+    if (c.y >= 0) g1 = child[c.y];
+    auto box_of = [&](int32_t r, float4 &lo, float4 &hi) {
+        if (r >= 0)
+            lo = nodebox[2 * (int64_t)r], hi = nodebox[2 * (int64_t)r + 1];
+        else
+            lo = __ldg(leafbox + 2 * (int64_t)~r), hi = __ldg(leafbox + 2 * (int64_t)~r + 1);
+    };
+    float4 lo[4], hi[4];
+    if (c.x >= 0 && c.y >= 0) {
+        L[0] = g0.x, L[1] = g0.y, L[2] = g1.x, L[3] = g1.y;
+        nl = 4;
+    } else {  // 3 leaves: the internal child's two children and the leaf child
+        const int2 g = c.x >= 0 ? g0 : g1;
+        L[0] = g.x, L[1] = g.y, L[2] = c.x >= 0 ? c.y : c.x, L[3] = 0;
+        nl = 3;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (k < nl) box_of(L[k], lo[k], hi[k]);
+    // old: the two non-root internal nodes (4 leaves) or the one (3 leaves)
+    const int32_t ia = c.x >= 0 ? c.x : c.y;  // an internal node id to reuse
+    const int32_t ib = (c.x >= 0 && c.y >= 0) ? c.y : -1;
+    float old_cost = area(nodebox[2 * (int64_t)ia], nodebox[2 * (int64_t)ia + 1]);
+    if (ib >= 0) old_cost += area(nodebox[2 * (int64_t)ib], nodebox[2 * (int64_t)ib + 1]);
+    // pair unions
+    float pa[4][4];
+    float4 plo[4][4], phi[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i + 1; j < 4; ++j) {
+            plo[i][j] = fmin4(lo[i], lo[j]), phi[i][j] = fmax4(hi[i], hi[j]);
+            pa[i][j] = area(plo[i][j], phi[i][j]);
+        }
+    float best = old_cost;
+    int choice = -1;  // 0..2: pairing (0,1|2,3), (0,2|1,3), (0,3|1,2); 3 + 3 x + p: single x, pair p of the rest
+    if (nl == 4) {
+        const float c2[3] = {pa[0][1] + pa[2][3], pa[0][2] + pa[1][3], pa[0][3] + pa[1][2]};
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (c2[k] < best) best = c2[k], choice = k;
+        // 1 + (1 + 2): single x; triple = the other three; inner pair p of the triple
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            int o[3], m = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (k != x) o[m++] = k;
+            const float4 tlo = fmin4(plo[o[0]][o[1]], lo[o[2]]), thi = fmax4(phi[o[0]][o[1]], hi[o[2]]);
+            const float ta = area(tlo, thi);
+            const float cp[3] = {pa[o[0]][o[1]], pa[o[0]][o[2]], pa[o[1]][o[2]]};
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (ta + cp[q] < best) best = ta + cp[q], choice = 3 + 3 * x + q;
+        }
+    } else {
+        const float c3[3] = {pa[0][1], pa[0][2], pa[1][2]};
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            if (c3[k] < best) best = c3[k], choice = k;
+    }
+    if (choice < 0 || !(best < old_cost * (1.f - 1e-5f))) return;
+    auto link = [&](int32_t node, int32_t r0, int32_t r1) {
+        child[node] = make_int2(r0, r1);
+        parent[r0 >= 0 ? r0 : (T - 1) + ~r0] = node;
+        parent[r1 >= 0 ? r1 : (T - 1) + ~r1] = node;
+    };
+    auto setbox = [&](int32_t node, float4 l, float4 h) {
+        nodebox[2 * (int64_t)node] = l, nodebox[2 * (int64_t)node + 1] = h;
+    };
+    if (nl == 3) {  // pair (i, j) under ia, the third leaf beside it under n
+        const int i = choice == 2 ? 1 : 0, j = choice == 0 ? 1 : 2, r = 3 - i - j;
+        link(ia, L[i], L[j]);
+        setbox(ia, fmin4(lo[i], lo[j]), fmax4(hi[i], hi[j]));
+        link(n, ia, L[r]);
+        return;
+    }
+    if (choice < 3) {
+        const int a0 = 0, a1 = choice + 1;  // pair with leaf 0
+        int b0 = -1, b1 = -1;
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+            if (k != a1) (b0 < 0 ? b0 : b1) = k;
+        link(ia, L[a0], L[a1]);
+        setbox(ia, plo[a0][a1], phi[a0][a1]);
+        link(ib, L[b0], L[b1]);
+        setbox(ib, plo[b0][b1], phi[b0][b1]);
+        link(n, ia, ib);
+        return;
+    }
+    const int x = (choice - 3) / 3, q = (choice - 3) % 3;
+    int o[3], m = 0;
+    for (int k = 0; k < 4; ++k)
+        if (k != x) o[m++] = k;
+    const int p0 = q == 2 ? o[1] : o[0], p1 = q == 0 ? o[1] : o[2], r = o[0] + o[1] + o[2] - p0 - p1;
+    link(ib, L[p0], L[p1]);  // inner pair
+    const float4 ilo = fmin4(lo[p0], lo[p1]), ihi = fmax4(hi[p0], hi[p1]);
+    setbox(ib, ilo, ihi);
+    link(ia, ib, L[r]);  // triple
+    setbox(ia, fmin4(ilo, lo[r]), fmax4(ihi, hi[r]));
+    link(n, ia, L[x]);
+}
+
 // the cast's stack bound for a freely restructured binary tree: its depth + 1 (one push per level at
 // most), as the maximum over the internal nodes' depths (k_depth), into *need
 __global__ void __launch_bounds__(256) k_depth_max(int64_t n, const int32_t *__restrict__ depth, unsigned int *need) {
@@ -959,14 +1091,21 @@ void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaS
         return;
     }
     if (restructure < 0 && width == 2) {
-        // -k: k parallel treelet passes over the depth partition (offsets 0, 1, 2, 0, ...), depths
-        // recomputed before each; nodes over 1-triangle leaves
+        // -k: k parallel treelet passes over a depth partition, depths recomputed before each
+        // (FGL_TREELET4: exhaustive 4-leaf treelets, offsets 0, 1, 0, ...; else greedy 8-leaf
+        // treelets, offsets 0, 1, 2, 0, ...); nodes over 1-triangle leaves
         for (int pass = 0; pass < -restructure; ++pass) {
             k_depth<<<grid_for(T - 1), 256, 0, s>>>(T, b.parent, b.depth);
             FGL_LAUNCHED("k_depth");
+#if FGL_TREELET4
+            k_treelet4<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>((int32_t)T, b.child, b.parent, b.nodebox,
+                                                                        b.leafbox, b.depth, pass & 1);
+            FGL_LAUNCHED("k_treelet4");
+#else
             k_treelet_par<<<(unsigned)((T - 1 + 127) / 128), 128, 0, s>>>((int32_t)T, b.child, b.parent, b.nodebox,
                                                                            b.leafbox, b.depth, pass % 3);
             FGL_LAUNCHED("k_treelet_par");
+#endif
         }
         k_nodes_free<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>(T, b.child, b.leafbox, b.nodebox, b.nodes);
         FGL_LAUNCHED("k_nodes_free");

@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(kVoxThreads) k_voxelize(const Node64 *__restri
                 const int take = min(32, sp);
                 const int node = lane < take ? s_stack[sp - 1 - lane] : -1;
                 sp -= take;
+                __syncwarp();  // the pushes below reuse the slots just read (memory order within the warp)
                 bool ov0 = false, ov1 = false;
                 int r0 = 0, r1 = 0;
                 if (node >= 0) {

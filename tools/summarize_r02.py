@@ -49,7 +49,8 @@ def raw(rep):
 def val(d, k):
     v, u = d[k]
     x = float(v.replace(",", ""))
-    return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "nsecond": 1e-9, "msecond": 1e-3}.get(u, 1.0)
+    return x * {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "us": 1e-6, "nsecond": 1e-9, "ns": 1e-9,
+                "msecond": 1e-3, "ms": 1e-3}.get(u, 1.0)
 
 
 def main():
