@@ -84,7 +84,7 @@ void dalloc(fgl_scene *s, T **p, size_t n) {
 
 void free_build(fgl_scene *s) {
     fgl::BuildBuffers &b = s->b;
-    void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.sort_status, b.sort_tiles,
+    void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.sort_status, b.sort_tiles, b.sort_rts,
                   b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth, b.agg,
                   b.cost, b.tsize, b.cost8, b.wq, b.wctr};
     for (void *p : ps)
@@ -111,6 +111,7 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.sort_status, (size_t)256 * fgl::sort_tile_blocks(T));
     FGL_CUDA(cudaMemset(b.sort_status, 0, sizeof(uint64_t) * 256 * fgl::sort_tile_blocks(T)));
     dalloc(s, &b.sort_tiles, 16);
+    dalloc(s, &b.sort_rts, (size_t)256 * fgl::sort_tile_blocks(T));
     FGL_CUDA(cudaMemset(b.sort_tiles, 0, 16 * sizeof(uint32_t)));  // tile counters + device sort epoch
     dalloc(s, &b.tri, 3 * T);
     dalloc(s, &b.child, nin);
@@ -905,8 +906,10 @@ fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key
     FGL_CUDA(cudaMallocAsync((void **)&tiles, 16 * sizeof(uint32_t), st));
     FGL_CUDA(cudaMemsetAsync(tiles, 0, 16 * sizeof(uint32_t), st));
     FGL_CUDA(cudaMallocAsync((void **)&ghist, 8 * 256 * sizeof(uint32_t), st));
+    uint32_t *rts = nullptr;
+    FGL_CUDA(cudaMallocAsync((void **)&rts, (size_t)256 * fgl::sort_tile_blocks(n) * sizeof(uint32_t), st));
     int slot = 0;
-    fgl::radix_sort_pairs(keys, vals, k1, v1, n, key_bits, status, tiles, ghist, false, &slot, st);
+    fgl::radix_sort_pairs(keys, vals, k1, v1, n, key_bits, status, tiles, ghist, false, &slot, st, 0, rts);
     if (slot == 1) {
         FGL_CUDA(cudaMemcpyAsync(keys, k1, n * sizeof(uint64_t), cudaMemcpyDeviceToDevice, st));
         FGL_CUDA(cudaMemcpyAsync(vals, v1, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
@@ -916,6 +919,7 @@ fgl_status fgl_sort_pairs(uint64_t *keys, uint32_t *vals, int64_t n, int32_t key
     cudaFreeAsync(status, st);
     cudaFreeAsync(tiles, st);
     cudaFreeAsync(ghist, st);
+    cudaFreeAsync(rts, st);
     FGL_API_END
 }
 

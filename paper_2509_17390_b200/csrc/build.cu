@@ -1004,7 +1004,7 @@ void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s) {
     FGL_LAUNCHED("k_morton");
     int slot = 0;
     radix_sort_pairs(b.keys[0], ps ? nullptr : b.vals[0], b.keys[1], ps ? nullptr : b.vals[1], T, key_bits,
-                     b.sort_status, b.sort_tiles, b.ghist, true, &slot, s, ps);
+                     b.sort_status, b.sort_tiles, b.ghist, true, &slot, s, ps, b.sort_rts);
     b.sorted_slot = slot;
 }
 

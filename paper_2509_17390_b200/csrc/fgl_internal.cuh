@@ -105,6 +105,7 @@ struct BuildBuffers {
     uint32_t *ghist = nullptr;     // [8][256] digit histograms
     uint64_t *sort_status = nullptr;  // [nblk][256] look-back status words (epoch | flag | count)
     uint32_t *sort_tiles = nullptr;   // [16]: [0..7] per-pass tile counters, [8] device epoch counter
+    uint32_t *sort_rts = nullptr;     // [256][tiles] tile digit counts / offsets (reduce-then-scan passes)
     float4 *tri = nullptr;         // [3T] tri48 in leaf order
     int2 *child = nullptr;         // [T-1]
     int2 *range = nullptr;         // [T-1]
@@ -136,7 +137,8 @@ int sort_tile_blocks(int64_t n);
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
                       uint64_t *status, uint32_t *tile_ctr /*[16], zeroed once at allocation*/, uint32_t *ghist,
                       bool ghist_ready, int *result_slot, cudaStream_t s,
-                      int shift0 = 0);  // vals0 == nullptr: key-only passes over bits [shift0, shift0 + key_bits)
+                      int shift0 = 0,  // vals0 == nullptr: key-only passes over bits [shift0, shift0 + key_bits)
+                      uint32_t *rts = nullptr);  // [256][sort_tile_blocks(n)]: enables reduce-then-scan passes
 void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *ghist, cudaStream_t s,
                       int shift0 = 0);
 

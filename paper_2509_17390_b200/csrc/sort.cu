@@ -29,6 +29,13 @@ constexpr int kWarps = kThreads / 32;
 #ifndef FGL_SORT_ITEMS_K
 #define FGL_SORT_ITEMS_K 12
 #endif
+#ifndef FGL_SORT_RTS_MIN
+#define FGL_SORT_RTS_MIN (1 << 30)  // keys from which a pass runs reduce-then-scan instead of onesweep (measured
+                                     // no faster at 10 M keys: 110 vs 99 us per pass; off)
+#endif
+#ifndef FGL_SORT_MINB
+#define FGL_SORT_MINB 4  // resident CTAs per SM the register budget is sized for
+#endif
 #ifndef FGL_SORT_WIN
 #define FGL_SORT_WIN 8  // look-back window: predecessor tiles read per round
 #endif
@@ -61,13 +68,16 @@ __global__ void __launch_bounds__(kThreads) k_digit_hist(const uint64_t *__restr
 // counters, warps in key order); the ranked tile is staged in shared memory in digit order so the
 // global scatter writes runs of equal digits from consecutive threads (coalesced), after the
 // decoupled look-back has produced each digit's global offset.
-template <int kIt, bool kVals>
-__global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__restrict__ kin,
+// kRts (reduce-then-scan, large inputs): the tile's global digit offsets come precomputed in
+// offs[digit][tile] (k_tile_hist + k_offs_scan) instead of from the look-back; tile = blockIdx.x.
+template <int kIt, bool kVals, bool kRts = false>
+__global__ void __launch_bounds__(kThreads, FGL_SORT_MINB) k_onesweep(const uint64_t *__restrict__ kin,
                                                           const uint32_t *__restrict__ vin,
                                                           uint64_t *__restrict__ kout, uint32_t *__restrict__ vout,
                                                           int64_t n, int shift, const uint32_t *__restrict__ hist,
                                                           uint64_t *status, uint32_t *tile_ctr,
-                                                          const uint32_t *epoch_end, int pass, int npass) {
+                                                          const uint32_t *epoch_end, int pass, int npass,
+                                                          const uint32_t *__restrict__ offs = nullptr) {
     static_assert(kThreads == 256, "one thread per digit");
     constexpr int kT = kThreads * kIt, kSpan = kT / kWarps;
     __shared__ uint32_t wh[kWarps][256];
@@ -79,8 +89,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
     __shared__ uint32_t s_val[kVals ? kT : 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, d = threadIdx.x;
     // this sort's epochs are (end - npass, end]: written by k_sort_begin earlier on the stream
-    const uint32_t epoch = *epoch_end - (uint32_t)npass + 1u + (uint32_t)pass;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    const uint32_t epoch = kRts ? 0u : *epoch_end - (uint32_t)npass + 1u + (uint32_t)pass;
+    if (threadIdx.x == 0) s_tile = kRts ? blockIdx.x : atomicAdd(tile_ctr, 1u);
     for (int i = threadIdx.x; i < kWarps * 256; i += kThreads) (&wh[0][0])[i] = 0;
     // block-wide exclusive scan over the 256 digits (one value per thread)
     auto scan256 = [&](uint32_t v) -> uint32_t {
@@ -96,7 +106,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
         __syncthreads();  // s_wsum may be reused by the next scan
         return off + x - v;
     };
-    s_base[d] = scan256(hist[d]);  // digit bases from the all-pass histogram
+    if constexpr (!kRts) s_base[d] = scan256(hist[d]);  // digit bases from the all-pass histogram
+    __syncthreads();
     const uint32_t tile = s_tile;
     const uint32_t lt = (1u << lane) - 1u;
     const int64_t base = (int64_t)tile * kT + (int64_t)w * kSpan;
@@ -126,12 +137,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
         wh[ww][d] = cnt;
         cnt += c;
     }
-    const uint64_t ep = (uint64_t)epoch << 32;
-    // status words carry their own payload, so relaxed (L2-coherent) accesses suffice
-    cuda::atomic_ref<uint64_t, cuda::thread_scope_device> mine(status[(int64_t)tile * 256 + d]);
-    mine.store(ep | (tile == 0 ? kPrefix : kAgg) | cnt, cuda::std::memory_order_relaxed);
-    const uint32_t tstart = scan256(cnt);
+    const uint32_t tstart = [&]() {
+        if constexpr (kRts) {
+            return scan256(cnt);
+        } else {
+            const uint64_t ep = (uint64_t)epoch << 32;
+            // status words carry their own payload, so relaxed (L2-coherent) accesses suffice
+            cuda::atomic_ref<uint64_t, cuda::thread_scope_device> mine(status[(int64_t)tile * 256 + d]);
+            mine.store(ep | (tile == 0 ? kPrefix : kAgg) | cnt, cuda::std::memory_order_relaxed);
+            return scan256(cnt);
+        }
+    }();
     s_tstart[d] = tstart;
+    if constexpr (kRts) {
+        s_base[d] = offs[(int64_t)d * gridDim.x + tile] - tstart;  // global start of digit d in this tile
+    } else {
     // decoupled look-back: kWin predecessors per round (independent loads in flight), accumulating
     // published tile counts until the nearest published inclusive prefix
     uint32_t excl = 0;
@@ -163,9 +183,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
             if (!done && t == t0) __nanosleep(FGL_SORT_BACKOFF);  // predecessor not yet published: yield issue slots
 #endif
         }
-        mine.store(ep | kPrefix | (excl + cnt), cuda::std::memory_order_relaxed);
+        cuda::atomic_ref<uint64_t, cuda::thread_scope_device> mine(status[(int64_t)tile * 256 + d]);
+        mine.store(((uint64_t)epoch << 32) | kPrefix | (excl + cnt), cuda::std::memory_order_relaxed);
     }
     s_base[d] += excl - tstart;  // global position = s_base[digit] + staged position
+    }
     __syncthreads();
     // stage the tile in digit order
 #pragma unroll
@@ -188,6 +210,64 @@ __global__ void __launch_bounds__(kThreads, 4) k_onesweep(const uint64_t *__rest
         if constexpr (kVals) vout[pos] = s_val[p];
     }
 }
+// Reduce-then-scan pass, step 1: the digit histogram of every tile (same tile layout as k_onesweep),
+// stored digit-major: thist[digit][tile].
+template <int kIt>
+__global__ void __launch_bounds__(kThreads) k_tile_hist(const uint64_t *__restrict__ kin, int64_t n, int shift,
+                                                       uint32_t *__restrict__ thist) {
+    constexpr int kT = kThreads * kIt;
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kT;
+#pragma unroll
+    for (int i = 0; i < kIt; ++i) {
+        const int64_t idx = base + i * kThreads + threadIdx.x;
+        if (idx < n) atomicAdd(&h[(kin[idx] >> shift) & 0xFF], 1u);
+    }
+    __syncthreads();
+    thist[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = h[threadIdx.x];
+}
+
+// Reduce-then-scan pass, step 2: one CTA per digit d turns its row of tile counts into the tiles'
+// global start positions, in place: offs[d][t] = (keys with a smaller digit) + (keys with digit d in
+// tiles before t). The digit base comes from the all-pass histogram.
+__global__ void __launch_bounds__(kThreads) k_offs_scan(uint32_t *__restrict__ thist, int ntiles,
+                                                       const uint32_t *__restrict__ hist) {
+    __shared__ uint32_t s_w[kWarps];
+    __shared__ uint32_t s_carry;
+    const int d = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // digit base: sum of hist[0..d)
+    uint32_t b = threadIdx.x < (unsigned)d ? hist[threadIdx.x] : 0u;
+    for (int o = 16; o; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (lane == 0) s_w[w] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int k = 0; k < kWarps; ++k) t += s_w[k];
+        s_carry = t;
+    }
+    __syncthreads();
+    uint32_t *row = thist + (int64_t)d * ntiles;
+    for (int c0 = 0; c0 < ntiles; c0 += kThreads) {
+        const int t = c0 + threadIdx.x;
+        const uint32_t v = t < ntiles ? row[t] : 0u;
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        uint32_t off = s_carry;
+        for (int k = 0; k < w; ++k) off += s_w[k];
+        if (t < ntiles) row[t] = off + x - v;
+        __syncthreads();
+        if (threadIdx.x == kThreads - 1) s_carry = off + x;
+        __syncthreads();
+    }
+}
+
 // Per-sort setup on the stream: zero the per-pass tile counters and reserve npass fresh epochs
 // (ctl[8] = the last epoch of this sort; epoch 0 marks never-written status words and is skipped
 // at wrap-around).
@@ -215,7 +295,7 @@ void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *g
 
 void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_t *vals1, int64_t n, int key_bits,
                       uint64_t *status, uint32_t *tile_ctr, uint32_t *ghist, bool ghist_ready,
-                      int *result_slot, cudaStream_t s, int shift0) {
+                      int *result_slot, cudaStream_t s, int shift0, uint32_t *rts) {
     *result_slot = 0;
     if (n <= 1) return;
     if (n >= (int64_t)kValMask) throw Error(1, "radix sort: n must be < 2^30");
@@ -229,7 +309,32 @@ void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_
     uint64_t *k[2] = {keys0, keys1};
     uint32_t *v[2] = {vals0, vals1};
     int cur = 0;
+    // large inputs: reduce-then-scan passes (no look-back chain across thousands of tiles)
+    const bool use_rts = rts != nullptr && n >= (int64_t)FGL_SORT_RTS_MIN;
     for (int p = 0; p < npass; ++p) {
+        if (use_rts) {
+            const int sh = shift0 + 8 * p;
+            if (kv) {
+                k_tile_hist<kItemsKV><<<nblk, kThreads, 0, s>>>(k[cur], n, sh, rts);
+                FGL_LAUNCHED("k_tile_hist");
+                k_offs_scan<<<256, kThreads, 0, s>>>(rts, (int)nblk, ghist + 256 * p);
+                FGL_LAUNCHED("k_offs_scan");
+                k_onesweep<kItemsKV, true, true><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n,
+                                                                           sh, ghist + 256 * p, status, tile_ctr + p,
+                                                                           tile_ctr + 8, p, npass, rts);
+            } else {
+                k_tile_hist<kItemsK><<<nblk, kThreads, 0, s>>>(k[cur], n, sh, rts);
+                FGL_LAUNCHED("k_tile_hist");
+                k_offs_scan<<<256, kThreads, 0, s>>>(rts, (int)nblk, ghist + 256 * p);
+                FGL_LAUNCHED("k_offs_scan");
+                k_onesweep<kItemsK, false, true><<<nblk, kThreads, 0, s>>>(k[cur], nullptr, k[cur ^ 1], nullptr, n,
+                                                                           sh, ghist + 256 * p, status, tile_ctr + p,
+                                                                           tile_ctr + 8, p, npass, rts);
+            }
+            FGL_LAUNCHED("k_onesweep");
+            cur ^= 1;
+            continue;
+        }
         if (kv)
             k_onesweep<kItemsKV, true><<<nblk, kThreads, 0, s>>>(k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], n,
                                                                  shift0 + 8 * p, ghist + 256 * p, status,

@@ -189,3 +189,23 @@ def test_width8_refit(fgl):
     cfg2["mesh"] = synth.Mesh(v2, m.tris)
     v, rng_, tid, _ = _mode_b(fgl, cfg2, 10 ** 9, 0, scene=s)
     _parity(v, rng_, tid, label="C1 refit width 8")
+
+
+def test_width8_hit_points_counts_and_determinism(fgl):
+    """Optional outputs of the width-8 cast: hit points x* = o + t d, the Eq. 21 counters,
+    and bitwise determinism across casts."""
+    cfg = synth.config("C1")
+    m, pat, poses = cfg["mesh"], cfg["pattern"], cfg["poses"]
+    s = fgl.Scene(m.verts, m.tris, width=8)
+    r = s.cast(poses, pat, hit_xyz=True, counts=True)
+    r2 = s.cast(poses, pat)
+    assert np.array_equal(r["range"].cpu().numpy().view(np.int32), r2["range"].cpu().numpy().view(np.int32))
+    assert np.array_equal(r["tri_id"].cpu().numpy(), r2["tri_id"].cpu().numpy())
+    o, d = fgl.export_rays(pat, poses)
+    rng = r["range"].reshape(-1).cpu().numpy().astype(np.float64)
+    x = r["hit_xyz"].reshape(-1, 3).cpu().numpy().astype(np.float64)
+    exp = o.cpu().numpy().astype(np.float64) + rng[:, None] * d.cpu().numpy().astype(np.float64)
+    assert np.allclose(x, exp, rtol=0, atol=1e-5 + 1e-6 * np.abs(exp).max())
+    nc = r["node_counts"].cpu().numpy()
+    assert nc.min() >= 1 and nc.mean() < 20  # wide nodes: few visits per ray on C1
+    assert r["tri_counts"].cpu().numpy().min() >= 1
