@@ -666,6 +666,12 @@ __global__ void __launch_bounds__(256) k_treelet4(int32_t T, int2 *child, int32_
             if (c3[k] < best) best = c3[k], choice = k;
     }
     if (choice < 0 || !(best < old_cost * (1.f - 1e-5f))) return;
+    // runtime slot picks by select chains (an array indexed at run time would live in local memory)
+    auto pick = [&](int i, float4 &l, float4 &h, int32_t &r) {
+        l = i == 0 ? lo[0] : (i == 1 ? lo[1] : (i == 2 ? lo[2] : lo[3]));
+        h = i == 0 ? hi[0] : (i == 1 ? hi[1] : (i == 2 ? hi[2] : hi[3]));
+        r = i == 0 ? L[0] : (i == 1 ? L[1] : (i == 2 ? L[2] : L[3]));
+    };
     auto link = [&](int32_t node, int32_t r0, int32_t r1) {
         child[node] = make_int2(r0, r1);
         parent[r0 >= 0 ? r0 : (T - 1) + ~r0] = node;
@@ -674,37 +680,37 @@ __global__ void __launch_bounds__(256) k_treelet4(int32_t T, int2 *child, int32_
     auto setbox = [&](int32_t node, float4 l, float4 h) {
         nodebox[2 * (int64_t)node] = l, nodebox[2 * (int64_t)node + 1] = h;
     };
+    float4 l0, h0, l1, h1, l2, h2, l3, h3;
+    int32_t r0, r1, r2, r3;
     if (nl == 3) {  // pair (i, j) under ia, the third leaf beside it under n
         const int i = choice == 2 ? 1 : 0, j = choice == 0 ? 1 : 2, r = 3 - i - j;
-        link(ia, L[i], L[j]);
-        setbox(ia, fmin4(lo[i], lo[j]), fmax4(hi[i], hi[j]));
-        link(n, ia, L[r]);
+        pick(i, l0, h0, r0), pick(j, l1, h1, r1), pick(r, l2, h2, r2);
+        link(ia, r0, r1);
+        setbox(ia, fmin4(l0, l1), fmax4(h0, h1));
+        link(n, ia, r2);
         return;
     }
-    if (choice < 3) {
-        const int a0 = 0, a1 = choice + 1;  // pair with leaf 0
-        int b0 = -1, b1 = -1;
-#pragma unroll
-        for (int k = 1; k < 4; ++k)
-            if (k != a1) (b0 < 0 ? b0 : b1) = k;
-        link(ia, L[a0], L[a1]);
-        setbox(ia, plo[a0][a1], phi[a0][a1]);
-        link(ib, L[b0], L[b1]);
-        setbox(ib, plo[b0][b1], phi[b0][b1]);
+    if (choice < 3) {  // 2 + 2: leaf 0 with leaf choice + 1, the other two together
+        const int a1 = choice + 1, b0 = a1 == 1 ? 2 : 1, b1 = a1 == 3 ? 2 : 3;
+        pick(0, l0, h0, r0), pick(a1, l1, h1, r1), pick(b0, l2, h2, r2), pick(b1, l3, h3, r3);
+        link(ia, r0, r1);
+        setbox(ia, fmin4(l0, l1), fmax4(h0, h1));
+        link(ib, r2, r3);
+        setbox(ib, fmin4(l2, l3), fmax4(h2, h3));
         link(n, ia, ib);
         return;
     }
+    // 1 + (1 + 2): single x; the others o0 < o1 < o2; inner pair q of them
     const int x = (choice - 3) / 3, q = (choice - 3) % 3;
-    int o[3], m = 0;
-    for (int k = 0; k < 4; ++k)
-        if (k != x) o[m++] = k;
-    const int p0 = q == 2 ? o[1] : o[0], p1 = q == 0 ? o[1] : o[2], r = o[0] + o[1] + o[2] - p0 - p1;
-    link(ib, L[p0], L[p1]);  // inner pair
-    const float4 ilo = fmin4(lo[p0], lo[p1]), ihi = fmax4(hi[p0], hi[p1]);
+    const int o0 = x == 0 ? 1 : 0, o1 = x <= 1 ? 2 : 1, o2 = x <= 2 ? 3 : 2;
+    const int p0 = q == 2 ? o1 : o0, p1 = q == 0 ? o1 : o2, r = o0 + o1 + o2 - p0 - p1;
+    pick(p0, l0, h0, r0), pick(p1, l1, h1, r1), pick(r, l2, h2, r2), pick(x, l3, h3, r3);
+    link(ib, r0, r1);  // inner pair
+    const float4 ilo = fmin4(l0, l1), ihi = fmax4(h0, h1);
     setbox(ib, ilo, ihi);
-    link(ia, ib, L[r]);  // triple
-    setbox(ia, fmin4(ilo, lo[r]), fmax4(ihi, hi[r]));
-    link(n, ia, L[x]);
+    link(ia, ib, r2);  // triple
+    setbox(ia, fmin4(ilo, l2), fmax4(ihi, h2));
+    link(n, ia, r3);
 }
 
 // the cast's stack bound for a freely restructured binary tree: its depth + 1 (one push per level at

@@ -11,6 +11,8 @@
 // counter lives in device memory and is advanced by k_sort_begin on the stream, so a sort captured
 // in a CUDA graph gets fresh epochs on every replay (a host-side epoch would be baked into the
 // graph and let a replay accept the previous replay's status words).
+#include <cstdlib>
+
 #include <cuda/atomic>
 
 #include "fgl_internal.cuh"
@@ -310,7 +312,10 @@ void radix_sort_pairs(uint64_t *keys0, uint32_t *vals0, uint64_t *keys1, uint32_
     uint32_t *v[2] = {vals0, vals1};
     int cur = 0;
     // large inputs: reduce-then-scan passes (no look-back chain across thousands of tiles)
-    const bool use_rts = rts != nullptr && n >= (int64_t)FGL_SORT_RTS_MIN;
+    // FGL_SORT_RTS_MIN (environment) overrides the compiled threshold: A/B runs and the test of the path
+    int64_t rts_min = (int64_t)FGL_SORT_RTS_MIN;
+    if (const char *e = getenv("FGL_SORT_RTS_MIN")) rts_min = atoll(e);
+    const bool use_rts = rts != nullptr && n >= rts_min;
     for (int p = 0; p < npass; ++p) {
         if (use_rts) {
             const int sh = shift0 + 8 * p;

@@ -244,3 +244,33 @@ def test_morton_primitive_matches_oracle(fgl):
     for bits in (1, 7, 10, 21):
         g = fgl.morton_codes(torch.from_numpy(pts).cuda(), lo, hi, bits).cpu().numpy().view(np.uint64)
         assert np.array_equal(g, oracle.morton(pts, lo, hi, bits))
+
+
+def test_sort_reduce_then_scan_path_matches_oracle():
+    """The reduce-then-scan pass variant of the radix sort (off by default; forced here through
+    FGL_SORT_RTS_MIN) gives the same stable order as the oracle, key-value and packed key-only
+    (the latter through a full LBVH build compared with the default build)."""
+    import os
+    import subprocess
+    import sys
+    ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = r'''
+import numpy as np, torch, oracle, synth, paper_2509_17390_b200 as fgl
+rng = np.random.default_rng(3)
+n = 300_001
+keys = rng.integers(0, 2 ** 40, n, dtype=np.int64).astype(np.uint64)
+keys[::7] = keys[1::7][: len(keys[::7])]  # duplicates: stability matters
+vals = np.arange(n, dtype=np.uint32)
+k, v = fgl.sort_pairs(torch.from_numpy(keys.view(np.int64)).cuda(), torch.from_numpy(vals.view(np.int32)).cuda(), 40)
+ok_, ov_ = oracle.stable_sort(keys, vals)
+assert np.array_equal(k.cpu().numpy().view(np.uint64), ok_) and np.array_equal(v.cpu().numpy().view(np.uint32), ov_)
+m = synth.soup(200_003, seed=9)
+e = fgl.Scene(m.verts, m.tris).export()
+import hashlib
+print("OK", hashlib.sha256(e["sorted_keys"].tobytes() + e["nodes"].tobytes() + e["tri48"].tobytes()).hexdigest())
+'''
+    env = dict(os.environ, FGL_SORT_RTS_MIN="1")
+    r1 = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT, timeout=600)
+    assert r1.returncode == 0 and "OK" in r1.stdout, r1.stderr[-2000:]
+    r0 = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT, timeout=600)
+    assert r0.returncode == 0 and r0.stdout == r1.stdout, (r0.stdout, r1.stdout)
