@@ -900,6 +900,9 @@ struct LaneStackN {
     }
 };
 
+#ifndef FGL_FLAT_VISIT
+#define FGL_FLAT_VISIT 0  // 1: branch-light node visit (selects, idle lanes re-read the root)
+#endif
 #ifndef FGL_LEAF_HANDOFF
 #define FGL_LEAF_HANDOFF 0  // 1: both children hit, near one a leaf: postpone it, descend the far one (no stack op)
 #endif
@@ -939,7 +942,35 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
 #pragma unroll
         for (int u = 0; u < FGL_DESCEND_UNROLL; ++u) {  // nodes per warp vote
         go = active && cur >= 0 && cur != kDone;
+#if FGL_FLAT_VISIT
+        {
+            // flat visit: every lane runs the node visit (idle lanes re-read the root, L1-resident, and
+            // discard it), decisions by selects; the pops are the only divergent branches
+            float4 na, nb, nc, ndf;
+            ldg_node(nodes + (go ? cur : 0), na, nb, nc, ndf);
+            const int32_t c0 = __float_as_int(ndf.x), c1 = __float_as_int(ndf.y);
+            if (kCount && go) ++h.nodes;
+            float t0, t1;
+            const bool h0 = slab_sel<OCT>(p, na.x, na.y, na.z, na.w, nc.x, nc.y, tmin, h.t, t0) && go;
+            const bool h1 = slab_sel<OCT>(p, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, tmin, h.t, t1) && go;
+            const bool swap = h1 && (!h0 || t1 < t0);  // the nearer hit child is c1
+            const int32_t nearc = swap ? c1 : c0, farc = swap ? c0 : c1;
+            if (h0 && h1) st.push(sp, ((uint64_t)__float_as_uint(swap ? t0 : t1) << 32) | (uint32_t)farc);
+            if (h0 || h1) cur = nearc;
+            bool need = go && !(h0 || h1);
+            if ((h0 || h1) && nearc < 0 && leaf == 0) leaf = nearc, need = true;
+            if (need) {
+                cur = pop_live(st, sp, tlim);
+                if (cur < 0 && leaf == 0) {
+                    leaf = cur;
+                    cur = pop_live(st, sp, tlim);
+                }
+            }
+        }
+        if (false) {
+#else
         if (go) {
+#endif
             float4 na, nb, nc, ndf;
             ldg_node(nodes + cur, na, nb, nc, ndf);
             const int4 nd = make_int4(__float_as_int(ndf.x), __float_as_int(ndf.y), 0, 0);
@@ -1429,6 +1460,7 @@ void launch_cast_rosette(const SceneView &sv, const RosetteParams &p, const floa
 void launch_cast_rays(const SceneView &sv, const float *orig, const float *dir, int64_t R, float t_min, float t_max,
                       const CastOut &o, CastCounter *ctr, cudaStream_t s) {
     RaysGen g{orig, dir, R, t_min, t_max};
+    if ((R + 31) / 32 >= (int64_t(1) << 31)) throw Error(1, "explicit-ray cast: more than 2^31 ray tiles in one call");
     launch_persistent(sv, g, (R + 31) / 32, o, ctr, s);
 }
 
