@@ -345,7 +345,8 @@ def run_reference(a):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": _describe(cfg, P, 1), "sample_rays_per_step": n, "triangles": m.T},
             "cpu_baseline": {"value": v, "unit": "rays/s", "cores": oracle.threads(), "kind": "oracle",
-                             "sample": f"{n} seeded rays per step of {a.config} pose 0 vs all {m.T} triangles"},
+                             "sample": f"{n} seeded rays per step of {a.config} pose 0 vs all {m.T} triangles",
+                             "host": _host_cpu()},
             "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
