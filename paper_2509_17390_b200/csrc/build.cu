@@ -6,7 +6,8 @@
 //   reorder  : triangle records (tri48) gathered into sorted (leaf) order
 //   karras   : Eq. 6 LCP-split binary radix tree, one thread per internal node,
 //              "bitwise operations ... without recursion"
-//   refit    : Eq. 7 bottom-up union with atomic arrival counters
+//   refit    : Eq. 7 by its closed form: each node's box is the exact union of its
+//              sorted leaf range, read from 8-ary box aggregates (no bottom-up climb)
 //   nodes    : traversal nodes (both child boxes per node; subtrees of <= leaf_size triangles
 //              become leaves), laid out in Karras (Morton) order ("Morton order").
 #include <cuda/atomic>
