@@ -47,6 +47,7 @@ def _args():
     ap.add_argument("--morton-bits", type=int, default=0, help="b of Eq. 5 (0 = library default)")
     ap.add_argument("--quantized", type=int, default=0, help="width 4 only: 8-bit child boxes (node64q)")
     ap.add_argument("--restructure", type=int, default=0, help="treelet restructuring passes (NEXT-4, width 2)")
+    ap.add_argument("--treelets", type=int, default=0, help="1: bottom-up 4-leaf treelets inside the build (width 2)")
     ap.add_argument("--morton-box", type=int, default=0, help="0 = cubic (R22, default), 1 = per-axis (Eq. 5)")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--gather", choices=["fused", "nccl", "none"], default="fused",
@@ -771,7 +772,7 @@ def main():
     poses_d = torch.from_numpy(np.ascontiguousarray(cfg["poses_rank"])).to(dev)
     stream = torch.cuda.current_stream()
     scene = fgl.Scene(verts_d, tris_d, device=dev, leaf_size=a.leaf_size, morton_box=a.morton_box, width=a.width,
-                      morton_bits=a.morton_bits, quantized=a.quantized, restructure=a.restructure)
+                      morton_bits=a.morton_bits, quantized=a.quantized, restructure=a.restructure, treelets=a.treelets)
     out = scene.cast(poses_d, pat)
     shape = tuple(out["range"].shape)
     gather = None
@@ -957,7 +958,7 @@ def main():
         ih = [torch.empty(shape, dtype=torch.int32).pin_memory() for _ in range(NS)]
         pds = [torch.empty_like(poses_d) for _ in range(NS)]
         scs = [fgl.Scene(device=dev, leaf_size=a.leaf_size, morton_box=a.morton_box, width=a.width,
-                         morton_bits=a.morton_bits, quantized=a.quantized, restructure=a.restructure)
+                         morton_bits=a.morton_bits, quantized=a.quantized, restructure=a.restructure, treelets=a.treelets)
                for _ in range(NS)]
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
         scratch = [dict(range=torch.empty(shape, dtype=torch.float32, device=dev),

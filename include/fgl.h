@@ -74,7 +74,14 @@ typedef struct {
                             -k = k PARALLEL passes: treelets of <= 8 leaves over a depth
                             partition (roots at depth = pass mod 3), all re-clustered at once in
                             one launch per pass (no bottom-up chain), 1-triangle leaves        */
-    int32_t reserved[2]; /* must be zero                                                     */
+    int32_t treelets;    /* width 2, restructure 0: 1 = optimise every 4-leaf treelet bottom-up
+                            INSIDE the fused build (each node, as it completes, re-links its <= 4
+                            grandchildren into the lowest-SAH of the 3 / 15 binary topologies;
+                            after Karras & Aila 2013 at treelet size 4): a better tree for the
+                            cast at almost no build cost; leaves keep <= leaf_size triangles, the
+                            scene counts as restructured (range[] of re-linked nodes is not a
+                            leaf interval). 0 = the Eq. 6 Karras tree (default)               */
+    int32_t reserved[1]; /* must be zero                                                     */
 } fgl_build_opts;
 
 typedef struct {

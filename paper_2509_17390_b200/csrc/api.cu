@@ -86,7 +86,7 @@ void free_build(fgl_scene *s) {
     fgl::BuildBuffers &b = s->b;
     void *ps[] = {b.cent, b.box, b.partial, b.sync, b.keys[0], b.keys[1], b.vals[0], b.vals[1], b.ghist, b.sort_status, b.sort_tiles, b.sort_rts,
                   b.tri, b.child, b.range, b.parent, b.flags, b.leafbox, b.nodebox, b.nodes, b.nodes4, b.depth, b.agg,
-                  b.cost, b.tsize, b.cost8, b.wq, b.wctr};
+                  b.cost, b.tsize, b.cost8, b.wq, b.wctr, b.gslot, b.lbvh_up};
     for (void *p : ps)
         if (p) cudaFree(p);
     b = fgl::BuildBuffers();
@@ -133,6 +133,15 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.cost8, 8 * nin);
     dalloc(s, &b.wq, T);
     dalloc(s, &b.wctr, 4);
+    dalloc(s, &b.gslot, nin);
+    FGL_CUDA(cudaMemset(b.gslot, 0, nin * sizeof(unsigned long long)));  // epoch 0 is never a build's
+    {
+        const size_t ub = fgl::lbvh_up_bytes(T);
+        char *u = nullptr;
+        dalloc(s, &u, ub);
+        FGL_CUDA(cudaMemset(u, 0, ub));  // arrival counters start at 0 and reset themselves
+        b.lbvh_up = u;
+    }
 }
 
 fgl::SceneView view(const fgl_scene *s) {
@@ -545,7 +554,8 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     // default b (R7): 10 bits per axis (30-bit keys, four sort passes) below 4 M primitives, where
     // the cubic cells are already finer than the primitives; 13 above (the 10 M-triangle terrain
     // loses 7% cast speed at b = 10)
-    int bits = s->T < (int64_t(1) << 22) ? 10 : 13, leaf = 2, cubic = 1, width = 2, quant = 0, restructure = 0;
+    int bits = s->T < (int64_t(1) << 22) ? 10 : 13, leaf = 2, cubic = 1, width = 2, quant = 0, restructure = 0,
+        treelets = 0;
     if (opts) {
         if (opts->quantized < 0 || opts->quantized > 1) throw Error(FGL_E_USAGE, "quantized must be 0 or 1");
         quant = opts->quantized;
@@ -553,8 +563,9 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
         if (width != 2 && width != 4 && width != 8) throw Error(FGL_E_USAGE, "width must be 2, 4 or 8");
         if (opts->morton_box < 0 || opts->morton_box > 1) throw Error(FGL_E_USAGE, "morton_box must be 0 or 1");
         cubic = opts->morton_box == 0;
-        for (int i = 0; i < 2; ++i)
-            if (opts->reserved[i]) throw Error(FGL_E_USAGE, "fgl_build_opts.reserved must be zero");
+        if (opts->reserved[0]) throw Error(FGL_E_USAGE, "fgl_build_opts.reserved must be zero");
+        if (opts->treelets < 0 || opts->treelets > 1) throw Error(FGL_E_USAGE, "treelets must be 0 or 1");
+        treelets = opts->treelets;
         if (opts->restructure < -8 || opts->restructure > 8) throw Error(FGL_E_USAGE, "restructure must be in [-8, 8]");
         restructure = opts->restructure;
         if (opts->morton_bits) bits = opts->morton_bits;
@@ -574,10 +585,12 @@ fgl_status fgl_scene_build(fgl_scene *s, const fgl_build_opts *opts, void *strea
     if (s->gauss) {
         if (width != 2 || quant) throw Error(FGL_E_USAGE, "a Gaussian scene builds width-2 nodes only");
         if (!cubic) throw Error(FGL_E_USAGE, "a Gaussian scene uses the cubic Morton box");
+        if (restructure || treelets) throw Error(FGL_E_USAGE, "a Gaussian scene builds the plain Karras tree");
         fgl::launch_gauss_build(s->verts, s->g_quat, s->g_scale, s->g_opac, s->kappa, s->b, bits, leaf, st);
     } else {
         if (restructure && width != 2) throw Error(FGL_E_USAGE, "restructure needs width 2");
-        fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, quant, st, restructure);
+        if (treelets && (width != 2 || restructure)) throw Error(FGL_E_USAGE, "treelets needs width 2, restructure 0");
+        fgl::launch_build(s->verts, s->V, s->tris, s->b, bits, leaf, cubic, width, quant, st, restructure, treelets);
     }
     if (timed) FGL_CUDA(cudaEventRecord(s->ev1, st));
     s->built = true;
@@ -827,6 +840,13 @@ fgl_status fgl_scene_export(const fgl_scene *s, const fgl_export *out, void *str
     if (!out) throw Error(FGL_E_USAGE, "out is NULL");
     DeviceGuard g(s->dev);
     cudaStream_t st = (cudaStream_t)stream;
+    if (!s->gauss && (out->leaf_box || out->node_box)) {
+        // the fused build stores only the boxes a sibling needs: derive them all (exact unions over
+        // the current tree; tri48 is regathered identically), so the export is right after any build,
+        // refit or graph replay — the scene's traversal data do not change
+        fgl_scene *m = const_cast<fgl_scene *>(s);
+        fgl::launch_complete_boxes(m->verts, m->V, m->tris, m->b, st);
+    }
     FGL_CUDA(cudaStreamSynchronize(st));
     const int64_t T = s->T, nin = std::max<int64_t>(T - 1, 0);
     const fgl::BuildBuffers &b = s->b;

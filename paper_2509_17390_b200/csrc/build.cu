@@ -10,6 +10,8 @@
 //              sorted leaf range, read from 8-ary box aggregates (no bottom-up climb)
 //   nodes    : traversal nodes (both child boxes per node; subtrees of <= leaf_size triangles
 //              become leaves), laid out in Karras (Morton) order ("Morton order").
+#include <cstdlib>
+
 #include <cuda/atomic>
 
 #include "fgl_internal.cuh"
@@ -22,6 +24,9 @@
 #endif
 #ifndef FGL_RANGEBOX_DYN
 #define FGL_RANGEBOX_DYN 0  // 1: Eq. 7 closed form by loops with exact trip counts (measured slower)
+#endif
+#ifndef FGL_FUSED_LBVH
+#define FGL_FUSED_LBVH 1  // width 2: one bottom-up kernel for leaf records, tree, boxes and node64 (k_lbvh)
 #endif
 #ifndef FGL_FUSED_NODES
 #define FGL_FUSED_NODES 0  // 1: k_karras writes the binary traversal nodes (no separate k_nodes pass)
@@ -45,6 +50,27 @@ __global__ void k_validate(const float *__restrict__ verts, int64_t V, const int
 
 // vertex gather with the index clamped to [0, V) (memory-safe before validation is checked)
 __device__ __forceinline__ int32_t clampv(int32_t i, int64_t V) { return i < 0 ? 0 : (i >= V ? (int32_t)(V - 1) : i); }
+
+// 12-byte rows by one 8-byte and one 4-byte load (row i starts 8-byte aligned iff i is even; the base
+// is cudaMalloc-aligned)
+__device__ __forceinline__ float3 ldv2(const float *__restrict__ verts, int32_t i) {
+    const float *p = verts + 3 * (int64_t)i;
+    if (i & 1) {
+        const float2 yz = __ldg(reinterpret_cast<const float2 *>(p + 1));
+        return make_float3(__ldg(p), yz.x, yz.y);
+    }
+    const float2 xy = __ldg(reinterpret_cast<const float2 *>(p));
+    return make_float3(xy.x, xy.y, __ldg(p + 2));
+}
+__device__ __forceinline__ int3 ldtri(const int32_t *__restrict__ tris, int64_t k) {
+    const int32_t *p = tris + 3 * k;
+    if (k & 1) {
+        const int2 yz = __ldg(reinterpret_cast<const int2 *>(p + 1));
+        return make_int3(__ldg(p), yz.x, yz.y);
+    }
+    const int2 xy = __ldg(reinterpret_cast<const int2 *>(p));
+    return make_int3(xy.x, xy.y, __ldg(p + 2));
+}
 
 __device__ __forceinline__ float3 ldv(const float *__restrict__ verts, int32_t i) {
     return make_float3(__ldg(verts + 3 * (int64_t)i), __ldg(verts + 3 * (int64_t)i + 1), __ldg(verts + 3 * (int64_t)i + 2));
@@ -110,7 +136,7 @@ __global__ void __launch_bounds__(256) k_prep(const float *__restrict__ verts, i
             v = i < 3 ? warp_min(v) : warp_max(v);
             if (lane == 0) box[i] = v;
         }
-        if (lane == 0) *sync = 0u;
+        if (lane == 0) *sync = 0u, sync[2] = 0u, sync[3] += 1u;  // k_lbvh: [2] pending count, [3] slot epoch
     }
 }
 
@@ -173,6 +199,8 @@ __global__ void __launch_bounds__(256) k_morton(const float4 *__restrict__ cent,
     __syncthreads();
     const int npass = (3 * bits + 7) / 8;
     const MortonBox m = mb;
+    // (warp-aggregating the digit counts — one atomic when the whole warp shares a digit, or per
+    // match_any group — measured slower: 115-120 vs 87 us at 10 M keys)
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < T; k += (int64_t)gridDim.x * blockDim.x) {
         float4 c = cent[k];
         uint64_t code = morton_code(m, c.x, c.y, c.z);
@@ -817,6 +845,707 @@ __global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const i
     nodes[i] = nd;
 }
 
+// ---- fused A2 leaf records + A5 Karras tree + A6 Eq. 7 boxes + A7 node64 (width 2, default build) --
+// The binary radix tree of Eq. 6 has one internal node per adjacent pair of sorted keys:
+// the node split at g (between leaves g and g + 1) covers the maximal run of leaves around g whose
+// adjacent LCPs delta(k, k + 1) all exceed delta(g, g + 1). A node covering [l, r] is therefore the
+// LEFT child of the node split at r when delta(r, r + 1) > delta(l - 1, l), else the RIGHT child of
+// the node split at l - 1 (never equal for distinct augmented keys; delta = -1 outside [0, n)).
+// That makes the tree buildable bottom-up with the boxes (after Apetrei 2014): every leaf climbs;
+// at a parent the first child to arrive deposits its box and far endpoint and stops, the second
+// unites both boxes — Eq. 7, exact min/max — writes the parent's node64 and climbs on.
+// Karras's numbering is kept (an internal node is indexed by its right endpoint if it is a left
+// child, by its left endpoint if a right child, the root is 0), so a node split at g has children
+// g and g + 1 and child / range / parent / node64 are bit-identical to k_karras + k_nodes.
+// One CTA per kChunk consecutive leaves, one thread per leaf: parents whose split lies inside the
+// chunk meet in shared memory; a node whose parent's range leaves the chunk (the chunk boundaries'
+// ancestors, a few per chunk) meets its sibling through a global slot per split — an epoch-tagged
+// exchange of the far endpoint, the boxes passed through nodebox / leafbox, fenced. Leaf records
+// (tri48) are gathered here in leaf order; leaf and node boxes are stored only where a sibling needs
+// them (all_boxes = 1 stores them all; the scene export fills them in on demand otherwise).
+#ifndef FGL_LBVH_CHUNK
+#define FGL_LBVH_CHUNK 256
+#endif
+constexpr int kChunk = FGL_LBVH_CHUNK;  // leaves (= threads) per k_lbvh CTA
+constexpr int kSlotEmpty = -1, kSlotDone = -2;
+constexpr int kMaxRounds = 100;  // > the depth of a Karras tree (delta strictly grows downwards, < 96)
+
+struct Box6 {
+    float lx, ly, lz, hx, hy, hz;
+};
+
+__device__ __forceinline__ Box6 box_union(const Box6 &a, const Box6 &b) {
+    return Box6{fminf(a.lx, b.lx), fminf(a.ly, b.ly), fminf(a.lz, b.lz),
+                fmaxf(a.hx, b.hx), fmaxf(a.hy, b.hy), fmaxf(a.hz, b.hz)};
+}
+__device__ __forceinline__ float box_area(const Box6 &b) {  // half surface area (SAH weight)
+    const float dx = b.hx - b.lx, dy = b.hy - b.ly, dz = b.hz - b.lz;
+    return dx * dy + dy * dz + dz * dx;
+}
+// lo.w carries the node's height in the traversal tree (treelet builds; 0 otherwise)
+__device__ __forceinline__ void box_store(float4 *p, const Box6 &b, int h = 0) {
+    p[0] = make_float4(b.lx, b.ly, b.lz, __int_as_float(h));
+    p[1] = make_float4(b.hx, b.hy, b.hz, 0.f);
+}
+__device__ __forceinline__ Box6 box_load_cg(const float4 *p, int &h) {
+    const float4 l = __ldcg(p), hi = __ldcg(p + 1);
+    h = __float_as_int(l.w);
+    return Box6{l.x, l.y, l.z, hi.x, hi.y, hi.z};
+}
+
+// delta(i, i + 1) of the augmented keys (R7), -1 when the pair leaves [0, n)
+__device__ __forceinline__ int adj_delta(const uint64_t *__restrict__ k, int n, int i, int ks) {
+    if (i < 0 || i + 1 >= n) return -1;
+    const uint64_t x = (__ldg(k + i) ^ __ldg(k + i + 1)) >> ks;
+    return x ? __clzll((long long)x) : 64 + __clz(i ^ (i + 1));
+}
+
+struct LbvhOut {
+    int2 *child, *range;
+    int32_t *parent;
+    float4 *leafbox, *nodebox;
+    Node64 *nodes;
+    unsigned long long *gslot;
+    unsigned int *wneed;  // treelet builds: the traversal-stack bound (height + margin), by the root
+    int n, leaf_size, all_boxes;
+    uint32_t epoch;
+};
+
+// one child of an internal node: child-array ref (internal index / ~leaf), node64 ref (internal
+// index / make_leaf(first, count) when the subtree holds <= leaf_size triangles), box, height in
+// the traversal tree (0 for node64 leaves)
+struct Kid {
+    int32_t c, nr;
+    Box6 b;
+    int h;
+};
+
+__device__ __forceinline__ Kid kid_of(const LbvhOut &o, int32_t c, int first, int count, const Box6 &b, int h) {
+    return Kid{c, (c < 0 || count <= o.leaf_size) ? make_leaf(first, count) : c, b, (c < 0 || count <= o.leaf_size) ? 0 : h};
+}
+
+// write internal node K with children a (slot 0) and b (slot 1): node64, child links, parents
+__device__ __forceinline__ void put_kids(const LbvhOut &o, int K, const Kid &a, const Kid &b) {
+    o.child[K] = make_int2(a.c, b.c);
+    o.parent[a.c >= 0 ? a.c : (o.n - 1) + ~a.c] = K;
+    o.parent[b.c >= 0 ? b.c : (o.n - 1) + ~b.c] = K;
+    if (K == 0) o.parent[0] = -1;
+    Node64 nd;
+    nd.a = make_float4(a.b.lx, a.b.hx, a.b.ly, a.b.hy);
+    nd.b = make_float4(b.b.lx, b.b.hx, b.b.ly, b.b.hy);
+    nd.c = make_float4(a.b.lz, a.b.hz, b.b.lz, b.b.hz);
+    nd.d = make_int4(a.nr, b.nr, 0, 0);
+    o.nodes[K] = nd;
+}
+
+// internal node K = split g over leaves [l, r], children boxes a (left) and b (right), heights ha, hb
+__device__ __forceinline__ void put_node(const LbvhOut &o, int K, int g, int l, int r, const Box6 &a, const Box6 &b,
+                                         int ha = 0, int hb = 0) {
+    const int32_t left = l == g ? ~g : g, right = r == g + 1 ? ~(g + 1) : g + 1;
+    o.range[K] = make_int2(l, r);
+    put_kids(o, K, kid_of(o, left, l, g - l + 1, a, ha), kid_of(o, right, g + 1, r - g, b, hb));
+}
+
+// treelet builds: height of node [l, r] seen by the traversal (0 when it is a node64 leaf)
+__device__ __forceinline__ int trav_height(const LbvhOut &o, int l, int r, int h) {
+    return r - l + 1 <= o.leaf_size ? 0 : h;
+}
+
+// climb from the complete node [l, r] (boundary LCPs dl, dr; height h) through global slots until
+// this thread arrives first somewhere or completes the root
+template <bool kTreelet>
+__device__ __forceinline__ void lbvh_global_climb(const LbvhOut &o, const uint64_t *__restrict__ keys, int ks, int l,
+                                                  int r, int dl, int dr, Box6 box, int h, bool published) {
+    while (true) {
+        const bool left = dr > dl;
+        const int gp = left ? r : l - 1;
+        if (!published)
+            box_store(l == r ? o.leafbox + 2 * (int64_t)l : o.nodebox + 2 * (int64_t)(left ? r : l), box,
+                      kTreelet ? trav_height(o, l, r, h) : 0);
+        published = false;
+        // release this node's box, acquire the sibling's (the first arrival released its own)
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> slot(o.gslot[gp]);
+        const unsigned long long old = slot.exchange(((unsigned long long)o.epoch << 32) | (uint32_t)(left ? l : r),
+                                                     cuda::std::memory_order_acq_rel);
+        if ((uint32_t)(old >> 32) != o.epoch) return;  // first to arrive: the sibling completes gp
+        const int other = (int)(uint32_t)old;
+        const int sl = left ? gp + 1 : other, sr = left ? other : gp;
+        int hs;
+        const Box6 sib = box_load_cg(sl == sr ? o.leafbox + 2 * (int64_t)sl : o.nodebox + 2 * (int64_t)(left ? gp + 1 : gp), hs);
+        const int hm = kTreelet ? trav_height(o, l, r, h) : 0;
+        const Box6 &A = left ? box : sib, &B = left ? sib : box;
+        const int L = left ? l : other, R = left ? other : r;
+        dl = adj_delta(keys, o.n, L - 1, ks);
+        dr = adj_delta(keys, o.n, R, ks);
+        const bool root = dl < 0 && dr < 0;
+        const Box6 u = box_union(A, B);
+        put_node(o, root ? 0 : (dr > dl ? R : L), gp, L, R, A, B, left ? hm : hs, left ? hs : hm);
+        h = 1 + max(hm, hs);
+        if (root) {
+            box_store(o.nodebox, u, h);
+            if (kTreelet) *o.wneed = (unsigned int)(h + 1 + 3);  // + 3: refit may split <= 8-triangle leaves
+            return;
+        }
+        box = u, l = L, r = R;
+    }
+}
+
+constexpr int32_t kNone = INT32_MIN;  // k_lbvh staging: no entry
+
+// boxes in shared memory as six planes (conflict-free for nearby indices; a 24-byte struct array
+// takes 2-way bank conflicts on every field)
+struct BoxRef {
+    float *p;
+    __device__ __forceinline__ operator Box6() const {
+        return Box6{p[0], p[kChunk], p[2 * kChunk], p[3 * kChunk], p[4 * kChunk], p[5 * kChunk]};
+    }
+    __device__ __forceinline__ BoxRef &operator=(const Box6 &b) {
+        p[0] = b.lx, p[kChunk] = b.ly, p[2 * kChunk] = b.lz, p[3 * kChunk] = b.hx, p[4 * kChunk] = b.hy,
+        p[5 * kChunk] = b.hz;
+        return *this;
+    }
+};
+struct BoxArr {
+    float v[6 * kChunk];
+    __device__ __forceinline__ BoxRef operator[](int i) { return BoxRef{v + i}; }
+};
+
+// k_lbvh shared memory (dynamic: > 48 KB with the treelet records)
+template <bool kTreelet>
+struct LbvhSmem {
+    int sdelta[kChunk + 1];   // delta(c0 + i - 1, c0 + i), i = 0..cnt
+    int sslot[kChunk];        // split c0 + s: first arrival's far endpoint / empty / done
+    int wn[kMaxRounds + 1];   // wn[k]: nodes completed in round k - 1
+    int spar_int[kChunk];     // staged parent of internal node c0 + i
+    int spar_leaf[kChunk];    // staged parent of leaf c0 + i
+    int sheight[kTreelet ? kChunk : 1];  // internal node c0 + i: height
+    BoxArr slbox;             // leaf c0 + i
+    BoxArr snbox;             // internal node c0 + i, once complete
+    int2 schild[kChunk];      // staged child refs of internal node c0 + i (kNone: not completed here)
+    int2 srange[kChunk];      // staged leaf range of internal node c0 + i
+    int2 wl[2][kChunk];       // round work lists: (l, r) of completed nodes
+    int smark[kChunk];        // position p starts an output unit ending at smark[p] (kNone: no)
+    int swarp[kChunk / 32 + 1];
+    int4 sref[kTreelet ? kChunk : 1];  // internal node c0 + i: (child refs, node64 refs)
+};
+
+// ---- levels above the chunks ----------------------------------------------------------------------
+// Every chunk's nodes whose parent spans a chunk boundary ("units": maximal subtrees inside the
+// chunk, they tile it) are emitted in leaf order; kGroup consecutive chunks form a group one level
+// up, whose last CTA to finish (arrival counter) builds the tree over the group's units in shared
+// memory exactly as over leaves — units play the leaves, the LCP across a unit boundary is the
+// adjacent-key delta there — and emits its own units, and so on until one group holds everything
+// and completes the root. A segment with more than kUnitCap units (or a group with more than
+// kChunk) sends its units to the global pending list instead (k_lbvh_top climbs those through the
+// global slots), and everything above it follows ("poisoned"), so both paths never meet in one node.
+constexpr int kUnitCap = 64;
+constexpr int kGroup = 8;
+constexpr int kMaxLevels = 8;
+struct Unit {
+    int4 m;  // (a, b, height, 0): leaves [a, b]
+    float4 lo, hi;
+};
+struct UpPlan {
+    Unit *units[kMaxLevels];          // level i: nseg[i] segments x kUnitCap units
+    int *cnt[kMaxLevels];             // level i, per segment: unit count, -1 = poisoned
+    unsigned int *ctr[kMaxLevels];    // level i >= 1, per group: arrivals of its level i-1 segments
+    int nseg[kMaxLevels];
+    int nlev;                         // nseg[nlev - 1] == 1
+    int force_global;                 // test hook FGL_LBVH_GLOBAL: 1 = every chunk's units go to the global
+                                      // list, 2 = every odd chunk's, 4 = every odd group's (levels >= 1)
+};
+
+// segment counts per level and the carve-up of BuildBuffers::lbvh_up (bytes: lbvh_up_bytes)
+static UpPlan lbvh_plan(int64_t T, void *base) {
+    UpPlan up{};
+    up.nseg[0] = (int)((T + kChunk - 1) / kChunk);
+    up.nlev = 1;
+    while (up.nseg[up.nlev - 1] > 1) {
+        if (up.nlev == kMaxLevels) throw Error(1, "lbvh: too many levels");
+        up.nseg[up.nlev] = (up.nseg[up.nlev - 1] + kGroup - 1) / kGroup;
+        ++up.nlev;
+    }
+    char *p = static_cast<char *>(base);
+    auto take = [&](size_t bytes) {
+        char *q = p;
+        p += (bytes + 255) & ~size_t(255);
+        return q;
+    };
+    for (int i = 0; i < up.nlev; ++i) {
+        up.ctr[i] = reinterpret_cast<unsigned int *>(take(sizeof(unsigned int) * up.nseg[i]));  // zeroed once
+        up.cnt[i] = reinterpret_cast<int *>(take(sizeof(int) * up.nseg[i]));
+        up.units[i] = i + 1 < up.nlev ? reinterpret_cast<Unit *>(take(sizeof(Unit) * kUnitCap * (size_t)up.nseg[i])) : nullptr;
+    }
+    if (base == nullptr) up.units[0] = reinterpret_cast<Unit *>(p);  // size query: end pointer
+    return up;
+}
+
+
+// a unit whose parent will be built by the global climb: publish its box where the sibling looks
+// (Karras index by side) and list it for k_lbvh_top
+template <bool kTreelet>
+__device__ __forceinline__ void lbvh_push_global(const LbvhOut &o, const uint64_t *__restrict__ keys, int ks,
+                                                 const Unit &u, int4 *pend, unsigned int *pend_n) {
+    const int l = u.m.x, r = u.m.y;
+    const int dl = adj_delta(keys, o.n, l - 1, ks), dr = adj_delta(keys, o.n, r, ks);
+    float4 *dst = l == r ? o.leafbox + 2 * (int64_t)l : o.nodebox + 2 * (int64_t)(dr > dl ? r : l);
+    dst[0] = make_float4(u.lo.x, u.lo.y, u.lo.z, __int_as_float(kTreelet ? trav_height(o, l, r, u.m.z) : 0));
+    dst[1] = u.hi;
+    pend[atomicAdd(pend_n, 1u)] = make_int4(l, r, u.m.z, 0);
+}
+
+// Write the marked units (smark[p] = end position, p < P) of segment `seg` at level `lev` in
+// position order (block-wide rank by ballots), or poison the segment and push them to the global
+// list when they do not fit (or when `poison` is set). All threads of the CTA call this.
+template <bool kTreelet, class UnitOf>
+__device__ void lbvh_emit(const LbvhOut &o, const uint64_t *__restrict__ keys, int ks, const UpPlan &up, int lev,
+                          int seg, int P, const int *smark, int *swarp, UnitOf unit_of, int4 *pend,
+                          unsigned int *pend_n, bool poison = false) {
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const bool has = t < P && smark[t] != kNone;
+    const unsigned bal = __ballot_sync(0xffffffffu, has);
+    if (lane == 0) swarp[w] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+        const int c = swarp[k];
+        before += k < w ? c : 0;
+        total += c;
+    }
+    const int rank = before + __popc(bal & ((1u << lane) - 1u));
+    const bool bad = poison || total > kUnitCap;
+    if (has) {
+        const Unit u = unit_of(t, smark[t]);
+        if (bad)
+            lbvh_push_global<kTreelet>(o, keys, ks, u, pend, pend_n);
+        else
+            up.units[lev][(int64_t)seg * kUnitCap + rank] = u;
+    }
+    if (t == 0) up.cnt[lev][seg] = bad ? -1 : total;
+    __syncthreads();  // swarp / smark reuse
+}
+
+// The levels above the chunks (see UpPlan). Called by every CTA after its segment is emitted at
+// level 0; the last CTA of each group goes on up.
+template <bool kTreelet>
+__device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys, int ks, const UpPlan &up, int seg,
+                            LbvhSmem<kTreelet> &S, int4 *pend, unsigned int *pend_n) {
+    __shared__ int s_last, s_off[kGroup + 1], s_poison;
+    const int t = threadIdx.x, n = o.n;
+    for (int lev = 1; lev < up.nlev; ++lev) {
+        const int group = seg / kGroup, first = group * kGroup, gsize = min(kGroup, up.nseg[lev - 1] - first);
+        __syncthreads();  // this segment's units / count written (by several threads)
+        if (t == 0) {
+            __threadfence();  // release them (cumulative over the barrier) before the arrival
+            s_last = atomicAdd(up.ctr[lev] + group, 1u) == (unsigned)(gsize - 1);
+            if (s_last) up.ctr[lev][group] = 0;  // self-resetting for the next build
+        }
+        __syncthreads();
+        if (!s_last) return;
+        if (t == 0) __threadfence();  // acquire the group's segments (the barrier below spreads it)
+        __syncthreads();
+        seg = group;
+        if (t == 0) {
+            int off = 0, poison = 0;
+            for (int k = 0; k < gsize; ++k) {
+                const int c = __ldcg(up.cnt[lev - 1] + first + k);
+                s_off[k] = off;
+                if (c < 0) poison = 1;
+                off += max(c, 0);
+            }
+            s_off[gsize] = off;
+            s_poison = poison || off > kChunk || ((up.force_global & 4) && (group & 1));
+        }
+        __syncthreads();
+        const int m = s_off[gsize];
+        // units of the group in order: position v -> segment k, index v - s_off[k]
+        auto load_unit = [&](int v) -> Unit {
+            int k = 0;
+            while (v >= s_off[k + 1]) ++k;
+            const Unit *src = up.units[lev - 1] + (int64_t)(first + k) * kUnitCap + (v - s_off[k]);
+            Unit r;
+            r.m = __ldcg(&src->m), r.lo = __ldcg(&src->lo), r.hi = __ldcg(&src->hi);
+            return r;
+        };
+        if (s_poison) {  // everything here climbs globally (m may exceed the CTA); the segment above is poisoned
+            for (int v = t; v < m; v += blockDim.x) lbvh_push_global<kTreelet>(o, keys, ks, load_unit(v), pend, pend_n);
+            if (lev + 1 < up.nlev && t == 0) up.cnt[lev][seg] = -1;
+            continue;
+        }
+        Unit u{};
+        if (t < m) u = load_unit(t);
+        // shared-memory tree over the m units (same scheme as over leaves; unit u plays leaf u)
+        int *const sdelta = S.sdelta, *const sslot = S.sslot, *const wn = S.wn, *const smark = S.smark;
+        int *const uh = S.spar_int;  // unit heights
+        int *const nh = S.spar_leaf;  // node heights (stored like the boxes)
+        BoxArr &ubox = S.slbox, &nbox = S.snbox;
+        int2 *const uab = S.schild;   // unit leaf ranges
+        int2 (*const wl)[kChunk] = S.wl;
+        sslot[t] = kSlotEmpty, smark[t] = kNone;
+        if (t <= kMaxRounds) wn[t] = 0;
+        if (t < m) {
+            uab[t] = make_int2(u.m.x, u.m.y);
+            uh[t] = u.m.z;
+            ubox[t] = Box6{u.lo.x, u.lo.y, u.lo.z, u.hi.x, u.hi.y, u.hi.z};
+            sdelta[t] = adj_delta(keys, n, u.m.x - 1, ks);
+            if (t == m - 1) sdelta[m] = adj_delta(keys, n, u.m.y, ks);
+        }
+        __syncthreads();
+        int count = m;
+        for (int round = 0; count > 0; ++round) {
+            if (t < count) {
+                int U = t, W = t;
+                if (round > 0) {
+                    const int2 e = wl[round & 1][t];
+                    U = e.x, W = e.y;
+                }
+                const int dl = sdelta[U], dr = sdelta[W + 1];
+                if (dl >= 0 || dr >= 0) {
+                    const bool left = dr > dl;
+                    const int gs = left ? W : U - 1;  // the gap between units gs and gs + 1
+                    if (gs < 0 || gs > m - 2) {
+                        smark[U] = W;
+                    } else {
+                        int other;
+                        asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;"
+                                     : "=r"(other)
+                                     : "r"((uint32_t)__cvta_generic_to_shared(&sslot[gs])), "r"(left ? U : W)
+                                     : "memory");
+                        if (other != kSlotEmpty) {
+                            sslot[gs] = kSlotDone;
+                            const int U2 = left ? U : other, W2 = left ? other : W;
+                            const int L = uab[U2].x, R = uab[W2].y, g = uab[gs].y;  // leaves; split after leaf g
+                            const Box6 A = U2 == gs ? ubox[gs] : nbox[gs];
+                            const Box6 B = W2 == gs + 1 ? ubox[gs + 1] : nbox[gs + 1];
+                            int ha = 0, hb = 0;
+                            if (kTreelet) {
+                                ha = trav_height(o, L, g, U2 == gs ? uh[gs] : nh[gs]);
+                                hb = trav_height(o, g + 1, R, W2 == gs + 1 ? uh[gs + 1] : nh[gs + 1]);
+                            }
+                            const int dlp = sdelta[U2], drp = sdelta[W2 + 1];
+                            const bool root = dlp < 0 && drp < 0;
+                            const Box6 bu = box_union(A, B);
+                            put_node(o, root ? 0 : (drp > dlp ? R : L), g, L, R, A, B, ha, hb);
+                            const int q = root ? 0 : (drp > dlp ? W2 : U2);
+                            nbox[q] = bu;
+                            const int hh = 1 + max(ha, hb);
+                            if (kTreelet) nh[q] = hh;
+                            if (root) {
+                                box_store(o.nodebox, bu, kTreelet ? hh : 0);
+                                if (kTreelet) *o.wneed = (unsigned int)(hh + 1 + 3);
+                            }
+                            wl[(round + 1) & 1][atomicAdd(&wn[round + 1], 1)] = make_int2(U2, W2);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            count = wn[round + 1];
+        }
+        if (t < m - 1) {
+            const int f = sslot[t];
+            if (f >= 0) {
+                if (f <= t)
+                    smark[f] = t;
+                else
+                    smark[t + 1] = f;
+            }
+        }
+        __syncthreads();
+        if (lev + 1 >= up.nlev) return;  // the top group: the root is complete
+        auto unit_of = [&](int p, int e) -> Unit {
+            const int dl = sdelta[p], dr = sdelta[e + 1];
+            const int q = p == e ? p : (dr > dl ? e : p);
+            const Box6 bx = p == e ? ubox[p] : nbox[q];
+            const int hh = p == e ? uh[p] : (kTreelet ? nh[q] : 0);
+            return Unit{make_int4(uab[p].x, uab[e].y, hh, 0), make_float4(bx.lx, bx.ly, bx.lz, 0.f),
+                        make_float4(bx.hx, bx.hy, bx.hz, 0.f)};
+        };
+        lbvh_emit<kTreelet>(o, keys, ks, up, lev, seg, m, smark, S.swarp, unit_of, pend, pend_n);
+    }
+}
+
+// kTreelet: after a node completes in shared memory, the treelet of its <= 4 grandchildren is
+// re-linked into the lowest-SAH of its binary topologies (3 with 3 leaves, 15 with 4: the 3
+// balanced pairings and 12 chains; Karras & Aila 2013's exhaustive treelet search at size 4, done
+// bottom-up inside the build) — the node keeps its index and box, its internal children keep
+// their indices. The subtree leaf ranges stop being contiguous (range[] is kept for the treelet
+// roots only; the scene is marked restructured).
+template <bool kTreelet>
+__global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : (kChunk <= 256 ? 6 : 3)) k_lbvh(const float *__restrict__ verts, int64_t V,
+                                                 const int32_t *__restrict__ tris, const uint32_t *__restrict__ perm,
+                                                 const uint64_t *__restrict__ keys, int ks, uint64_t pmask,
+                                                 float4 *__restrict__ tri, LbvhOut o, int4 *__restrict__ pend,
+                                                 unsigned int *pend_n, UpPlan up) {
+    extern __shared__ __align__(16) unsigned char lbvh_smem[];
+    LbvhSmem<kTreelet> &S = *reinterpret_cast<LbvhSmem<kTreelet> *>(lbvh_smem);
+    int *const sdelta = S.sdelta, *const sslot = S.sslot, *const wn = S.wn, *const sheight = S.sheight;
+    int *const spar_int = S.spar_int, *const spar_leaf = S.spar_leaf, *const smark = S.smark;
+    BoxArr &slbox = S.slbox, &snbox = S.snbox;
+    int4 *const sref = S.sref;
+    int2 *const schild = S.schild, *const srange = S.srange;
+    int2 (*const wl)[kChunk] = S.wl;
+    const int n = o.n, t = threadIdx.x, c0 = blockIdx.x * kChunk, cnt = min(kChunk, n - c0), j = c0 + t;
+    sslot[t] = kSlotEmpty;
+    if (t <= kMaxRounds) wn[t] = 0;
+    schild[t] = make_int2(kNone, kNone);
+    spar_int[t] = kNone, spar_leaf[t] = kNone, smark[t] = kNone;
+    // staged parent links: child ref c (internal index or ~leaf, both inside the chunk) -> idx
+    auto stage_parent = [&](int32_t c, int idx) {
+        if (c >= 0)
+            spar_int[c - c0] = idx;
+        else
+            spar_leaf[~c - c0] = idx;
+    };
+    Box6 box{};
+    if (t < cnt) {
+        const uint64_t key = __ldg(keys + j);
+        const uint32_t k = perm ? __ldg(perm + j) : (uint32_t)(key & pmask);
+        const int3 ti = ldtri(tris, (int64_t)k);
+        const float3 a = ldv2(verts, clampv(ti.x, V)), b = ldv2(verts, clampv(ti.y, V)), c = ldv2(verts, clampv(ti.z, V));
+        tri[3 * (int64_t)j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
+        tri[3 * (int64_t)j + 1] = make_float4(b.x, b.y, b.z, 0.f);
+        tri[3 * (int64_t)j + 2] = make_float4(c.x, c.y, c.z, 0.f);
+        box = Box6{fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)),
+                   fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z))};
+        slbox[t] = box;
+        if (o.all_boxes) box_store(o.leafbox + 2 * (int64_t)j, box);
+        sdelta[t] = adj_delta(keys, n, j - 1, ks);
+        if (t == cnt - 1) sdelta[cnt] = adj_delta(keys, n, j, ks);
+    }
+    __syncthreads();
+    // phase 1, bottom-up in rounds: round k holds the nodes completed in round k - 1 (round 0: the
+    // leaves), compacted onto the first threads, so the climb runs on dense warps; two children meet
+    // at their parent's split slot in shared memory, the second completes the parent.
+    int count = cnt;
+    for (int round = 0; count > 0; ++round) {
+        if (t < count) {
+            int l = j, r = j;
+            if (round > 0) {
+                const int2 e = wl[round & 1][t];
+                l = e.x, r = e.y;
+            }
+            const int dl = sdelta[l - c0], dr = sdelta[r + 1 - c0];
+            if (dl >= 0 || dr >= 0) {  // not the root
+                const bool left = dr > dl;
+                const int gp = left ? r : l - 1;
+                if (gp < c0 || gp > c0 + cnt - 2) {  // split on a chunk boundary: an output unit
+                    smark[l - c0] = r - c0;
+                } else {
+                    const int s = gp - c0;
+                    // release this node's box / refs (stored at completion), acquire the sibling's
+                    int other;
+                    asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;"
+                                 : "=r"(other)
+                                 : "r"((uint32_t)__cvta_generic_to_shared(&sslot[s])), "r"(left ? l : r)
+                                 : "memory");
+                    if (other != kSlotEmpty) {  // second to arrive: complete the parent
+                        sslot[s] = kSlotDone;
+                        int h = 0;
+                        const int L = left ? l : other, R = left ? other : r;
+                        // both children: [L, gp] and [gp + 1, R]
+                        const Box6 A = L == gp ? slbox[L - c0] : snbox[gp - c0];
+                        const Box6 B = R == gp + 1 ? slbox[R - c0] : snbox[gp + 1 - c0];
+                        const int dlp = sdelta[L - c0], drp = sdelta[R + 1 - c0];
+                        const bool root = dlp < 0 && drp < 0;
+                        const int K = root ? 0 : (drp > dlp ? R : L);
+                        const Box6 u = box_union(A, B);
+                        srange[K - c0] = make_int2(L, R);
+                        if (K == 0) spar_int[0] = -1;
+                        if constexpr (kTreelet) {
+                            const int32_t cl = L == gp ? ~gp : gp, cr = R == gp + 1 ? ~(gp + 1) : gp + 1;
+                            // children: refs, node64 refs (leaf_size collapse), heights; boxes stay in smem
+                            const int nl = gp - L + 1, nrr = R - gp;
+                            const bool ia = cl >= 0 && nl > o.leaf_size, ib = cr >= 0 && nrr > o.leaf_size;
+                            const int32_t ncl = ia ? cl : make_leaf(L, nl), ncr = ib ? cr : make_leaf(gp + 1, nrr);
+                            const int hcl = ia ? sheight[cl - c0] : 0, hcr = ib ? sheight[cr - c0] : 0;
+                            auto boxof = [&](int32_t c) -> Box6 { return c >= 0 ? (Box6)snbox[c - c0] : (Box6)slbox[~c - c0]; };
+                            auto hof = [&](int32_t c, int32_t nr) -> int { return nr >= 0 ? sheight[c - c0] : 0; };
+                            // internal node idx takes children (ca, na, ha) and (cb, nb, hb): staged links,
+                            // record, box (children's boxes re-read: a child re-linked just before is current)
+                            auto link = [&](int idx, int32_t ca, int32_t na, int ha, int32_t cb, int32_t nb, int hb) {
+                                schild[idx - c0] = make_int2(ca, cb);
+                                stage_parent(ca, idx);
+                                stage_parent(cb, idx);
+                                sref[idx - c0] = make_int4(ca, cb, na, nb);
+                                snbox[idx - c0] = box_union(boxof(ca), boxof(cb));
+                                sheight[idx - c0] = 1 + max(ha, hb);
+                            };
+                            auto sel4 = [](int i, int v0, int v1, int v2, int v3) { return i == 0 ? v0 : (i == 1 ? v1 : (i == 2 ? v2 : v3)); };
+                            int choice = -1;  // -1: keep the Karras topology
+                            int xc0 = 0, xc1 = 0, xc2 = 0, xc3 = 0, xn0 = 0, xn1 = 0, xn2 = 0, xn3 = 0;
+                            if (ia || ib) {
+                                // treelet leaves: x0, x1 under the left child (or the left child), x2, x3 likewise
+                                const int4 ra = ia ? sref[cl - c0] : make_int4(cl, cl, ncl, ncl);
+                                const int4 rb = ib ? sref[cr - c0] : make_int4(cr, cr, ncr, ncr);
+                                xc0 = ra.x, xc1 = ra.y, xn0 = ra.z, xn1 = ra.w, xc2 = rb.x, xc3 = rb.y, xn2 = rb.z, xn3 = rb.w;
+                                if (!(ia && ib)) {
+                                    // 3 leaves y0 y1 y2 (the leaf child at lc): chains only, w alone, the others paired
+                                    if (!ia) xc1 = xc2, xn1 = xn2, xc2 = xc3, xn2 = xn3;  // y = (leaf, x2, x3)
+                                    const Box6 y0 = boxof(xc0), y1 = boxof(xc1), y2 = boxof(xc2);
+                                    const int lc = ia ? 2 : 0;
+                                    const float a01 = box_area(box_union(y0, y1)), a02 = box_area(box_union(y0, y2)),
+                                                a12 = box_area(box_union(y1, y2));
+                                    float best = (lc == 2 ? a01 : a12) * 0.9999f;
+                                    if (lc != 0 && a12 < best) best = a12, choice = 0;
+                                    if (a02 < best) best = a02, choice = 1;
+                                    if (lc != 2 && a01 < best) best = a01, choice = 2;
+                                    if (choice >= 0) {
+                                        const int I0 = ia ? cl : cr;
+                                        const int p = choice == 0 ? 1 : 0, q = choice == 2 ? 1 : 2;
+                                        const int cp = sel4(p, xc0, xc1, xc2, 0), np = sel4(p, xn0, xn1, xn2, 0);
+                                        const int cq = sel4(q, xc0, xc1, xc2, 0), nq = sel4(q, xn0, xn1, xn2, 0);
+                                        const int cw = sel4(choice, xc0, xc1, xc2, 0), nw = sel4(choice, xn0, xn1, xn2, 0);
+                                        link(I0, cp, np, hof(cp, np), cq, nq, hof(cq, nq));
+                                        link(K, cw, nw, hof(cw, nw), I0, I0, sheight[I0 - c0]);
+                                    }
+                                } else {
+                                    float pa[4][4];
+                                    {
+                                        const Box6 xb[4] = {boxof(xc0), boxof(xc1), boxof(xc2), boxof(xc3)};
+#pragma unroll
+                                        for (int a = 0; a < 4; ++a)
+#pragma unroll
+                                            for (int b = a + 1; b < 4; ++b) pa[a][b] = pa[b][a] = box_area(box_union(xb[a], xb[b]));
+                                        float best = (pa[0][1] + pa[2][3]) * 0.9999f;
+                                        // balanced: (0 1 | 2 3) is the current one; (0 2 | 1 3) = 1, (0 3 | 1 2) = 2
+                                        if (pa[0][2] + pa[1][3] < best) best = pa[0][2] + pa[1][3], choice = 1;
+                                        if (pa[0][3] + pa[1][2] < best) best = pa[0][3] + pa[1][2], choice = 2;
+                                        // chains: w alone at the top, z next, the remaining pair at the bottom
+#pragma unroll
+                                        for (int w = 0; w < 4; ++w) {
+                                            const int o1 = (w + 1) & 3, o2 = (w + 2) & 3, o3 = (w + 3) & 3;
+                                            const float tri_a = box_area(box_union(box_union(xb[o1], xb[o2]), xb[o3]));
+                                            if (tri_a + pa[o2][o3] < best) best = tri_a + pa[o2][o3], choice = 3 + 3 * w + 0;
+                                            if (tri_a + pa[o1][o3] < best) best = tri_a + pa[o1][o3], choice = 3 + 3 * w + 1;
+                                            if (tri_a + pa[o1][o2] < best) best = tri_a + pa[o1][o2], choice = 3 + 3 * w + 2;
+                                        }
+                                    }
+                                    if (choice >= 0) {
+                                        // leaf slots: pair (s0, s1) under cl, (s2, s3) under cr (balanced); chain:
+                                        // w alone under K, z with cr under cl, (s2, s3) under cr
+                                        int s0, s1, s2, s3;
+                                        if (choice == 1) s0 = 0, s1 = 2, s2 = 1, s3 = 3;
+                                        else if (choice == 2) s0 = 0, s1 = 3, s2 = 1, s3 = 2;
+                                        else {
+                                            const int w = (choice - 3) / 3, zs = (choice - 3) % 3;
+                                            const int o1 = (w + 1) & 3, o2 = (w + 2) & 3, o3 = (w + 3) & 3;
+                                            s0 = w, s1 = zs == 0 ? o1 : (zs == 1 ? o2 : o3);
+                                            s2 = zs == 0 ? o2 : o1, s3 = zs == 2 ? o2 : o3;
+                                        }
+                                        const int c0_ = sel4(s0, xc0, xc1, xc2, xc3), n0_ = sel4(s0, xn0, xn1, xn2, xn3);
+                                        const int c1_ = sel4(s1, xc0, xc1, xc2, xc3), n1_ = sel4(s1, xn0, xn1, xn2, xn3);
+                                        const int c2_ = sel4(s2, xc0, xc1, xc2, xc3), n2_ = sel4(s2, xn0, xn1, xn2, xn3);
+                                        const int c3_ = sel4(s3, xc0, xc1, xc2, xc3), n3_ = sel4(s3, xn0, xn1, xn2, xn3);
+                                        link(cr, c2_, n2_, hof(c2_, n2_), c3_, n3_, hof(c3_, n3_));
+                                        if (choice <= 2) {
+                                            link(cl, c0_, n0_, hof(c0_, n0_), c1_, n1_, hof(c1_, n1_));
+                                            link(K, cl, cl, sheight[cl - c0], cr, cr, sheight[cr - c0]);
+                                        } else {
+                                            link(cl, c1_, n1_, hof(c1_, n1_), cr, cr, sheight[cr - c0]);
+                                            link(K, c0_, n0_, hof(c0_, n0_), cl, cl, sheight[cl - c0]);
+                                        }
+                                    }
+                                }
+                            }
+                            if (choice < 0) link(K, cl, ncl, hcl, cr, ncr, hcr);
+                            h = sheight[K - c0];
+                        } else {
+                            const int32_t cl = L == gp ? ~gp : gp, cr = R == gp + 1 ? ~(gp + 1) : gp + 1;
+                            schild[K - c0] = make_int2(cl, cr);
+                            stage_parent(cl, K);
+                            stage_parent(cr, K);
+                            snbox[K - c0] = u;
+                        }
+                        if (o.all_boxes || root) box_store(o.nodebox + 2 * (int64_t)K, u, kTreelet ? h : 0);
+                        if (kTreelet && root) *o.wneed = (unsigned int)(h + 1 + 3);
+                        wl[(round + 1) & 1][atomicAdd(&wn[round + 1], 1)] = make_int2(L, R);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        count = wn[round + 1];
+    }
+    // first arrivals whose sibling never came: their parent spans the chunk boundary (output units)
+    if (t < cnt - 1) {
+        const int f = sslot[t];
+        if (f >= 0) {
+            const int g = c0 + t;  // positions relative to the chunk
+            if (f <= g)
+                smark[f - c0] = t;
+            else
+                smark[t + 1] = f - c0;
+        }
+    }
+    // write the staged nodes out, node K = c0 + t by thread t (coalesced rows, holes where a node
+    // spans the chunk boundary: k_lbvh_top writes those)
+    if (t < cnt) {
+        const int K = c0 + t;
+        const int2 ch = schild[t];
+        if (ch.x != kNone) {
+            o.child[K] = ch;
+            o.range[K] = srange[t];
+            int32_t r0, r1;
+            if constexpr (kTreelet) {
+                const int4 rf = sref[t];
+                r0 = rf.z, r1 = rf.w;
+            } else {
+                auto nref = [&](int32_t c) -> int32_t {
+                    if (c < 0) return make_leaf(~c, 1);
+                    const int2 rg = srange[c - c0];
+                    const int count = rg.y - rg.x + 1;
+                    return count <= o.leaf_size ? make_leaf(rg.x, count) : c;
+                };
+                r0 = nref(ch.x), r1 = nref(ch.y);
+            }
+            const Box6 a = ch.x >= 0 ? snbox[ch.x - c0] : slbox[~ch.x - c0];
+            const Box6 b = ch.y >= 0 ? snbox[ch.y - c0] : slbox[~ch.y - c0];
+            Node64 nd;
+            nd.a = make_float4(a.lx, a.hx, a.ly, a.hy);
+            nd.b = make_float4(b.lx, b.hx, b.ly, b.hy);
+            nd.c = make_float4(a.lz, a.hz, b.lz, b.hz);
+            nd.d = make_int4(r0, r1, 0, 0);
+            o.nodes[K] = nd;
+        }
+        if (spar_int[t] != kNone) o.parent[K] = spar_int[t];
+        if (spar_leaf[t] != kNone) o.parent[(n - 1) + K] = spar_leaf[t];
+    }
+    if (up.nlev <= 1) return;  // a single chunk: the root completed here
+    __syncthreads();           // smark complete
+    // the chunk's units in leaf order; position p = leaf c0 + p; a node [l, r] is stored at its
+    // Karras index (r if a left child, l if a right child) - c0
+    auto unit_of = [&](int p, int e) -> Unit {
+        const int l = c0 + p, r = c0 + e;
+        const int dl = sdelta[p], dr = sdelta[e + 1];
+        const int q = l == r ? p : (dr > dl ? e : p);
+        const Box6 bx = l == r ? slbox[p] : snbox[q];
+        const int hh = (kTreelet && l != r) ? sheight[q] : 0;
+        return Unit{make_int4(l, r, hh, 0), make_float4(bx.lx, bx.ly, bx.lz, 0.f), make_float4(bx.hx, bx.hy, bx.hz, 0.f)};
+    };
+    const bool force = (up.force_global & 1) || ((up.force_global & 2) && (blockIdx.x & 1));
+    lbvh_emit<kTreelet>(o, keys, ks, up, 0, blockIdx.x, cnt, smark, S.swarp, unit_of, pend, pend_n, force);
+    lbvh_levels<kTreelet>(o, keys, ks, up, blockIdx.x, S, pend, pend_n);
+}
+
+// The tree above the chunks: every pending node climbs through the global slots (all chunks' pending
+// nodes at once, so the fenced chain is paid once, not per chunk).
+template <bool kTreelet>
+__global__ void __launch_bounds__(256) k_lbvh_top(const uint64_t *__restrict__ keys, int ks, LbvhOut o,
+                                                  const int4 *__restrict__ pend, const unsigned int *pend_n,
+                                                  const unsigned int *epoch_p) {
+    o.epoch = *epoch_p;
+    const unsigned int cnt = *pend_n;
+    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+        const int4 e = pend[i];
+        const int l = e.x, r = e.y;
+        const int dl = adj_delta(keys, o.n, l - 1, ks), dr = adj_delta(keys, o.n, r, ks);
+        int hb;
+        const Box6 box = box_load_cg(l == r ? o.leafbox + 2 * (int64_t)l : o.nodebox + 2 * (int64_t)(dr > dl ? r : l), hb);
+        lbvh_global_climb<kTreelet>(o, keys, ks, l, r, dl, dr, box, e.z, true);
+    }
+}
+
 // depth of every internal node (root = 0) by walking the parent links (L2-resident, ~log T steps)
 __global__ void __launch_bounds__(256) k_depth(int64_t n, const int32_t *__restrict__ parent,
                                                int32_t *__restrict__ depth) {
@@ -1175,7 +1904,7 @@ void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
 }
 
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  int cubic, int width, int quantized, cudaStream_t s, int restructure) {
+                  int cubic, int width, int quantized, cudaStream_t s, int restructure, int treelets) {
     const int64_t T = b.T;
     {
         NvtxRange r("fgl build: A2 prep (centroids, scene box)");
@@ -1187,6 +1916,43 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
         launch_morton_sort(b, bits, cubic, s);
     }
     const int ps = b.packed_shift, slot = b.sorted_slot;
+    if ((FGL_FUSED_LBVH || treelets) && width == 2 && restructure == 0 && T >= 2) {
+        // leaf records + Karras tree + Eq. 7 boxes + node64 in one pass (k_lbvh)
+        NvtxRange r("fgl build: A2 leaf records + A5-A7 Karras tree, Eq. 7 boxes, node64 (fused)");
+        FGL_CUDA(cudaMemsetAsync(b.wctr + 3, 0, sizeof(unsigned int), s));
+        b.width = 2, b.quantized = 0, b.restructured = 0;
+        static const int all_boxes = [] {
+            const char *e = std::getenv("FGL_ALL_BOXES");
+            return e && *e == '1' ? 1 : 0;
+        }();
+        LbvhOut o{b.child, b.range, b.parent, b.leafbox, b.nodebox, b.nodes, b.gslot, b.wctr + 3,
+                  (int)T, leaf_size, all_boxes, 0u};
+        const uint32_t *perm = ps ? nullptr : b.vals[slot];
+        const uint64_t pmask = ps ? (uint64_t(1) << ps) - 1 : 0;
+        const unsigned grid = (unsigned)((T + kChunk - 1) / kChunk);
+        // pending list: the centroids are dead after the sort; <= 2 x (ceil(T / kChunk) - 1) x 96
+        // entries (children of nodes that span a chunk boundary: the boundaries' ancestors) < T
+        int4 *pend = reinterpret_cast<int4 *>(b.cent);
+        UpPlan up = lbvh_plan(T, b.lbvh_up);
+        if (const char *e = std::getenv("FGL_LBVH_GLOBAL")) up.force_global = std::atoi(e);
+        const unsigned top_grid = (unsigned)std::min<int64_t>(148 * 8, (T + 255) / 256);
+        if (treelets) {
+            constexpr int sm = (int)sizeof(LbvhSmem<true>);
+            FGL_CUDA(cudaFuncSetAttribute(k_lbvh<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            k_lbvh<true><<<grid, kChunk, sm, s>>>(verts, V, tris, perm, b.keys[slot], ps, pmask, b.tri, o, pend, b.sync + 2, up);
+            FGL_LAUNCHED("k_lbvh");
+            k_lbvh_top<true><<<top_grid, 256, 0, s>>>(b.keys[slot], ps, o, pend, b.sync + 2, b.sync + 3);
+        } else {
+            constexpr int sm = (int)sizeof(LbvhSmem<false>);
+            FGL_CUDA(cudaFuncSetAttribute(k_lbvh<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+            k_lbvh<false><<<grid, kChunk, sm, s>>>(verts, V, tris, perm, b.keys[slot], ps, pmask, b.tri, o, pend, b.sync + 2, up);
+            FGL_LAUNCHED("k_lbvh");
+            k_lbvh_top<false><<<top_grid, 256, 0, s>>>(b.keys[slot], ps, o, pend, b.sync + 2, b.sync + 3);
+        }
+        FGL_LAUNCHED("k_lbvh_top");
+        b.restructured = treelets ? 1 : 0;
+        return;
+    }
     {
         // leaf-order records, leaf boxes and the 8-ary box aggregates used by the Eq. 7 boxes
         NvtxRange r("fgl build: A7 leaf-order records + leaf boxes");
@@ -1197,6 +1963,30 @@ void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffe
     }
     NvtxRange r("fgl build: A5-A7 Karras tree, Eq. 7 boxes, traversal nodes");
     launch_tree(b, leaf_size, width, quantized, s, restructure);
+}
+
+size_t lbvh_up_bytes(int64_t T) {
+    const UpPlan up = lbvh_plan(std::max<int64_t>(T, 1), nullptr);
+    return (size_t)reinterpret_cast<char *>(up.units[0]) + 256;
+}
+
+void launch_complete_boxes(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, cudaStream_t s) {
+    const int64_t T = b.T;
+    const int ps = b.packed_shift, slot = b.sorted_slot;
+    k_reorder<<<(unsigned)((T + 255) / 256), 256, 0, s>>>(verts, V, tris, ps ? nullptr : b.vals[slot], b.keys[slot],
+                                                          ps ? (uint64_t(1) << ps) - 1 : 0, T, b.tri, b.leafbox, b.agg);
+    FGL_LAUNCHED("k_reorder");
+    AggLevels L = launch_aggregates(b, s);
+    if (T >= 2 && b.restructured) {  // free topology: boxes bottom-up over the child links
+        FGL_CUDA(cudaMemsetAsync(b.flags, 0, sizeof(int32_t) * (T - 1), s));
+        k_treelet<<<(unsigned)((T + 255) / 256), 256, 0, s>>>((int32_t)T, b.child, b.parent, b.nodebox, b.leafbox,
+                                                              b.cost, b.tsize, reinterpret_cast<unsigned int *>(b.flags),
+                                                              0);
+        FGL_LAUNCHED("k_treelet");
+    } else if (T >= 2) {
+        k_refit_boxes<<<(unsigned)((T - 1 + 255) / 256), 256, 0, s>>>((int)T, b.range, L, b.nodebox);
+        FGL_LAUNCHED("k_refit_boxes");
+    }
 }
 
 }  // namespace fgl

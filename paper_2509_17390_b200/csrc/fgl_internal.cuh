@@ -127,9 +127,11 @@ struct BuildBuffers {
     float *cost8 = nullptr;        // [T-1][8] SAH collapse costs C(n, 1..8) (width 8)
     int32_t *wq = nullptr;         // [T] top-down collapse work queue (width 8)
     unsigned int *wctr = nullptr;  // [4] queue head, tail, done, max stack need (width 8)
+    unsigned long long *gslot = nullptr;  // [T-1] k_lbvh global meeting slots (epoch << 32 | endpoint), zeroed once
+    void *lbvh_up = nullptr;       // k_lbvh levels above the chunks: units, counts, arrival counters (zeroed once)
 };
 
-constexpr int kPrepBlocks = 592;  // 4 x 148 SMs
+constexpr int kPrepBlocks = 888;  // 6 x 148 SMs (latency-bound gather: more loads in flight)
 
 // ---- launchers ------------------------------------------------------------------------------------
 // sort.cu
@@ -144,12 +146,16 @@ void digit_histograms(const uint64_t *keys, int64_t n, int key_bits, uint32_t *g
 
 // build.cu
 void launch_build(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int bits, int leaf_size,
-                  int cubic, int width, int quantized, cudaStream_t s, int restructure = 0);
+                  int cubic, int width, int quantized, cudaStream_t s, int restructure = 0, int treelets = 0);
 void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
                      cudaStream_t s);
 void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s);
 void launch_tree(BuildBuffers &b, int leaf_size, int width, int quantized, cudaStream_t s, int restructure = 0);
 void launch_refit(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, int leaf_size, cudaStream_t s);
+// leaf boxes + Eq. 7 node boxes of the current tree, recomputed exactly (the fused build stores only
+// those a sibling needs; the scene export calls this)
+size_t lbvh_up_bytes(int64_t T);  // bytes of BuildBuffers::lbvh_up
+void launch_complete_boxes(const float *verts, int64_t V, const int32_t *tris, BuildBuffers &b, cudaStream_t s);
 void launch_wide8(BuildBuffers &b, cudaStream_t s);  // wide.cu: SAH collapse to node96q
 void launch_morton_points(const float *pts, int64_t n, const float *lo, const float *hi, int bits,
                           uint64_t *codes, cudaStream_t s);

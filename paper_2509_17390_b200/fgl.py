@@ -31,7 +31,7 @@ class FglError(RuntimeError):
 
 class BuildOpts(Structure):
     _fields_ = [("morton_bits", c_int32), ("leaf_size", c_int32), ("morton_box", c_int32), ("width", c_int32),
-                ("quantized", c_int32), ("restructure", c_int32), ("reserved", c_int32 * 2)]
+                ("quantized", c_int32), ("restructure", c_int32), ("treelets", c_int32), ("reserved", c_int32 * 1)]
 
 
 class Stats(Structure):
@@ -183,7 +183,7 @@ class Scene:
 
     def __init__(self, verts=None, tris=None, device=None, build: bool = True, morton_bits: int = 0,
                  leaf_size: int = 0, morton_box: int = 0, width: int = 0, quantized: int = 0, restructure: int = 0,
-                 stream=None):
+                 treelets: int = 0, stream=None):
         """leaf_size / width 0 = library defaults; morton_box 0 = cubic (R22), 1 = per-axis (Eq. 5)."""
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
@@ -194,6 +194,7 @@ class Scene:
         self.morton_bits, self.leaf_size, self.morton_box, self.width = morton_bits, leaf_size, morton_box, width
         self.quantized = quantized
         self.restructure = restructure
+        self.treelets = treelets
         self.T = 0
         if verts is not None:
             self.upload(verts, tris, stream)
@@ -236,7 +237,8 @@ class Scene:
               width: int | None = None, stream=None):
         mb = self.morton_box if morton_box is None else morton_box
         o = BuildOpts(morton_bits or self.morton_bits, leaf_size or self.leaf_size, int(mb),
-                      int(width or self.width), int(self.quantized), int(self.restructure), (c_int32 * 2)())
+                      int(width or self.width), int(self.quantized), int(self.restructure), int(self.treelets),
+                      (c_int32 * 1)())
         _check(lib().fgl_scene_build(self._h, ctypes.byref(o), _stream(stream)))
         return self
 

@@ -198,6 +198,72 @@ def test_build_matches_oracle(fgl, name, leaf_size, cubic, width, bits, quant):
         assert np.array_equal(box, np.concatenate([sub.min(0), sub.max(0)]))
 
 
+@pytest.mark.parametrize("T", [2, 3, 511, 512, 513, 1024, 1025, 4097, 65537])
+@pytest.mark.parametrize("leaf_size", [1, 2])
+def test_fused_tree_at_chunk_edges(fgl, T, leaf_size):
+    """The default width-2 build meets siblings in shared memory inside 512-leaf chunks and through
+    global slots across them (k_lbvh): ragged last chunks (one leaf), exact chunk multiples and many
+    chunks must give the oracle's Eq. 6 tree and exact Eq. 7 node boxes; duplicated centroids force
+    the index tie-break across chunk boundaries."""
+    m = synth.soup(T, seed=T)
+    if T > 600:  # 600 identical triangles: a run of equal codes that straddles a chunk boundary
+        m.verts[:3 * 600] = np.tile(m.verts[:3], (600, 1))
+    s = fgl.Scene(m.verts, m.tris, leaf_size=leaf_size)
+    g = s.export()
+    o = oracle.lbvh(m.verts, m.tris, bits=10, cubic=True)
+    for k_g, k_o in (("perm", "perm"), ("child", "child"), ("range", "range"), ("node_box", "node_box")):
+        assert np.array_equal(g[k_g], o[k_o]), k_g
+    visited, cover = _decode_nodes(g["nodes"], T, leaf_size)
+    assert np.all(cover == 1)
+    V = m.verts[m.tris[o["perm"]]]
+    for box, ref in visited:
+        if ref[0] == "leaf":
+            f, c = ref[1], ref[2]
+        else:
+            f, l = o["range"][ref[1]]
+            c = l - f + 1
+            assert c > leaf_size
+        sub = V[f:f + c].reshape(-1, 3)
+        assert np.array_equal(box, np.concatenate([sub.min(0), sub.max(0)]))
+
+
+@pytest.mark.parametrize("T,mode", [(1025, 1), (70001, 1), (70001, 2), (70001, 4), (300007, 6)])
+def test_fused_tree_global_fallback(fgl, T, mode, monkeypatch):
+    """FGL_LBVH_GLOBAL sends boundary subtrees through the global-slot climb (k_lbvh_top, the path
+    taken when a chunk or a group overflows its shared-memory unit budget): every chunk (1), every
+    odd chunk (2), every odd group above the chunks (4) — partial overflow poisons everything above
+    it — must give the same Eq. 6 tree and node64s as the hierarchical levels."""
+    m = synth.soup(T, seed=11)
+    a = fgl.Scene(m.verts, m.tris).export()
+    monkeypatch.setenv("FGL_LBVH_GLOBAL", str(mode))
+    b = fgl.Scene(m.verts, m.tris).export()
+    for k in ("child", "range", "nodes", "tri48", "node_box"):
+        assert a[k].tobytes() == b[k].tobytes(), k
+    o = oracle.lbvh(m.verts, m.tris, bits=10, cubic=True)
+    assert np.array_equal(b["child"], o["child"]) and np.array_equal(b["range"], o["range"])
+
+
+def test_fused_tree_terrain_full_size(fgl, monkeypatch):
+    """C3's 10 M-triangle terrain (39 k chunks, 7 levels above them, duplicate codes): every node's
+    children tile its leaf range (the radix-tree invariant of Eq. 6), every node but the root has
+    one parent, and the tree is bitwise the one the all-global fallback builds."""
+    m = synth.scene_terrain(3).mesh
+    v, t = torch.from_numpy(m.verts).cuda(), torch.from_numpy(m.tris).cuda()
+    a = fgl.Scene(v, t).export()
+    child, rng = a["child"].astype(np.int64), a["range"].astype(np.int64)
+    lo = np.where(child >= 0, rng[np.maximum(child, 0), 0], ~child)
+    hi = np.where(child >= 0, rng[np.maximum(child, 0), 1], ~child)
+    assert np.array_equal(lo[:, 0], rng[:, 0]) and np.array_equal(hi[:, 1], rng[:, 1])
+    assert np.array_equal(hi[:, 0] + 1, lo[:, 1])
+    assert rng[0, 0] == 0 and rng[0, 1] == m.T - 1
+    internal = child[child >= 0]
+    assert np.array_equal(np.sort(internal), np.arange(1, m.T - 1))
+    monkeypatch.setenv("FGL_LBVH_GLOBAL", "1")
+    b = fgl.Scene(v, t).export()
+    for k in ("child", "range", "nodes", "tri48"):
+        assert a[k].tobytes() == b[k].tobytes(), k
+
+
 def test_build_is_deterministic(fgl):
     m = synth.soup(5000, seed=1)
     a = fgl.Scene(m.verts, m.tris).export()
