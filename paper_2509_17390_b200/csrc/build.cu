@@ -866,6 +866,9 @@ __global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const i
 #ifndef FGL_LBVH_CHUNK
 #define FGL_LBVH_CHUNK 256
 #endif
+#ifndef FGL_LBVH_MINB
+#define FGL_LBVH_MINB (1536 / FGL_LBVH_CHUNK)  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr int kChunk = FGL_LBVH_CHUNK;  // leaves (= threads) per k_lbvh CTA
 constexpr int kSlotEmpty = -1, kSlotDone = -2;
 constexpr int kMaxRounds = 100;  // > the depth of a Karras tree (delta strictly grows downwards, < 96)
@@ -1023,7 +1026,7 @@ struct LbvhSmem {
     BoxArr snbox;             // internal node c0 + i, once complete
     int2 schild[kChunk];      // staged child refs of internal node c0 + i (kNone: not completed here)
     int2 srange[kChunk];      // staged leaf range of internal node c0 + i
-    int2 wl[2][kChunk];       // round work lists: (l, r) of completed nodes
+    int4 wl[2][kChunk];       // round work lists: (l, r, split) of nodes to complete
     int smark[kChunk];        // position p starts an output unit ending at smark[p] (kNone: no)
     int swarp[kChunk / 32 + 1];
     int4 sref[kTreelet ? kChunk : 1];  // internal node c0 + i: (child refs, node64 refs)
@@ -1081,6 +1084,17 @@ static UpPlan lbvh_plan(int64_t T, void *base) {
 }
 
 
+// append `it` to a shared work list, one shared atomic per warp (called by whole warps)
+__device__ __forceinline__ void append_item(int4 *list, int *n, bool push, const int4 &it) {
+    const unsigned bal = __ballot_sync(0xffffffffu, push);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(n, __popc(bal));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (push) list[base + __popc(bal & ((1u << lane) - 1u))] = it;
+}
+
 // a unit whose parent will be built by the global climb: publish its box where the sibling looks
 // (Karras index by side) and list it for k_lbvh_top
 template <bool kTreelet>
@@ -1129,19 +1143,21 @@ __device__ void lbvh_emit(const LbvhOut &o, const uint64_t *__restrict__ keys, i
 // level 0; the last CTA of each group goes on up.
 template <bool kTreelet>
 __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys, int ks, const UpPlan &up, int seg,
-                            LbvhSmem<kTreelet> &S, int4 *pend, unsigned int *pend_n) {
+                            LbvhSmem<kTreelet> &S, int4 *pend, unsigned int *pend_n, bool arrived) {
     __shared__ int s_last, s_off[kGroup + 1], s_poison;
     const int t = threadIdx.x, n = o.n;
     for (int lev = 1; lev < up.nlev; ++lev) {
         const int group = seg / kGroup, first = group * kGroup, gsize = min(kGroup, up.nseg[lev - 1] - first);
-        __syncthreads();  // this segment's units / count written (by several threads)
-        if (t == 0) {
-            __threadfence();  // release them (cumulative over the barrier) before the arrival
-            s_last = atomicAdd(up.ctr[lev] + group, 1u) == (unsigned)(gsize - 1);
-            if (s_last) up.ctr[lev][group] = 0;  // self-resetting for the next build
+        if (!(lev == 1 && arrived)) {  // (level 1: the caller arrived already, as the last of its group)
+            __syncthreads();  // this segment's units / count written (by several threads)
+            if (t == 0) {
+                __threadfence();  // release them (cumulative over the barrier) before the arrival
+                s_last = atomicAdd(up.ctr[lev] + group, 1u) == (unsigned)(gsize - 1);
+                if (s_last) up.ctr[lev][group] = 0;  // self-resetting for the next build
+            }
+            __syncthreads();
+            if (!s_last) return;
         }
-        __syncthreads();
-        if (!s_last) return;
         if (t == 0) __threadfence();  // acquire the group's segments (the barrier below spreads it)
         __syncthreads();
         seg = group;
@@ -1180,7 +1196,7 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
         int *const nh = S.spar_leaf;  // node heights (stored like the boxes)
         BoxArr &ubox = S.slbox, &nbox = S.snbox;
         int2 *const uab = S.schild;   // unit leaf ranges
-        int2 (*const wl)[kChunk] = S.wl;
+        int4 (*const wl)[kChunk] = S.wl;
         sslot[t] = kSlotEmpty, smark[t] = kNone;
         if (t <= kMaxRounds) wn[t] = 0;
         if (t < m) {
@@ -1193,11 +1209,34 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
         __syncthreads();
         int count = m;
         for (int round = 0; count > 0; ++round) {
+            int4 next = make_int4(0, 0, 0, 0);
+            bool push = false;
             if (t < count) {
                 int U = t, W = t;
-                if (round > 0) {
-                    const int2 e = wl[round & 1][t];
-                    U = e.x, W = e.y;
+                if (round > 0) {  // complete the node over units [U2, W2], split at gap gs (second arrival last round)
+                    const int4 e = wl[round & 1][t];
+                    const int U2 = e.x, W2 = e.y, gs = e.z;
+                    const int L = uab[U2].x, R = uab[W2].y, g = uab[gs].y;  // leaves; split after leaf g
+                    const Box6 A = U2 == gs ? (Box6)ubox[gs] : (Box6)nbox[gs];
+                    const Box6 B = W2 == gs + 1 ? (Box6)ubox[gs + 1] : (Box6)nbox[gs + 1];
+                    int ha = 0, hb = 0;
+                    if (kTreelet) {
+                        ha = trav_height(o, L, g, U2 == gs ? uh[gs] : nh[gs]);
+                        hb = trav_height(o, g + 1, R, W2 == gs + 1 ? uh[gs + 1] : nh[gs + 1]);
+                    }
+                    const int dlp = sdelta[U2], drp = sdelta[W2 + 1];
+                    const bool root = dlp < 0 && drp < 0;
+                    const Box6 bu = box_union(A, B);
+                    put_node(o, root ? 0 : (drp > dlp ? R : L), g, L, R, A, B, ha, hb);
+                    const int q = root ? 0 : (drp > dlp ? W2 : U2);
+                    nbox[q] = bu;
+                    const int hh = 1 + max(ha, hb);
+                    if (kTreelet) nh[q] = hh;
+                    if (root) {
+                        box_store(o.nodebox, bu, kTreelet ? hh : 0);
+                        if (kTreelet) *o.wneed = (unsigned int)(hh + 1 + 3);
+                    }
+                    U = U2, W = W2;
                 }
                 const int dl = sdelta[U], dr = sdelta[W + 1];
                 if (dl >= 0 || dr >= 0) {
@@ -1206,39 +1245,16 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
                     if (gs < 0 || gs > m - 2) {
                         smark[U] = W;
                     } else {
-                        int other;
-                        asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;"
-                                     : "=r"(other)
-                                     : "r"((uint32_t)__cvta_generic_to_shared(&sslot[gs])), "r"(left ? U : W)
-                                     : "memory");
+                        const int other = atomicExch(&sslot[gs], left ? U : W);
                         if (other != kSlotEmpty) {
                             sslot[gs] = kSlotDone;
-                            const int U2 = left ? U : other, W2 = left ? other : W;
-                            const int L = uab[U2].x, R = uab[W2].y, g = uab[gs].y;  // leaves; split after leaf g
-                            const Box6 A = U2 == gs ? ubox[gs] : nbox[gs];
-                            const Box6 B = W2 == gs + 1 ? ubox[gs + 1] : nbox[gs + 1];
-                            int ha = 0, hb = 0;
-                            if (kTreelet) {
-                                ha = trav_height(o, L, g, U2 == gs ? uh[gs] : nh[gs]);
-                                hb = trav_height(o, g + 1, R, W2 == gs + 1 ? uh[gs + 1] : nh[gs + 1]);
-                            }
-                            const int dlp = sdelta[U2], drp = sdelta[W2 + 1];
-                            const bool root = dlp < 0 && drp < 0;
-                            const Box6 bu = box_union(A, B);
-                            put_node(o, root ? 0 : (drp > dlp ? R : L), g, L, R, A, B, ha, hb);
-                            const int q = root ? 0 : (drp > dlp ? W2 : U2);
-                            nbox[q] = bu;
-                            const int hh = 1 + max(ha, hb);
-                            if (kTreelet) nh[q] = hh;
-                            if (root) {
-                                box_store(o.nodebox, bu, kTreelet ? hh : 0);
-                                if (kTreelet) *o.wneed = (unsigned int)(hh + 1 + 3);
-                            }
-                            wl[(round + 1) & 1][atomicAdd(&wn[round + 1], 1)] = make_int2(U2, W2);
+                            next = make_int4(left ? U : other, left ? other : W, gs, 0);
+                            push = true;
                         }
                     }
                 }
             }
+            append_item(wl[(round + 1) & 1], &wn[round + 1], push, next);
             __syncthreads();
             count = wn[round + 1];
         }
@@ -1272,7 +1288,7 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
 // their indices. The subtree leaf ranges stop being contiguous (range[] is kept for the treelet
 // roots only; the scene is marked restructured).
 template <bool kTreelet>
-__global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : (kChunk <= 256 ? 6 : 3)) k_lbvh(const float *__restrict__ verts, int64_t V,
+__global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : FGL_LBVH_MINB) k_lbvh(const float *__restrict__ verts, int64_t V,
                                                  const int32_t *__restrict__ tris, const uint32_t *__restrict__ perm,
                                                  const uint64_t *__restrict__ keys, int ks, uint64_t pmask,
                                                  float4 *__restrict__ tri, LbvhOut o, int4 *__restrict__ pend,
@@ -1284,7 +1300,7 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : (
     BoxArr &slbox = S.slbox, &snbox = S.snbox;
     int4 *const sref = S.sref;
     int2 *const schild = S.schild, *const srange = S.srange;
-    int2 (*const wl)[kChunk] = S.wl;
+    int4 (*const wl)[kChunk] = S.wl;
     const int n = o.n, t = threadIdx.x, c0 = blockIdx.x * kChunk, cnt = min(kChunk, n - c0), j = c0 + t;
     sslot[t] = kSlotEmpty;
     if (t <= kMaxRounds) wn[t] = 0;
@@ -1317,13 +1333,136 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : (
     // phase 1, bottom-up in rounds: round k holds the nodes completed in round k - 1 (round 0: the
     // leaves), compacted onto the first threads, so the climb runs on dense warps; two children meet
     // at their parent's split slot in shared memory, the second completes the parent.
+    // a node is completed one round after its second child arrived (after the barrier), so the
+    // children's boxes and records are visible without a fence; the exchange at the slot only has to
+    // decide who is second
     int count = cnt;
     for (int round = 0; count > 0; ++round) {
+        int4 next = make_int4(0, 0, 0, 0);
+        bool push = false;
         if (t < count) {
             int l = j, r = j;
             if (round > 0) {
-                const int2 e = wl[round & 1][t];
-                l = e.x, r = e.y;
+                const int4 e = wl[round & 1][t];  // (L, R, split)
+                const int L = e.x, R = e.y, gp = e.z;
+                int h = 0;
+                // both children: [L, gp] and [gp + 1, R]
+                const Box6 A = L == gp ? slbox[L - c0] : snbox[gp - c0];
+                const Box6 B = R == gp + 1 ? slbox[R - c0] : snbox[gp + 1 - c0];
+                const int dlp = sdelta[L - c0], drp = sdelta[R + 1 - c0];
+                const bool root = dlp < 0 && drp < 0;
+                const int K = root ? 0 : (drp > dlp ? R : L);
+                const Box6 u = box_union(A, B);
+                srange[K - c0] = make_int2(L, R);
+                if (K == 0) spar_int[0] = -1;
+                if constexpr (kTreelet) {
+                    const int32_t cl = L == gp ? ~gp : gp, cr = R == gp + 1 ? ~(gp + 1) : gp + 1;
+                    // children: refs, node64 refs (leaf_size collapse), heights; boxes stay in smem
+                    const int nl = gp - L + 1, nrr = R - gp;
+                    const bool ia = cl >= 0 && nl > o.leaf_size, ib = cr >= 0 && nrr > o.leaf_size;
+                    const int32_t ncl = ia ? cl : make_leaf(L, nl), ncr = ib ? cr : make_leaf(gp + 1, nrr);
+                    const int hcl = ia ? sheight[cl - c0] : 0, hcr = ib ? sheight[cr - c0] : 0;
+                    auto boxof = [&](int32_t c) -> Box6 { return c >= 0 ? (Box6)snbox[c - c0] : (Box6)slbox[~c - c0]; };
+                    auto hof = [&](int32_t c, int32_t nr) -> int { return nr >= 0 ? sheight[c - c0] : 0; };
+                    // internal node idx takes children (ca, na, ha) and (cb, nb, hb): staged links,
+                    // record, box (children's boxes re-read: a child re-linked just before is current)
+                    auto link = [&](int idx, int32_t ca, int32_t na, int ha, int32_t cb, int32_t nb, int hb) {
+                        schild[idx - c0] = make_int2(ca, cb);
+                        stage_parent(ca, idx);
+                        stage_parent(cb, idx);
+                        sref[idx - c0] = make_int4(ca, cb, na, nb);
+                        snbox[idx - c0] = box_union(boxof(ca), boxof(cb));
+                        sheight[idx - c0] = 1 + max(ha, hb);
+                    };
+                    auto sel4 = [](int i, int v0, int v1, int v2, int v3) { return i == 0 ? v0 : (i == 1 ? v1 : (i == 2 ? v2 : v3)); };
+                    int choice = -1;  // -1: keep the Karras topology
+                    int xc0 = 0, xc1 = 0, xc2 = 0, xc3 = 0, xn0 = 0, xn1 = 0, xn2 = 0, xn3 = 0;
+                    if (ia || ib) {
+                        // treelet leaves: x0, x1 under the left child (or the left child), x2, x3 likewise
+                        const int4 ra = ia ? sref[cl - c0] : make_int4(cl, cl, ncl, ncl);
+                        const int4 rb = ib ? sref[cr - c0] : make_int4(cr, cr, ncr, ncr);
+                        xc0 = ra.x, xc1 = ra.y, xn0 = ra.z, xn1 = ra.w, xc2 = rb.x, xc3 = rb.y, xn2 = rb.z, xn3 = rb.w;
+                        if (!(ia && ib)) {
+                            // 3 leaves y0 y1 y2 (the leaf child at lc): chains only, w alone, the others paired
+                            if (!ia) xc1 = xc2, xn1 = xn2, xc2 = xc3, xn2 = xn3;  // y = (leaf, x2, x3)
+                            const Box6 y0 = boxof(xc0), y1 = boxof(xc1), y2 = boxof(xc2);
+                            const int lc = ia ? 2 : 0;
+                            const float a01 = box_area(box_union(y0, y1)), a02 = box_area(box_union(y0, y2)),
+                                        a12 = box_area(box_union(y1, y2));
+                            float best = (lc == 2 ? a01 : a12) * 0.9999f;
+                            if (lc != 0 && a12 < best) best = a12, choice = 0;
+                            if (a02 < best) best = a02, choice = 1;
+                            if (lc != 2 && a01 < best) best = a01, choice = 2;
+                            if (choice >= 0) {
+                                const int I0 = ia ? cl : cr;
+                                const int p = choice == 0 ? 1 : 0, q = choice == 2 ? 1 : 2;
+                                const int cp = sel4(p, xc0, xc1, xc2, 0), np = sel4(p, xn0, xn1, xn2, 0);
+                                const int cq = sel4(q, xc0, xc1, xc2, 0), nq = sel4(q, xn0, xn1, xn2, 0);
+                                const int cw = sel4(choice, xc0, xc1, xc2, 0), nw = sel4(choice, xn0, xn1, xn2, 0);
+                                link(I0, cp, np, hof(cp, np), cq, nq, hof(cq, nq));
+                                link(K, cw, nw, hof(cw, nw), I0, I0, sheight[I0 - c0]);
+                            }
+                        } else {
+                            float pa[4][4];
+                            {
+                                const Box6 xb[4] = {boxof(xc0), boxof(xc1), boxof(xc2), boxof(xc3)};
+#pragma unroll
+                                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                                    for (int b = a + 1; b < 4; ++b) pa[a][b] = pa[b][a] = box_area(box_union(xb[a], xb[b]));
+                                float best = (pa[0][1] + pa[2][3]) * 0.9999f;
+                                // balanced: (0 1 | 2 3) is the current one; (0 2 | 1 3) = 1, (0 3 | 1 2) = 2
+                                if (pa[0][2] + pa[1][3] < best) best = pa[0][2] + pa[1][3], choice = 1;
+                                if (pa[0][3] + pa[1][2] < best) best = pa[0][3] + pa[1][2], choice = 2;
+                                // chains: w alone at the top, z next, the remaining pair at the bottom
+#pragma unroll
+                                for (int w = 0; w < 4; ++w) {
+                                    const int o1 = (w + 1) & 3, o2 = (w + 2) & 3, o3 = (w + 3) & 3;
+                                    const float tri_a = box_area(box_union(box_union(xb[o1], xb[o2]), xb[o3]));
+                                    if (tri_a + pa[o2][o3] < best) best = tri_a + pa[o2][o3], choice = 3 + 3 * w + 0;
+                                    if (tri_a + pa[o1][o3] < best) best = tri_a + pa[o1][o3], choice = 3 + 3 * w + 1;
+                                    if (tri_a + pa[o1][o2] < best) best = tri_a + pa[o1][o2], choice = 3 + 3 * w + 2;
+                                }
+                            }
+                            if (choice >= 0) {
+                                // leaf slots: pair (s0, s1) under cl, (s2, s3) under cr (balanced); chain:
+                                // w alone under K, z with cr under cl, (s2, s3) under cr
+                                int s0, s1, s2, s3;
+                                if (choice == 1) s0 = 0, s1 = 2, s2 = 1, s3 = 3;
+                                else if (choice == 2) s0 = 0, s1 = 3, s2 = 1, s3 = 2;
+                                else {
+                                    const int w = (choice - 3) / 3, zs = (choice - 3) % 3;
+                                    const int o1 = (w + 1) & 3, o2 = (w + 2) & 3, o3 = (w + 3) & 3;
+                                    s0 = w, s1 = zs == 0 ? o1 : (zs == 1 ? o2 : o3);
+                                    s2 = zs == 0 ? o2 : o1, s3 = zs == 2 ? o2 : o3;
+                                }
+                                const int c0_ = sel4(s0, xc0, xc1, xc2, xc3), n0_ = sel4(s0, xn0, xn1, xn2, xn3);
+                                const int c1_ = sel4(s1, xc0, xc1, xc2, xc3), n1_ = sel4(s1, xn0, xn1, xn2, xn3);
+                                const int c2_ = sel4(s2, xc0, xc1, xc2, xc3), n2_ = sel4(s2, xn0, xn1, xn2, xn3);
+                                const int c3_ = sel4(s3, xc0, xc1, xc2, xc3), n3_ = sel4(s3, xn0, xn1, xn2, xn3);
+                                link(cr, c2_, n2_, hof(c2_, n2_), c3_, n3_, hof(c3_, n3_));
+                                if (choice <= 2) {
+                                    link(cl, c0_, n0_, hof(c0_, n0_), c1_, n1_, hof(c1_, n1_));
+                                    link(K, cl, cl, sheight[cl - c0], cr, cr, sheight[cr - c0]);
+                                } else {
+                                    link(cl, c1_, n1_, hof(c1_, n1_), cr, cr, sheight[cr - c0]);
+                                    link(K, c0_, n0_, hof(c0_, n0_), cl, cl, sheight[cl - c0]);
+                                }
+                            }
+                        }
+                    }
+                    if (choice < 0) link(K, cl, ncl, hcl, cr, ncr, hcr);
+                    h = sheight[K - c0];
+                } else {
+                    const int32_t cl = L == gp ? ~gp : gp, cr = R == gp + 1 ? ~(gp + 1) : gp + 1;
+                    schild[K - c0] = make_int2(cl, cr);
+                    stage_parent(cl, K);
+                    stage_parent(cr, K);
+                    snbox[K - c0] = u;
+                }
+                if (o.all_boxes || root) box_store(o.nodebox + 2 * (int64_t)K, u, kTreelet ? h : 0);
+                if (kTreelet && root) *o.wneed = (unsigned int)(h + 1 + 3);
+                l = L, r = R;
             }
             const int dl = sdelta[l - c0], dr = sdelta[r + 1 - c0];
             if (dl >= 0 || dr >= 0) {  // not the root
@@ -1333,137 +1472,16 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : (
                     smark[l - c0] = r - c0;
                 } else {
                     const int s = gp - c0;
-                    // release this node's box / refs (stored at completion), acquire the sibling's
-                    int other;
-                    asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;"
-                                 : "=r"(other)
-                                 : "r"((uint32_t)__cvta_generic_to_shared(&sslot[s])), "r"(left ? l : r)
-                                 : "memory");
-                    if (other != kSlotEmpty) {  // second to arrive: complete the parent
+                    const int other = atomicExch(&sslot[s], left ? l : r);
+                    if (other != kSlotEmpty) {  // second to arrive: the parent completes next round
                         sslot[s] = kSlotDone;
-                        int h = 0;
-                        const int L = left ? l : other, R = left ? other : r;
-                        // both children: [L, gp] and [gp + 1, R]
-                        const Box6 A = L == gp ? slbox[L - c0] : snbox[gp - c0];
-                        const Box6 B = R == gp + 1 ? slbox[R - c0] : snbox[gp + 1 - c0];
-                        const int dlp = sdelta[L - c0], drp = sdelta[R + 1 - c0];
-                        const bool root = dlp < 0 && drp < 0;
-                        const int K = root ? 0 : (drp > dlp ? R : L);
-                        const Box6 u = box_union(A, B);
-                        srange[K - c0] = make_int2(L, R);
-                        if (K == 0) spar_int[0] = -1;
-                        if constexpr (kTreelet) {
-                            const int32_t cl = L == gp ? ~gp : gp, cr = R == gp + 1 ? ~(gp + 1) : gp + 1;
-                            // children: refs, node64 refs (leaf_size collapse), heights; boxes stay in smem
-                            const int nl = gp - L + 1, nrr = R - gp;
-                            const bool ia = cl >= 0 && nl > o.leaf_size, ib = cr >= 0 && nrr > o.leaf_size;
-                            const int32_t ncl = ia ? cl : make_leaf(L, nl), ncr = ib ? cr : make_leaf(gp + 1, nrr);
-                            const int hcl = ia ? sheight[cl - c0] : 0, hcr = ib ? sheight[cr - c0] : 0;
-                            auto boxof = [&](int32_t c) -> Box6 { return c >= 0 ? (Box6)snbox[c - c0] : (Box6)slbox[~c - c0]; };
-                            auto hof = [&](int32_t c, int32_t nr) -> int { return nr >= 0 ? sheight[c - c0] : 0; };
-                            // internal node idx takes children (ca, na, ha) and (cb, nb, hb): staged links,
-                            // record, box (children's boxes re-read: a child re-linked just before is current)
-                            auto link = [&](int idx, int32_t ca, int32_t na, int ha, int32_t cb, int32_t nb, int hb) {
-                                schild[idx - c0] = make_int2(ca, cb);
-                                stage_parent(ca, idx);
-                                stage_parent(cb, idx);
-                                sref[idx - c0] = make_int4(ca, cb, na, nb);
-                                snbox[idx - c0] = box_union(boxof(ca), boxof(cb));
-                                sheight[idx - c0] = 1 + max(ha, hb);
-                            };
-                            auto sel4 = [](int i, int v0, int v1, int v2, int v3) { return i == 0 ? v0 : (i == 1 ? v1 : (i == 2 ? v2 : v3)); };
-                            int choice = -1;  // -1: keep the Karras topology
-                            int xc0 = 0, xc1 = 0, xc2 = 0, xc3 = 0, xn0 = 0, xn1 = 0, xn2 = 0, xn3 = 0;
-                            if (ia || ib) {
-                                // treelet leaves: x0, x1 under the left child (or the left child), x2, x3 likewise
-                                const int4 ra = ia ? sref[cl - c0] : make_int4(cl, cl, ncl, ncl);
-                                const int4 rb = ib ? sref[cr - c0] : make_int4(cr, cr, ncr, ncr);
-                                xc0 = ra.x, xc1 = ra.y, xn0 = ra.z, xn1 = ra.w, xc2 = rb.x, xc3 = rb.y, xn2 = rb.z, xn3 = rb.w;
-                                if (!(ia && ib)) {
-                                    // 3 leaves y0 y1 y2 (the leaf child at lc): chains only, w alone, the others paired
-                                    if (!ia) xc1 = xc2, xn1 = xn2, xc2 = xc3, xn2 = xn3;  // y = (leaf, x2, x3)
-                                    const Box6 y0 = boxof(xc0), y1 = boxof(xc1), y2 = boxof(xc2);
-                                    const int lc = ia ? 2 : 0;
-                                    const float a01 = box_area(box_union(y0, y1)), a02 = box_area(box_union(y0, y2)),
-                                                a12 = box_area(box_union(y1, y2));
-                                    float best = (lc == 2 ? a01 : a12) * 0.9999f;
-                                    if (lc != 0 && a12 < best) best = a12, choice = 0;
-                                    if (a02 < best) best = a02, choice = 1;
-                                    if (lc != 2 && a01 < best) best = a01, choice = 2;
-                                    if (choice >= 0) {
-                                        const int I0 = ia ? cl : cr;
-                                        const int p = choice == 0 ? 1 : 0, q = choice == 2 ? 1 : 2;
-                                        const int cp = sel4(p, xc0, xc1, xc2, 0), np = sel4(p, xn0, xn1, xn2, 0);
-                                        const int cq = sel4(q, xc0, xc1, xc2, 0), nq = sel4(q, xn0, xn1, xn2, 0);
-                                        const int cw = sel4(choice, xc0, xc1, xc2, 0), nw = sel4(choice, xn0, xn1, xn2, 0);
-                                        link(I0, cp, np, hof(cp, np), cq, nq, hof(cq, nq));
-                                        link(K, cw, nw, hof(cw, nw), I0, I0, sheight[I0 - c0]);
-                                    }
-                                } else {
-                                    float pa[4][4];
-                                    {
-                                        const Box6 xb[4] = {boxof(xc0), boxof(xc1), boxof(xc2), boxof(xc3)};
-#pragma unroll
-                                        for (int a = 0; a < 4; ++a)
-#pragma unroll
-                                            for (int b = a + 1; b < 4; ++b) pa[a][b] = pa[b][a] = box_area(box_union(xb[a], xb[b]));
-                                        float best = (pa[0][1] + pa[2][3]) * 0.9999f;
-                                        // balanced: (0 1 | 2 3) is the current one; (0 2 | 1 3) = 1, (0 3 | 1 2) = 2
-                                        if (pa[0][2] + pa[1][3] < best) best = pa[0][2] + pa[1][3], choice = 1;
-                                        if (pa[0][3] + pa[1][2] < best) best = pa[0][3] + pa[1][2], choice = 2;
-                                        // chains: w alone at the top, z next, the remaining pair at the bottom
-#pragma unroll
-                                        for (int w = 0; w < 4; ++w) {
-                                            const int o1 = (w + 1) & 3, o2 = (w + 2) & 3, o3 = (w + 3) & 3;
-                                            const float tri_a = box_area(box_union(box_union(xb[o1], xb[o2]), xb[o3]));
-                                            if (tri_a + pa[o2][o3] < best) best = tri_a + pa[o2][o3], choice = 3 + 3 * w + 0;
-                                            if (tri_a + pa[o1][o3] < best) best = tri_a + pa[o1][o3], choice = 3 + 3 * w + 1;
-                                            if (tri_a + pa[o1][o2] < best) best = tri_a + pa[o1][o2], choice = 3 + 3 * w + 2;
-                                        }
-                                    }
-                                    if (choice >= 0) {
-                                        // leaf slots: pair (s0, s1) under cl, (s2, s3) under cr (balanced); chain:
-                                        // w alone under K, z with cr under cl, (s2, s3) under cr
-                                        int s0, s1, s2, s3;
-                                        if (choice == 1) s0 = 0, s1 = 2, s2 = 1, s3 = 3;
-                                        else if (choice == 2) s0 = 0, s1 = 3, s2 = 1, s3 = 2;
-                                        else {
-                                            const int w = (choice - 3) / 3, zs = (choice - 3) % 3;
-                                            const int o1 = (w + 1) & 3, o2 = (w + 2) & 3, o3 = (w + 3) & 3;
-                                            s0 = w, s1 = zs == 0 ? o1 : (zs == 1 ? o2 : o3);
-                                            s2 = zs == 0 ? o2 : o1, s3 = zs == 2 ? o2 : o3;
-                                        }
-                                        const int c0_ = sel4(s0, xc0, xc1, xc2, xc3), n0_ = sel4(s0, xn0, xn1, xn2, xn3);
-                                        const int c1_ = sel4(s1, xc0, xc1, xc2, xc3), n1_ = sel4(s1, xn0, xn1, xn2, xn3);
-                                        const int c2_ = sel4(s2, xc0, xc1, xc2, xc3), n2_ = sel4(s2, xn0, xn1, xn2, xn3);
-                                        const int c3_ = sel4(s3, xc0, xc1, xc2, xc3), n3_ = sel4(s3, xn0, xn1, xn2, xn3);
-                                        link(cr, c2_, n2_, hof(c2_, n2_), c3_, n3_, hof(c3_, n3_));
-                                        if (choice <= 2) {
-                                            link(cl, c0_, n0_, hof(c0_, n0_), c1_, n1_, hof(c1_, n1_));
-                                            link(K, cl, cl, sheight[cl - c0], cr, cr, sheight[cr - c0]);
-                                        } else {
-                                            link(cl, c1_, n1_, hof(c1_, n1_), cr, cr, sheight[cr - c0]);
-                                            link(K, c0_, n0_, hof(c0_, n0_), cl, cl, sheight[cl - c0]);
-                                        }
-                                    }
-                                }
-                            }
-                            if (choice < 0) link(K, cl, ncl, hcl, cr, ncr, hcr);
-                            h = sheight[K - c0];
-                        } else {
-                            const int32_t cl = L == gp ? ~gp : gp, cr = R == gp + 1 ? ~(gp + 1) : gp + 1;
-                            schild[K - c0] = make_int2(cl, cr);
-                            stage_parent(cl, K);
-                            stage_parent(cr, K);
-                            snbox[K - c0] = u;
-                        }
-                        if (o.all_boxes || root) box_store(o.nodebox + 2 * (int64_t)K, u, kTreelet ? h : 0);
-                        if (kTreelet && root) *o.wneed = (unsigned int)(h + 1 + 3);
-                        wl[(round + 1) & 1][atomicAdd(&wn[round + 1], 1)] = make_int2(L, R);
+                        next = make_int4(left ? l : other, left ? other : r, gp, 0);
+                        push = true;
                     }
                 }
             }
         }
+        append_item(wl[(round + 1) & 1], &wn[round + 1], push, next);
         __syncthreads();
         count = wn[round + 1];
     }
@@ -1479,40 +1497,45 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : (
         }
     }
     // write the staged nodes out, node K = c0 + t by thread t (coalesced rows, holes where a node
-    // spans the chunk boundary: k_lbvh_top writes those)
-    if (t < cnt) {
-        const int K = c0 + t;
-        const int2 ch = schild[t];
-        if (ch.x != kNone) {
-            o.child[K] = ch;
-            o.range[K] = srange[t];
-            int32_t r0, r1;
-            if constexpr (kTreelet) {
-                const int4 rf = sref[t];
-                r0 = rf.z, r1 = rf.w;
-            } else {
-                auto nref = [&](int32_t c) -> int32_t {
-                    if (c < 0) return make_leaf(~c, 1);
-                    const int2 rg = srange[c - c0];
-                    const int count = rg.y - rg.x + 1;
-                    return count <= o.leaf_size ? make_leaf(rg.x, count) : c;
-                };
-                r0 = nref(ch.x), r1 = nref(ch.y);
+    // spans the chunk boundary: the levels above write those)
+    auto write_out = [&]() {
+        if (t < cnt) {
+            const int K = c0 + t;
+            const int2 ch = schild[t];
+            if (ch.x != kNone) {
+                o.child[K] = ch;
+                o.range[K] = srange[t];
+                int32_t r0, r1;
+                if constexpr (kTreelet) {
+                    const int4 rf = sref[t];
+                    r0 = rf.z, r1 = rf.w;
+                } else {
+                    auto nref = [&](int32_t c) -> int32_t {
+                        if (c < 0) return make_leaf(~c, 1);
+                        const int2 rg = srange[c - c0];
+                        const int count = rg.y - rg.x + 1;
+                        return count <= o.leaf_size ? make_leaf(rg.x, count) : c;
+                    };
+                    r0 = nref(ch.x), r1 = nref(ch.y);
+                }
+                const Box6 a = ch.x >= 0 ? snbox[ch.x - c0] : slbox[~ch.x - c0];
+                const Box6 b = ch.y >= 0 ? snbox[ch.y - c0] : slbox[~ch.y - c0];
+                Node64 nd;
+                nd.a = make_float4(a.lx, a.hx, a.ly, a.hy);
+                nd.b = make_float4(b.lx, b.hx, b.ly, b.hy);
+                nd.c = make_float4(a.lz, a.hz, b.lz, b.hz);
+                nd.d = make_int4(r0, r1, 0, 0);
+                o.nodes[K] = nd;
             }
-            const Box6 a = ch.x >= 0 ? snbox[ch.x - c0] : slbox[~ch.x - c0];
-            const Box6 b = ch.y >= 0 ? snbox[ch.y - c0] : slbox[~ch.y - c0];
-            Node64 nd;
-            nd.a = make_float4(a.lx, a.hx, a.ly, a.hy);
-            nd.b = make_float4(b.lx, b.hx, b.ly, b.hy);
-            nd.c = make_float4(a.lz, a.hz, b.lz, b.hz);
-            nd.d = make_int4(r0, r1, 0, 0);
-            o.nodes[K] = nd;
+            if (spar_int[t] != kNone) o.parent[K] = spar_int[t];
+            if (spar_leaf[t] != kNone) o.parent[(n - 1) + K] = spar_leaf[t];
         }
-        if (spar_int[t] != kNone) o.parent[K] = spar_int[t];
-        if (spar_leaf[t] != kNone) o.parent[(n - 1) + K] = spar_leaf[t];
+    };
+    if (up.nlev <= 1) {  // a single chunk: the root completed here
+        write_out();
+        return;
     }
-    if (up.nlev <= 1) return;  // a single chunk: the root completed here
-    __syncthreads();           // smark complete
+    __syncthreads();  // smark complete
     // the chunk's units in leaf order; position p = leaf c0 + p; a node [l, r] is stored at its
     // Karras index (r if a left child, l if a right child) - c0
     auto unit_of = [&](int p, int e) -> Unit {
@@ -1525,7 +1548,19 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : (
     };
     const bool force = (up.force_global & 1) || ((up.force_global & 2) && (blockIdx.x & 1));
     lbvh_emit<kTreelet>(o, keys, ks, up, 0, blockIdx.x, cnt, smark, S.swarp, unit_of, pend, pend_n, force);
-    lbvh_levels<kTreelet>(o, keys, ks, up, blockIdx.x, S, pend, pend_n);
+    // arrive at the group one level up (thread 0: release fence + counter) while the others write
+    // the staged nodes out
+    __shared__ int s_arr;
+    if (t == 0) {
+        const int group = blockIdx.x / kGroup, gsize = min(kGroup, up.nseg[0] - group * kGroup);
+        __threadfence();
+        s_arr = atomicAdd(up.ctr[1] + group, 1u) == (unsigned)(gsize - 1);
+        if (s_arr) up.ctr[1][group] = 0;
+    }
+    write_out();
+    __syncthreads();
+    if (!s_arr) return;
+    lbvh_levels<kTreelet>(o, keys, ks, up, blockIdx.x, S, pend, pend_n, true);
 }
 
 // The tree above the chunks: every pending node climbs through the global slots (all chunks' pending
