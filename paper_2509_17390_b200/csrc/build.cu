@@ -3,6 +3,10 @@
 //   prep     : triangle centroids (the Morton point) + exact scene box [o, o+L] (last-block reduce)
 //   morton   : Eq. 5 codes, b bits per axis, x lowest, + the all-pass digit histogram
 //   sort     : stable LSD radix sort (sort.cu), "radix sort run massively in parallel"
+//   lbvh     : DEFAULT width-2 path, one kernel (k_lbvh): leaf records + Eq. 6 tree + Eq. 7 boxes +
+//              node64, built bottom-up in shared memory per chunk of sorted leaves and by the last
+//              CTA of each group of chunks above them (see the k_lbvh section); the steps below
+//              are the path of the other node widths and of the restructuring passes:
 //   reorder  : triangle records (tri48) gathered into sorted (leaf) order
 //   karras   : Eq. 6 LCP-split binary radix tree, one thread per internal node,
 //              "bitwise operations ... without recursion"
@@ -1044,8 +1048,12 @@ struct LbvhSmem {
 constexpr int kUnitCap = 64;
 constexpr int kGroup = 8;
 constexpr int kMaxLevels = 8;
+// a unit's boundary LCPs delta(a - 1, a) and delta(b, b + 1) (-1..95), packed in Unit::m.w
+__host__ __device__ __forceinline__ int pack_deltas(int dl, int dr) { return (dl + 1) | (dr + 1) << 8; }
+__host__ __device__ __forceinline__ int unpack_dl(int w) { return (w & 0xFF) - 1; }
+__host__ __device__ __forceinline__ int unpack_dr(int w) { return ((w >> 8) & 0xFF) - 1; }
 struct Unit {
-    int4 m;  // (a, b, height, 0): leaves [a, b]
+    int4 m;  // (a, b, height, packed boundary deltas): leaves [a, b]
     float4 lo, hi;
 };
 struct UpPlan {
@@ -1101,7 +1109,7 @@ template <bool kTreelet>
 __device__ __forceinline__ void lbvh_push_global(const LbvhOut &o, const uint64_t *__restrict__ keys, int ks,
                                                  const Unit &u, int4 *pend, unsigned int *pend_n) {
     const int l = u.m.x, r = u.m.y;
-    const int dl = adj_delta(keys, o.n, l - 1, ks), dr = adj_delta(keys, o.n, r, ks);
+    const int dl = unpack_dl(u.m.w), dr = unpack_dr(u.m.w);
     float4 *dst = l == r ? o.leafbox + 2 * (int64_t)l : o.nodebox + 2 * (int64_t)(dr > dl ? r : l);
     dst[0] = make_float4(u.lo.x, u.lo.y, u.lo.z, __int_as_float(kTreelet ? trav_height(o, l, r, u.m.z) : 0));
     dst[1] = u.hi;
@@ -1203,8 +1211,8 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
             uab[t] = make_int2(u.m.x, u.m.y);
             uh[t] = u.m.z;
             ubox[t] = Box6{u.lo.x, u.lo.y, u.lo.z, u.hi.x, u.hi.y, u.hi.z};
-            sdelta[t] = adj_delta(keys, n, u.m.x - 1, ks);
-            if (t == m - 1) sdelta[m] = adj_delta(keys, n, u.m.y, ks);
+            sdelta[t] = unpack_dl(u.m.w);  // the unit's boundary LCPs travel with it
+            if (t == m - 1) sdelta[m] = unpack_dr(u.m.w);
         }
         __syncthreads();
         int count = m;
@@ -1274,7 +1282,7 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
             const int q = p == e ? p : (dr > dl ? e : p);
             const Box6 bx = p == e ? ubox[p] : nbox[q];
             const int hh = p == e ? uh[p] : (kTreelet ? nh[q] : 0);
-            return Unit{make_int4(uab[p].x, uab[e].y, hh, 0), make_float4(bx.lx, bx.ly, bx.lz, 0.f),
+            return Unit{make_int4(uab[p].x, uab[e].y, hh, pack_deltas(dl, dr)), make_float4(bx.lx, bx.ly, bx.lz, 0.f),
                         make_float4(bx.hx, bx.hy, bx.hz, 0.f)};
         };
         lbvh_emit<kTreelet>(o, keys, ks, up, lev, seg, m, smark, S.swarp, unit_of, pend, pend_n);
@@ -1336,14 +1344,18 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : F
     // a node is completed one round after its second child arrived (after the barrier), so the
     // children's boxes and records are visible without a fence; the exchange at the slot only has to
     // decide who is second
+    // leaf pairs (the node split at j covers exactly [j, j + 1]: delta(j, j + 1) exceeds both
+    // neighbours' deltas) are completed in round 0 by the left leaf's thread; the right leaf stays idle
+    const bool pair_split = t + 1 < cnt && sdelta[t + 1] > sdelta[t] && sdelta[t + 1] > sdelta[t + 2];
+    const bool pair_right = t >= 1 && t < cnt && sdelta[t] > sdelta[t - 1] && sdelta[t] > sdelta[t + 1];
     int count = cnt;
     for (int round = 0; count > 0; ++round) {
         int4 next = make_int4(0, 0, 0, 0);
         bool push = false;
-        if (t < count) {
+        if (t < count && !(round == 0 && pair_right)) {
             int l = j, r = j;
-            if (round > 0) {
-                const int4 e = wl[round & 1][t];  // (L, R, split)
+            if (round > 0 || pair_split) {
+                const int4 e = round > 0 ? wl[round & 1][t] : make_int4(j, j + 1, j, 0);  // (L, R, split)
                 const int L = e.x, R = e.y, gp = e.z;
                 int h = 0;
                 // both children: [L, gp] and [gp + 1, R]
@@ -1544,7 +1556,8 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : F
         const int q = l == r ? p : (dr > dl ? e : p);
         const Box6 bx = l == r ? slbox[p] : snbox[q];
         const int hh = (kTreelet && l != r) ? sheight[q] : 0;
-        return Unit{make_int4(l, r, hh, 0), make_float4(bx.lx, bx.ly, bx.lz, 0.f), make_float4(bx.hx, bx.hy, bx.hz, 0.f)};
+        return Unit{make_int4(l, r, hh, pack_deltas(dl, dr)), make_float4(bx.lx, bx.ly, bx.lz, 0.f),
+                    make_float4(bx.hx, bx.hy, bx.hz, 0.f)};
     };
     const bool force = (up.force_global & 1) || ((up.force_global & 2) && (blockIdx.x & 1));
     lbvh_emit<kTreelet>(o, keys, ks, up, 0, blockIdx.x, cnt, smark, S.swarp, unit_of, pend, pend_n, force);
