@@ -1047,6 +1047,7 @@ struct LbvhSmem {
 // global slots), and everything above it follows ("poisoned"), so both paths never meet in one node.
 constexpr int kUnitCap = 64;
 constexpr int kGroup = 8;
+static_assert(kGroup <= 32, "one warp reads a group's segment counts");
 constexpr int kMaxLevels = 8;
 // a unit's boundary LCPs delta(a - 1, a) and delta(b, b + 1) (-1..95), packed in Unit::m.w
 __host__ __device__ __forceinline__ int pack_deltas(int dl, int dr) { return (dl + 1) | (dr + 1) << 8; }
@@ -1169,16 +1170,21 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
         if (t == 0) __threadfence();  // acquire the group's segments (the barrier below spreads it)
         __syncthreads();
         seg = group;
-        if (t == 0) {
-            int off = 0, poison = 0;
-            for (int k = 0; k < gsize; ++k) {
-                const int c = __ldcg(up.cnt[lev - 1] + first + k);
-                s_off[k] = off;
-                if (c < 0) poison = 1;
-                off += max(c, 0);
+        if (t < 32) {  // the segments' counts in parallel (one L2 round trip), prefix by shuffles
+            const int c = t < gsize ? __ldcg(up.cnt[lev - 1] + first + t) : 0;
+            int x = max(c, 0);
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, d);
+                if (t >= d) x += y;
             }
-            s_off[gsize] = off;
-            s_poison = poison || off > kChunk || ((up.force_global & 4) && (group & 1));
+            if (t < gsize) s_off[t] = x - max(c, 0);
+            const bool poison = __any_sync(0xffffffffu, c < 0);
+            const int off = __shfl_sync(0xffffffffu, x, 31);
+            if (t == 0) {
+                s_off[gsize] = off;
+                s_poison = poison || off > kChunk || ((up.force_global & 4) && (group & 1));
+            }
         }
         __syncthreads();
         const int m = s_off[gsize];
