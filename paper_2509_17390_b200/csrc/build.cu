@@ -1046,7 +1046,10 @@ struct LbvhSmem {
 // kChunk) sends its units to the global pending list instead (k_lbvh_top climbs those through the
 // global slots), and everything above it follows ("poisoned"), so both paths never meet in one node.
 constexpr int kUnitCap = 64;
-constexpr int kGroup = 8;
+#ifndef FGL_LBVH_GROUP
+#define FGL_LBVH_GROUP 16  // 8: one level more (C2 +11 us), 4: C2 +22 us and too many levels at 10 M
+#endif
+constexpr int kGroup = FGL_LBVH_GROUP;
 static_assert(kGroup <= 32, "one warp reads a group's segment counts");
 constexpr int kMaxLevels = 8;
 // a unit's boundary LCPs delta(a - 1, a) and delta(b, b + 1) (-1..95), packed in Unit::m.w
