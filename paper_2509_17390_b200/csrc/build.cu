@@ -870,6 +870,9 @@ __global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const i
 #ifndef FGL_LBVH_CHUNK
 #define FGL_LBVH_CHUNK 256
 #endif
+#ifndef FGL_TREELET_MIN
+#define FGL_TREELET_MIN 1  // in-build treelets: only at nodes over at least this many leaves
+#endif
 #ifndef FGL_LBVH_MINB
 #define FGL_LBVH_MINB (1536 / FGL_LBVH_CHUNK)  // resident CTAs per SM the register budget is sized for
 #endif
@@ -1047,7 +1050,7 @@ struct LbvhSmem {
 // global slots), and everything above it follows ("poisoned"), so both paths never meet in one node.
 constexpr int kUnitCap = 64;
 #ifndef FGL_LBVH_GROUP
-#define FGL_LBVH_GROUP 16  // 8: one level more (C2 +11 us), 4: C2 +22 us and too many levels at 10 M
+#define FGL_LBVH_GROUP 16  // max chunks per group; 16 below 2^22 leaves, 8 above (where 16 overflows)
 #endif
 constexpr int kGroup = FGL_LBVH_GROUP;
 static_assert(kGroup <= 32, "one warp reads a group's segment counts");
@@ -1066,6 +1069,7 @@ struct UpPlan {
     unsigned int *ctr[kMaxLevels];    // level i >= 1, per group: arrivals of its level i-1 segments
     int nseg[kMaxLevels];
     int nlev;                         // nseg[nlev - 1] == 1
+    int G;                            // segments per group (<= kGroup)
     int force_global;                 // test hook FGL_LBVH_GLOBAL: 1 = every chunk's units go to the global
                                       // list, 2 = every odd chunk's, 4 = every odd group's (levels >= 1)
 };
@@ -1073,11 +1077,14 @@ struct UpPlan {
 // segment counts per level and the carve-up of BuildBuffers::lbvh_up (bytes: lbvh_up_bytes)
 static UpPlan lbvh_plan(int64_t T, void *base) {
     UpPlan up{};
+    // 16-chunk groups save a level (~10 us of tail each); at 10 M triangles their ~17 units per
+    // chunk overflow a 256-unit group, so large trees use 8
+    up.G = T < (int64_t(1) << 22) ? kGroup : kGroup / 2;
     up.nseg[0] = (int)((T + kChunk - 1) / kChunk);
     up.nlev = 1;
     while (up.nseg[up.nlev - 1] > 1) {
         if (up.nlev == kMaxLevels) throw Error(1, "lbvh: too many levels");
-        up.nseg[up.nlev] = (up.nseg[up.nlev - 1] + kGroup - 1) / kGroup;
+        up.nseg[up.nlev] = (up.nseg[up.nlev - 1] + up.G - 1) / up.G;
         ++up.nlev;
     }
     char *p = static_cast<char *>(base);
@@ -1159,7 +1166,7 @@ __device__ void lbvh_levels(const LbvhOut &o, const uint64_t *__restrict__ keys,
     __shared__ int s_last, s_off[kGroup + 1], s_poison;
     const int t = threadIdx.x, n = o.n;
     for (int lev = 1; lev < up.nlev; ++lev) {
-        const int group = seg / kGroup, first = group * kGroup, gsize = min(kGroup, up.nseg[lev - 1] - first);
+        const int group = seg / up.G, first = group * up.G, gsize = min(up.G, up.nseg[lev - 1] - first);
         if (!(lev == 1 && arrived)) {  // (level 1: the caller arrived already, as the last of its group)
             __syncthreads();  // this segment's units / count written (by several threads)
             if (t == 0) {
@@ -1398,7 +1405,7 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : F
                     auto sel4 = [](int i, int v0, int v1, int v2, int v3) { return i == 0 ? v0 : (i == 1 ? v1 : (i == 2 ? v2 : v3)); };
                     int choice = -1;  // -1: keep the Karras topology
                     int xc0 = 0, xc1 = 0, xc2 = 0, xc3 = 0, xn0 = 0, xn1 = 0, xn2 = 0, xn3 = 0;
-                    if (ia || ib) {
+                    if ((ia || ib) && R - L + 1 >= FGL_TREELET_MIN) {  // small subtrees: little SAH to gain
                         // treelet leaves: x0, x1 under the left child (or the left child), x2, x3 likewise
                         const int4 ra = ia ? sref[cl - c0] : make_int4(cl, cl, ncl, ncl);
                         const int4 rb = ib ? sref[cr - c0] : make_int4(cr, cr, ncr, ncr);
@@ -1574,7 +1581,7 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : F
     // the staged nodes out
     __shared__ int s_arr;
     if (t == 0) {
-        const int group = blockIdx.x / kGroup, gsize = min(kGroup, up.nseg[0] - group * kGroup);
+        const int group = blockIdx.x / up.G, gsize = min(up.G, up.nseg[0] - group * up.G);
         __threadfence();
         s_arr = atomicAdd(up.ctr[1] + group, 1u) == (unsigned)(gsize - 1);
         if (s_arr) up.ctr[1][group] = 0;
