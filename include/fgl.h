@@ -129,7 +129,10 @@ FGL_API fgl_status fgl_scene_upload_mesh(fgl_scene *scene, const float *verts, i
 /* LBVH build, §IV-A, on the device, enqueued on `cuda_stream`:
  * centroids + scene box -> Morton codes (Eq. 5) -> stable LSD radix sort -> Karras radix tree
  * (Eq. 6) -> bottom-up refit (Eq. 7) -> triangle records reordered into leaf order -> traversal
- * nodes. opts may be NULL (defaults). Does no host synchronisation. */
+ * nodes. For width 2 (the default) the last four steps are one kernel that builds the tree and
+ * its Eq. 7 boxes bottom-up (the same tree, child links, ranges and nodes, bit for bit). opts may
+ * be NULL (defaults). Does no host synchronisation; graph-capturable (every replay rebuilds,
+ * also over new vertex data of the same size). */
 FGL_API fgl_status fgl_scene_build(fgl_scene *scene, const fgl_build_opts *opts, void *cuda_stream);
 
 /* Synchronises `cuda_stream` and returns FGL_E_DATA if the last upload failed validation. */
