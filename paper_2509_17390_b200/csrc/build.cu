@@ -1487,7 +1487,14 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : F
                             }
                         }
                     }
-                    if (choice < 0) link(K, cl, ncl, hcl, cr, ncr, hcr);
+                    if (choice < 0) {  // the Karras pair stays: its boxes are in registers already
+                        schild[K - c0] = make_int2(cl, cr);
+                        stage_parent(cl, K);
+                        stage_parent(cr, K);
+                        sref[K - c0] = make_int4(cl, cr, ncl, ncr);
+                        snbox[K - c0] = u;
+                        sheight[K - c0] = 1 + max(hcl, hcr);
+                    }
                     h = sheight[K - c0];
                 } else {
                     const int32_t cl = L == gp ? ~gp : gp, cr = R == gp + 1 ? ~(gp + 1) : gp + 1;
