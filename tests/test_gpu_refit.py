@@ -238,3 +238,11 @@ def test_treelets_rooms_same_hits_fewer_nodes(fgl):
     fresh = fgl.Scene(v2, m.tris)
     c1, c2 = ts.cast(poses, pat), fresh.cast(poses, pat)
     assert (c1["tri_id"] == c2["tri_id"]).float().mean().item() > 0.9999
+
+
+def test_treelets_option_errors(fgl):
+    m = synth.scene_c1()
+    for kw in (dict(treelets=2), dict(treelets=1, width=4), dict(treelets=1, restructure=-2)):
+        with pytest.raises(fgl.FglError) as e:
+            fgl.Scene(m.verts, m.tris, **kw)
+        assert e.value.status == 1, kw
