@@ -212,11 +212,34 @@ __device__ __forceinline__ float slab(const Pre &p, float lx, float hx, float ly
 // the persistent cast's test (constants from precompute_dyn: t_near / t_far are lower / upper
 // bounds of the exact plane distances, so no factor on t_far); hit flag and entry distance
 // returned separately (no +inf materialisation)
+#ifndef FGL_FFMA2
+#define FFMA2_DEFAULT 1
+#define FGL_FFMA2 FFMA2_DEFAULT  // slab planes in pairs: one FFMA2 (two IEEE fmas, sm_100) per axis
+#endif
+// (fma(lo, I, c_lo), fma(hi, I, c_hi)) — the two planes of one axis in one FFMA2 (fma.rn.f32x2: two
+// independent round-to-nearest fmas, bit-identical to two fmaf; I broadcast). The node's lo / hi
+// of an axis are adjacent floats (node64 layout), and so are the ray's constants (Pre).
+__device__ __forceinline__ void plane_pair(float lo, float hi, float I, float clo, float chi, float &tlo, float &thi) {
+#if FGL_FFMA2
+    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %4};\n\t"
+        "mov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(tlo), "=f"(thi)
+        : "f"(lo), "f"(hi), "f"(I), "f"(clo), "f"(chi));
+#else
+    tlo = fmaf(lo, I, clo), thi = fmaf(hi, I, chi);
+#endif
+}
+
 __device__ __forceinline__ bool slab_hit(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
                                          float tmin, float tmax, float &tn_out) {
-    const float ax = fmaf(lx, p.Ix, p.clx), bx = fmaf(hx, p.Ix, p.chx);
-    const float ay = fmaf(ly, p.Iy, p.cly), by = fmaf(hy, p.Iy, p.chy);
-    const float az = fmaf(lz, p.Iz, p.clz), bz = fmaf(hz, p.Iz, p.chz);
+    float ax, bx, ay, by, az, bz;
+    plane_pair(lx, hx, p.Ix, p.clx, p.chx, ax, bx);
+    plane_pair(ly, hy, p.Iy, p.cly, p.chy, ay, by);
+    plane_pair(lz, hz, p.Iz, p.clz, p.chz, az, bz);
     const float tn = fmaxf(fmaxf(fminf(ax, bx), fminf(ay, by)), fmaxf(fminf(az, bz), tmin));
     const float tf = fminf(fminf(fmaxf(ax, bx), fmaxf(ay, by)), fminf(fmaxf(az, bz), tmax));
     tn_out = tn;
@@ -232,9 +255,13 @@ template <int OCT>
 __device__ __forceinline__ bool slab_oct(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
                                          float tmin, float tmax, float &tn_out) {
     constexpr bool sx = OCT & 1, sy = OCT & 2, sz = OCT & 4;
-    const float nx = fmaf(sx ? hx : lx, p.Ix, sx ? p.chx : p.clx), fx = fmaf(sx ? lx : hx, p.Ix, sx ? p.clx : p.chx);
-    const float ny = fmaf(sy ? hy : ly, p.Iy, sy ? p.chy : p.cly), fy = fmaf(sy ? ly : hy, p.Iy, sy ? p.cly : p.chy);
-    const float nz = fmaf(sz ? hz : lz, p.Iz, sz ? p.chz : p.clz), fz = fmaf(sz ? lz : hz, p.Iz, sz ? p.clz : p.chz);
+    float tlx, thx, tly, thy, tlz, thz;
+    plane_pair(lx, hx, p.Ix, p.clx, p.chx, tlx, thx);
+    plane_pair(ly, hy, p.Iy, p.cly, p.chy, tly, thy);
+    plane_pair(lz, hz, p.Iz, p.clz, p.chz, tlz, thz);
+    const float nx = sx ? thx : tlx, fx = sx ? tlx : thx;
+    const float ny = sy ? thy : tly, fy = sy ? tly : thy;
+    const float nz = sz ? thz : tlz, fz = sz ? tlz : thz;
     const float tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, tmin));
     const float tf = fminf(fminf(fx, fy), fminf(fz, tmax));
     tn_out = tn;
