@@ -141,8 +141,63 @@ struct V3 {
 
 // Sheared coordinates of a vertex relative to the ray origin: (A_kx - Sx A_kz, A_ky - Sy A_kz, Sz A_kz)
 // with A = v - o (two roundings per coordinate, the same for every triangle sharing the vertex).
+#ifndef FGL_FFMA2
+#define FGL_FFMA2 1  // paired FP32 math (FFMA2 / FMUL2 / FADD2, sm_100): slab planes, shear, edge products
+#endif
+// (fma(lo, I, c_lo), fma(hi, I, c_hi)) — the two planes of one axis in one FFMA2 (fma.rn.f32x2: two
+// independent round-to-nearest fmas, bit-identical to two fmaf; I broadcast). The node's lo / hi
+// of an axis are adjacent floats (node64 layout), and so are the ray's constants (Pre).
+__device__ __forceinline__ void plane_pair(float lo, float hi, float I, float clo, float chi, float &tlo, float &thi) {
+#if FGL_FFMA2
+    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %4};\n\t"
+        "mov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(tlo), "=f"(thi)
+        : "f"(lo), "f"(hi), "f"(I), "f"(clo), "f"(chi));
+#else
+    tlo = fmaf(lo, I, clo), thi = fmaf(hi, I, chi);
+#endif
+}
+
+// (a0 * b0, a1 * b1) and (a0 + b0, a1 + b1), each lane of the pair rounded to nearest (FMUL2 /
+// FADD2: bit-identical to two __fmul_rn / __fadd_rn, never contracted)
+#ifndef FGL_PAIR_LEAF
+#define FGL_PAIR_LEAF 0  // 1: FMUL2 / FADD2 in the leaf test too (measured -4.6%: the pairs force spills at 48 registers)
+#endif
+__device__ __forceinline__ void mul_pair(float a0, float a1, float b0, float b1, float &r0, float &r1) {
+#if FGL_FFMA2 && FGL_PAIR_LEAF
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "mul.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(r0), "=f"(r1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+#else
+    r0 = __fmul_rn(a0, b0), r1 = __fmul_rn(a1, b1);
+#endif
+}
+__device__ __forceinline__ void sub_pair(float a0, float a1, float b0, float b1, float &r0, float &r1) {
+#if FGL_FFMA2 && FGL_PAIR_LEAF
+    asm("{.reg .b64 ra, rb, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\t"
+        "mov.b64 {%0, %1}, rd;}"
+        : "=f"(r0), "=f"(r1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+#else
+    r0 = __fsub_rn(a0, b0), r1 = __fsub_rn(a1, b1);
+#endif
+}
+
 __device__ __forceinline__ V3 shear(const Pre &p, float4 v) {
-    const float X = v.x - p.ox, Y = v.y - p.oy, Z = v.z - p.oz;
+    float X, Y;
+    sub_pair(v.x, v.y, p.ox, p.oy, X, Y);
+    const float Z = v.z - p.oz;
     // (A_kx, A_ky, A_kz) is the cyclic rotation of (X, Y, Z) that ends on kz, by branch-free selects.
     // The swap of kx and ky for d_kz < 0 in Woop et al. only orients the winding: it negates U, V, W,
     // T and det exactly (IEEE negation is exact), so a two-sided test returns the same t without it.
@@ -160,9 +215,13 @@ __device__ __forceinline__ V3 shear(const Pre &p, float4 v) {
 __device__ __forceinline__ bool hit_tri(const Pre &p, float4 a, float4 b, float4 c, float tmin, float best_t,
                                         int32_t best_id, int32_t id, float &t_out) {
     const V3 A = shear(p, a), B = shear(p, b), C = shear(p, c);
-    float U = __fsub_rn(__fmul_rn(C.x, B.y), __fmul_rn(C.y, B.x));
-    float V = __fsub_rn(__fmul_rn(A.x, C.y), __fmul_rn(A.y, C.x));
-    float W = __fsub_rn(__fmul_rn(B.x, A.y), __fmul_rn(B.y, A.x));
+    float u0, u1, v0, v1, w0, w1;
+    mul_pair(C.x, C.y, B.y, B.x, u0, u1);
+    mul_pair(A.x, A.y, C.y, C.x, v0, v1);
+    mul_pair(B.x, B.y, A.y, A.x, w0, w1);
+    float U = __fsub_rn(u0, u1);
+    float V = __fsub_rn(v0, v1);
+    float W = __fsub_rn(w0, w1);
     if ((U < 0.f || V < 0.f || W < 0.f) && (U > 0.f || V > 0.f || W > 0.f)) return false;
     if (U == 0.f || V == 0.f || W == 0.f) {
         const double Ud = (double)C.x * (double)B.y - (double)C.y * (double)B.x;
@@ -212,28 +271,6 @@ __device__ __forceinline__ float slab(const Pre &p, float lx, float hx, float ly
 // the persistent cast's test (constants from precompute_dyn: t_near / t_far are lower / upper
 // bounds of the exact plane distances, so no factor on t_far); hit flag and entry distance
 // returned separately (no +inf materialisation)
-#ifndef FGL_FFMA2
-#define FFMA2_DEFAULT 1
-#define FGL_FFMA2 FFMA2_DEFAULT  // slab planes in pairs: one FFMA2 (two IEEE fmas, sm_100) per axis
-#endif
-// (fma(lo, I, c_lo), fma(hi, I, c_hi)) — the two planes of one axis in one FFMA2 (fma.rn.f32x2: two
-// independent round-to-nearest fmas, bit-identical to two fmaf; I broadcast). The node's lo / hi
-// of an axis are adjacent floats (node64 layout), and so are the ray's constants (Pre).
-__device__ __forceinline__ void plane_pair(float lo, float hi, float I, float clo, float chi, float &tlo, float &thi) {
-#if FGL_FFMA2
-    asm("{.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\t"
-        "mov.b64 rb, {%4, %4};\n\t"
-        "mov.b64 rc, {%5, %6};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
-        "mov.b64 {%0, %1}, rd;}"
-        : "=f"(tlo), "=f"(thi)
-        : "f"(lo), "f"(hi), "f"(I), "f"(clo), "f"(chi));
-#else
-    tlo = fmaf(lo, I, clo), thi = fmaf(hi, I, chi);
-#endif
-}
-
 __device__ __forceinline__ bool slab_hit(const Pre &p, float lx, float hx, float ly, float hy, float lz, float hz,
                                          float tmin, float tmax, float &tn_out) {
     float ax, bx, ay, by, az, bz;
