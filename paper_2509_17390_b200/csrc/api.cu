@@ -113,7 +113,7 @@ void alloc_build(fgl_scene *s, int64_t T) {
     dalloc(s, &b.sort_tiles, 16);
     dalloc(s, &b.sort_rts, (size_t)256 * fgl::sort_tile_blocks(T));
     FGL_CUDA(cudaMemset(b.sort_tiles, 0, 16 * sizeof(uint32_t)));  // tile counters + device sort epoch
-    dalloc(s, &b.tri, 3 * T);
+    dalloc(s, &b.tri, (size_t)fgl::kTriStride * T);  // also the Gaussian records (3 float4 each)
     dalloc(s, &b.child, nin);
     dalloc(s, &b.range, nin);
     dalloc(s, &b.parent, 2 * T);
@@ -889,7 +889,17 @@ fgl_status fgl_scene_export(const fgl_scene *s, const fgl_export *out, void *str
                     out->node_box[6 * j + i] = (&f[2 * j].x)[i], out->node_box[6 * j + 3 + i] = (&f[2 * j + 1].x)[i];
         }
     }
-    cp(out->tri48, b.tri, 3 * T * sizeof(float4));
+    if (out->tri48 && T) {  // the export format is the 48-byte record; drop the pad of 64-byte ones
+        if (fgl::kTriStride == 3 || s->gauss) {
+            cp(out->tri48, b.tri, 3 * T * sizeof(float4));
+        } else {
+            std::vector<float4> tmp((size_t)fgl::kTriStride * T);
+            cp(tmp.data(), b.tri, tmp.size() * sizeof(float4));
+            float4 *o = reinterpret_cast<float4 *>(out->tri48);
+            for (int64_t j = 0; j < T; ++j)
+                for (int q = 0; q < 3; ++q) o[3 * j + q] = tmp[(size_t)fgl::kTriStride * j + q];
+        }
+    }
     cp(out->nodes, b.nodes, std::max<int64_t>(nin, 1) * sizeof(fgl::Node64));
     cp(out->nodes4, b.nodes4, std::max<int64_t>(nin, 1) * sizeof(fgl::Node128));
     cp(out->depth, b.depth, nin * sizeof(int32_t));

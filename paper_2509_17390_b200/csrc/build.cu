@@ -801,9 +801,9 @@ __global__ void __launch_bounds__(256) k_reorder(const float *__restrict__ verts
         const float3 a = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k), V)),
                      b = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 1), V)),
                      c = ldv(verts, clampv(__ldg(tris + 3 * (int64_t)k + 2), V));
-        tri[3 * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
-        tri[3 * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
-        tri[3 * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
+        tri[kTriStride * j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
+        tri[kTriStride * j + 1] = make_float4(b.x, b.y, b.z, 0.f);
+        tri[kTriStride * j + 2] = make_float4(c.x, c.y, c.z, 0.f);
         lo = make_float4(fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)), 0.f);
         hi = make_float4(fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z)), 0.f);
         leafbox[2 * j] = lo;
@@ -1351,9 +1351,9 @@ __global__ void __launch_bounds__(kChunk, kTreelet ? (kChunk <= 256 ? 4 : 2) : F
         const uint32_t k = perm ? __ldg(perm + j) : (uint32_t)(key & pmask);
         const int3 ti = ldtri(tris, (int64_t)k);
         const float3 a = ldv2(verts, clampv(ti.x, V)), b = ldv2(verts, clampv(ti.y, V)), c = ldv2(verts, clampv(ti.z, V));
-        tri[3 * (int64_t)j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
-        tri[3 * (int64_t)j + 1] = make_float4(b.x, b.y, b.z, 0.f);
-        tri[3 * (int64_t)j + 2] = make_float4(c.x, c.y, c.z, 0.f);
+        tri[kTriStride * (int64_t)j] = make_float4(a.x, a.y, a.z, __int_as_float((int32_t)k));
+        tri[kTriStride * (int64_t)j + 1] = make_float4(b.x, b.y, b.z, 0.f);
+        tri[kTriStride * (int64_t)j + 2] = make_float4(c.x, c.y, c.z, 0.f);
         box = Box6{fminf(a.x, fminf(b.x, c.x)), fminf(a.y, fminf(b.y, c.y)), fminf(a.z, fminf(b.z, c.z)),
                    fmaxf(a.x, fmaxf(b.x, c.x)), fmaxf(a.y, fmaxf(b.y, c.y)), fmaxf(a.z, fmaxf(b.z, c.z))};
         slbox[t] = box;

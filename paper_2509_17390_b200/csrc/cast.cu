@@ -372,7 +372,7 @@ __device__ __forceinline__ Hit trace(const SceneView &sv, const Ray &r, float tm
             const int32_t v = ~leaf;
             const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
             for (int32_t k = first; k < first + cnt; ++k) {
-                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 *tp = sv.tri + kTriStride * (int64_t)k;
                 const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
                 const int32_t id = __float_as_int(a.w);
                 if (kCount) ++h.tris;
@@ -454,7 +454,7 @@ __device__ __forceinline__ Hit trace4(const SceneView &sv, const Ray &r, float t
             const int32_t v = ~leaf;
             const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
             for (int32_t k = first; k < first + cnt; ++k) {
-                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 *tp = sv.tri + kTriStride * (int64_t)k;
                 const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
                 const int32_t id = __float_as_int(a.w);
                 if (kCount) ++h.tris;
@@ -548,7 +548,7 @@ __device__ __forceinline__ Hit trace4q(const SceneView &sv, const Ray &r, float 
             const int32_t v = ~leaf;
             const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
             for (int32_t k = first; k < first + cnt; ++k) {
-                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 *tp = sv.tri + kTriStride * (int64_t)k;
                 const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
                 const int32_t id = __float_as_int(a.w);
                 if (kCount) ++h.tris;
@@ -616,7 +616,7 @@ __device__ __forceinline__ Hit trace_packet(const SceneView &sv, const Ray &r, f
             const int32_t v = ~cur;
             const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
             for (int32_t k = first; k < first + cnt; ++k) {
-                const float4 *tp = sv.tri + 3 * (int64_t)k;
+                const float4 *tp = sv.tri + kTriStride * (int64_t)k;
                 const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
                 const int32_t id = __float_as_int(a.w);
                 if (kCount) ++h.tris;
@@ -1045,8 +1045,8 @@ __device__ __forceinline__ void descend(const Node64 *__restrict__ nodes, const 
             if (nd.x >= 0) prefetch_l1(nodes + nd.x);
             if (nd.y >= 0) prefetch_l1(nodes + nd.y);
 #if FGL_PREFETCH > 1
-            if (nd.x < 0 && nd.x != kEmptyRef) prefetch_l1(tri + 3 * (int64_t)((~nd.x) >> kLeafShift));
-            if (nd.y < 0 && nd.y != kEmptyRef) prefetch_l1(tri + 3 * (int64_t)((~nd.y) >> kLeafShift));
+            if (nd.x < 0 && nd.x != kEmptyRef) prefetch_l1(tri + kTriStride * (int64_t)((~nd.x) >> kLeafShift));
+            if (nd.y < 0 && nd.y != kEmptyRef) prefetch_l1(tri + kTriStride * (int64_t)((~nd.y) >> kLeafShift));
 #endif
 #endif
             if (kCount) ++h.nodes;
@@ -1098,8 +1098,16 @@ __device__ __forceinline__ void leaves(const float4 *__restrict__ tri, const Pre
         const int32_t v = ~leaf;
         const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
         for (int32_t k = first; k < first + cnt; ++k) {
-            const float4 *tp = tri + 3 * (int64_t)k;
-            const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+            const float4 *tp = tri + kTriStride * (int64_t)k;
+            float4 a, b, c;
+            if constexpr (kTriStride == 4) {  // 64-byte records: one 256-bit + one 128-bit load
+                asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                    : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                    : "l"(tp));
+                c = __ldg(tp + 2);
+            } else {
+                a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+            }
             const int32_t id = __float_as_int(a.w);
             if (kCount) ++h.tris;
             float t;

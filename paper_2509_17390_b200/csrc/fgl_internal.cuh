@@ -75,6 +75,12 @@ struct __align__(32) Node8 {
     uint4 c0b, c1a, c1b;
     int4 ref0, ref1;
 };
+// triangle records in leaf order: kTriStride float4 per triangle ({v0, id}, {v1, 0}, {v2, 0}[, pad]);
+// 4 makes each record 64-byte aligned so a leaf test fetches it with one 256-bit + one 128-bit load
+#ifndef FGL_TRI_STRIDE
+#define FGL_TRI_STRIDE 3
+#endif
+constexpr int kTriStride = FGL_TRI_STRIDE;
 constexpr float kFarBox = 3.0e38f;  // empty child: a degenerate box no ray with t <= t_max reaches
 constexpr int32_t kEmptyRef = INT32_MIN;
 constexpr int kLeafShift = 3;

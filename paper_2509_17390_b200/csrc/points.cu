@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(128) k_nearest(const Node64 *__restrict__ node
             const int32_t v = ~cur;
             const int32_t first = v >> kLeafShift, cnt = (v & (kMaxLeaf - 1)) + 1;
             for (int32_t k = first; k < first + cnt; ++k) {
-                const float4 p = __ldg(pts + 3 * (int64_t)k);  // tri48 record: v0 = the point, w = its index
+                const float4 p = __ldg(pts + kTriStride * (int64_t)k);  // tri48 record: v0 = the point, w = its index
                 const float dx = p.x - qx, dy = p.y - qy, dz = p.z - qz;
                 const float d2 = dx * dx + dy * dy + dz * dz;
                 const int32_t id = __float_as_int(p.w);
