@@ -129,19 +129,36 @@ __global__ void __launch_bounds__(256) k_prep(const float *__restrict__ verts, i
     if (threadIdx.x == 0) last = atomicAdd(sync, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
-    // last block: reduce all partials (L2 reads), publish the box, reset the counter
-    if (threadIdx.x < 32) {
-        for (int i = 0; i < 6; ++i) {
-            float v = i < 3 ? INFINITY : -INFINITY;
-            for (int b = lane; b < (int)gridDim.x; b += 32) {
-                float x = __ldcg(partial + b * 6 + i);
-                v = i < 3 ? fminf(v, x) : fmaxf(v, x);
+    // last block: reduce all partials (L2 reads, every thread's loads in flight at once — a single
+    // warp looping over them paid ~28 dependent L2 round trips per component, most of k_prep at 1 M
+    // triangles), publish the box, reset the counter
+    float r[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) r[i] = i < 3 ? INFINITY : -INFINITY;
+#pragma unroll
+    for (int q = 0; q < (kPrepBlocks + 255) / 256; ++q) {
+        const int b = threadIdx.x + q * (int)blockDim.x;
+        if (b < (int)gridDim.x) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const float x = __ldcg(partial + b * 6 + i);
+                r[i] = i < 3 ? fminf(r[i], x) : fmaxf(r[i], x);
             }
-            v = i < 3 ? warp_min(v) : warp_max(v);
-            if (lane == 0) box[i] = v;
         }
-        if (lane == 0) *sync = 0u, sync[2] = 0u, sync[3] += 1u;  // k_lbvh: [2] pending count, [3] slot epoch
     }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) r[i] = i < 3 ? warp_min(r[i]) : warp_max(r[i]);
+    __syncthreads();  // s is reused
+    if (lane == 0)
+        for (int i = 0; i < 6; ++i) s[w][i] = r[i];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[0][threadIdx.x];
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+            v = threadIdx.x < 3 ? fminf(v, s[ww][threadIdx.x]) : fmaxf(v, s[ww][threadIdx.x]);
+        box[threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) *sync = 0u, sync[2] = 0u, sync[3] += 1u;  // k_lbvh: [2] pending count, [3] slot epoch
 }
 
 // spread the low 21 bits of x to every third bit (bit i -> bit 3i)

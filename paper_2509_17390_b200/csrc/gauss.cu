@@ -75,18 +75,35 @@ __global__ void __launch_bounds__(256) k_gauss_prep(const float *__restrict__ mu
     if (threadIdx.x == 0) last = atomicAdd(sync, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
-    if (threadIdx.x < 32) {
-        for (int i = 0; i < 6; ++i) {
-            float v = i < 3 ? INFINITY : -INFINITY;
-            for (int b = lane; b < (int)gridDim.x; b += 32) {
+    // last block: every thread's partial loads in flight at once (one warp looping over them paid
+    // ~28 dependent L2 round trips per component), then warp and block reductions
+    float r[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i) r[i] = i < 3 ? INFINITY : -INFINITY;
+#pragma unroll
+    for (int qb = 0; qb < (kPrepBlocks + 255) / 256; ++qb) {
+        const int b = threadIdx.x + qb * (int)blockDim.x;
+        if (b < (int)gridDim.x) {
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
                 const float x = __ldcg(partial + b * 6 + i);
-                v = i < 3 ? fminf(v, x) : fmaxf(v, x);
+                r[i] = i < 3 ? fminf(r[i], x) : fmaxf(r[i], x);
             }
-            v = i < 3 ? wmin(v) : wmax(v);
-            if (lane == 0) box[i] = v;
         }
-        if (lane == 0) *sync = 0u;
     }
+#pragma unroll
+    for (int i = 0; i < 6; ++i) r[i] = i < 3 ? wmin(r[i]) : wmax(r[i]);
+    __syncthreads();  // s is reused
+    if (lane == 0)
+        for (int i = 0; i < 6; ++i) s[w][i] = r[i];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        float v = s[0][threadIdx.x];
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+            v = threadIdx.x < 3 ? fminf(v, s[ww][threadIdx.x]) : fmaxf(v, s[ww][threadIdx.x]);
+        box[threadIdx.x] = v;
+    }
+    if (threadIdx.x == 0) *sync = 0u;
 }
 
 // Leaf j = Gaussian k = perm(j): Eq. 4 box (outward: every rounding of R, |R| s and mu -+ r is
