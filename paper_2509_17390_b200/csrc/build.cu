@@ -887,6 +887,9 @@ __global__ void __launch_bounds__(256) k_nodes(int64_t n, int leaf_size, const i
 #ifndef FGL_LBVH_CHUNK
 #define FGL_LBVH_CHUNK 256
 #endif
+#ifndef FGL_MORTON_BLOCKS
+#define FGL_MORTON_BLOCKS (148 * 4)  // k_morton grid (each block adds its 8 x 256 digit counts to the global histogram)
+#endif
 #ifndef FGL_LBVH_ORDERED
 #define FGL_LBVH_ORDERED 0  // 1: round work lists in split order (ballot ranks) instead of atomic appends
                              // (measured: fewer bank conflicts but +32% instructions, C3 k_lbvh 0.73 -> 0.83 ms)
@@ -1859,7 +1862,7 @@ void launch_morton_sort(BuildBuffers &b, int bits, int cubic, cudaStream_t s) {
     while ((int64_t(1) << ib) < T) ++ib;
     const int ps = (FGL_SORT_PACKED && key_bits + ib <= 64) ? ib : 0;
     b.packed_shift = ps;
-    k_morton<<<grid_for(T, 256, 148 * 4), 256, 0, s>>>(b.cent, T, b.box, bits, cubic, b.keys[0], ps ? nullptr : b.vals[0],
+    k_morton<<<grid_for(T, 256, FGL_MORTON_BLOCKS), 256, 0, s>>>(b.cent, T, b.box, bits, cubic, b.keys[0], ps ? nullptr : b.vals[0],
                                                        ps, b.ghist);
     FGL_LAUNCHED("k_morton");
     int slot = 0;
