@@ -42,12 +42,25 @@ namespace {
 
 __global__ void k_validate(const float *__restrict__ verts, int64_t V, const int32_t *__restrict__ tris, int64_t T,
                            unsigned int *flag) {
+    // 16-byte loads over the (cudaMalloc-aligned, scene-owned) arrays, scalar tails
     unsigned int bad = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * T; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t x = tris[i];
-        if (x < 0 || x >= V) bad |= 1u;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nt4 = 3 * T / 4, nv4 = 3 * V / 4;
+    const int4 *t4 = reinterpret_cast<const int4 *>(tris);
+    const float4 *v4 = reinterpret_cast<const float4 *>(verts);
+    for (int64_t i = t0; i < nt4; i += stride) {
+        const int4 x = t4[i];
+        if ((unsigned)x.x >= (uint64_t)V || (unsigned)x.y >= (uint64_t)V || (unsigned)x.z >= (uint64_t)V ||
+            (unsigned)x.w >= (uint64_t)V)
+            bad |= 1u;
     }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 3 * V; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t i = 4 * nt4 + t0; i < 3 * T; i += stride)
+        if ((unsigned)tris[i] >= (uint64_t)V) bad |= 1u;
+    for (int64_t i = t0; i < nv4; i += stride) {
+        const float4 x = v4[i];
+        if (!(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w))) bad |= 2u;
+    }
+    for (int64_t i = 4 * nv4 + t0; i < 3 * V; i += stride)
         if (!isfinite(verts[i])) bad |= 2u;
     if (bad) atomicOr(flag, bad);
 }
@@ -1837,7 +1850,7 @@ inline int grid_for(int64_t n, int threads = 256, int max_blocks = 148 * 16) {
 void launch_validate(const float *verts, int64_t V, const int32_t *tris, int64_t T, unsigned int *flag,
                      cudaStream_t s) {
     FGL_CUDA(cudaMemsetAsync(flag, 0, sizeof(unsigned int), s));
-    k_validate<<<grid_for(3 * std::max(T, V)), 256, 0, s>>>(verts, V, tris, T, flag);
+    k_validate<<<grid_for(3 * std::max(T, V) / 4 + 1), 256, 0, s>>>(verts, V, tris, T, flag);
     FGL_LAUNCHED("k_validate");
 }
 

@@ -296,6 +296,28 @@ def test_error_reporting(fgl):
         s.cast_rays(np.zeros((1, 3), np.float32), np.ones((1, 3), np.float32), 1.0, 0.5)
 
 
+@pytest.mark.parametrize("where", [0, 1, 2, 500, 1000])
+def test_validation_finds_bad_entries_anywhere(fgl, where):
+    """The upload check reads the index and vertex arrays 16 bytes at a time with scalar tails: a
+    bad index or a non-finite coordinate must be found at any position (vector body or tail)."""
+    m = synth.soup(1001, seed=2)
+    tris = m.tris.copy()
+    tris.reshape(-1)[3 * where + (where % 3)] = m.verts.shape[0] + where  # out of range
+    with pytest.raises(fgl.FglError) as e:
+        fgl.Scene(m.verts, tris)
+    assert e.value.status == 2
+    tris.reshape(-1)[3 * where + (where % 3)] = -1
+    with pytest.raises(fgl.FglError) as e:
+        fgl.Scene(m.verts, tris)
+    assert e.value.status == 2
+    verts = m.verts.copy()
+    verts.reshape(-1)[3 * where + 2 - (where % 3)] = np.inf
+    with pytest.raises(fgl.FglError) as e:
+        fgl.Scene(verts, m.tris)
+    assert e.value.status == 2
+    fgl.Scene(m.verts, m.tris)  # and the unmodified mesh passes
+
+
 def test_cast_to_host_pipelined_matches_cast(fgl):
     cfg = _cfg("C2", poses=8)
     s = _scene(fgl, cfg["mesh"])
